@@ -1,0 +1,137 @@
+/*
+ * mgrc_gpu.h — C-ABI of the B200 (sm_100a) compress / decompress path.
+ *
+ * Drop-in boundary for the reference's container API
+ * (/root/reference/proj/include/mgrc/container.hpp:66-83) and the CLI
+ * multiblock driver (tools/mgrc.cpp:363-542).  Plain pointers and sizes only;
+ * no CUDA or torch types.  Every entry point returns 0 on success or the
+ * reference's errc ordinal + 1 (error.hpp:11-31; MGRC_E_*), with the message
+ * available from mgrc_gpu_last_error() on the calling thread.  Buffers may be
+ * host or device (CUDA) pointers: residency is detected per call.
+ *
+ * There is no CPU fallback: without a usable CUDA device every compute entry
+ * point fails with MGRC_E_CUDA.  Header-only entry points (inspect, describe,
+ * plan_chunks) run on the host.
+ */
+#ifndef MGRC_GPU_H
+#define MGRC_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGRC_GPU_API __attribute__((visibility("default")))
+
+/* status codes: errc ordinal + 1 (error.hpp:11-31) */
+enum {
+  MGRC_OK = 0,
+  MGRC_E_INVALID_SHAPE = 1,
+  MGRC_E_TOO_MANY_DIMS = 2,
+  MGRC_E_LEVEL_OUT_OF_RANGE = 3,
+  MGRC_E_SHAPE_MISMATCH = 4,
+  MGRC_E_NON_FINITE_INPUT = 5,
+  MGRC_E_DEGENERATE_DATA = 6,
+  MGRC_E_OVERFLOW = 7,
+  MGRC_E_UNKNOWN_CODEC = 8,
+  MGRC_E_CORRUPT_STREAM = 9,
+  MGRC_E_BAD_MAGIC = 10,
+  MGRC_E_UNSUPPORTED_VERSION = 11,
+  MGRC_E_CHECKSUM_MISMATCH = 12,
+  MGRC_E_TOLERANCE_UNREACHABLE = 13,
+  MGRC_E_PLANE_COUNT_OUT_OF_RANGE = 14,
+  MGRC_E_UNSATISFIABLE_TOLERANCE = 15,
+  MGRC_E_INVALID_STATE = 16,
+  MGRC_E_PREFIX_VIOLATION = 17,
+  MGRC_E_BUDGET_TOO_SMALL = 18,
+  MGRC_E_IO_ERROR = 19,
+  MGRC_E_CUDA = 100,            /* CUDA runtime failure / no device */
+  MGRC_E_INVALID_ARGUMENT = 101 /* null pointer, buffer too small */
+};
+
+enum { MGRC_DTYPE_F32 = 0, MGRC_DTYPE_F64 = 1 };             /* container.hpp:18 */
+enum { MGRC_NORM_INF = 0, MGRC_NORM_S = 1 };                 /* error_control.hpp:15 */
+enum { MGRC_MODE_ABS = 0, MGRC_MODE_REL = 1 };               /* error_control.hpp:16 */
+enum { MGRC_CODEC_RAW = 0, MGRC_CODEC_VARINT = 1, MGRC_CODEC_HUFFMAN = 2 }; /* codec.hpp:14 */
+
+/* ContainerInfo (container.hpp:37-51); coordinates are not returned here. */
+typedef struct {
+  uint16_t version;
+  uint8_t constant_field, coords_present, dtype, ndims, nlevels, codec_id;
+  uint64_t shape[4];
+  uint8_t mode, norm;
+  double smoothness, tol;
+  double bin_widths[65];
+  uint64_t payload_len;
+  uint32_t checksum;
+  uint64_t header_size;
+} mgrc_container_info;
+
+/* Replaces mgrc::compress(span<const float|double>, TensorGrid, ErrorSpec,
+ * Codec, exec) — container.hpp:69-74.  `coords` is NULL (index coordinates,
+ * make_grid(shape), grid.cpp:56) or ndims pointers to per-axis coordinates
+ * (make_grid(shape, coords), grid.cpp:70).  *out is a host buffer owned by
+ * the caller (release with mgrc_gpu_free). */
+MGRC_GPU_API int mgrc_gpu_compress(const void* data, int dtype, int ndims, const uint64_t* shape,
+                                   const double* const* coords, double tol, int norm, double smoothness, int mode,
+                                   int codec, uint8_t** out, uint64_t* out_len);
+
+/* Same, writing the container into a caller buffer (host or device).  With
+ * dst == NULL only *out_len is produced (the container stays staged). */
+MGRC_GPU_API int mgrc_gpu_compress_to(const void* data, int dtype, int ndims, const uint64_t* shape,
+                                      const double* const* coords, double tol, int norm, double smoothness, int mode,
+                                      int codec, void* dst, uint64_t dst_capacity, uint64_t* out_len);
+
+/* Replaces mgrc::decompress(span<const uint8_t>, exec) — container.hpp:76-77.
+ * *out is a host buffer of prod(shape) floats (dtype f32) or doubles. */
+MGRC_GPU_API int mgrc_gpu_decompress(const uint8_t* in, uint64_t len, void** out, int* dtype, int* ndims,
+                                     uint64_t* shape);
+
+/* Same, into a caller buffer (host or device) of dst_capacity bytes. */
+MGRC_GPU_API int mgrc_gpu_decompress_into(const uint8_t* in, uint64_t len, void* dst, uint64_t dst_capacity,
+                                          int* dtype, int* ndims, uint64_t* shape);
+
+/* Replaces mgrc::inspect / mgrc::describe — container.hpp:79-83 (host only). */
+MGRC_GPU_API int mgrc_gpu_inspect(const uint8_t* in, uint64_t len, mgrc_container_info* info);
+MGRC_GPU_API int mgrc_gpu_describe(const uint8_t* in, uint64_t len, char** text);
+
+/* Replaces mgrc::plan_chunks (chunking.hpp:38-44).  ranges[(b*ndims + a)*2 +
+ * {0,1}] = [begin, end) of block b on axis a, row-major block order. */
+MGRC_GPU_API int mgrc_gpu_plan_chunks(int ndims, const uint64_t* shape, int dtype, uint64_t budget,
+                                      uint64_t* nblocks, uint64_t* ranges, uint64_t cap_blocks);
+
+/* The CLI's multiblock compress (tools/mgrc.cpp:363-484) on one GPU: global
+ * REL normalisation, per-block ABS compress with the block's coordinate
+ * slice, and the u32 count | u64 offsets | containers framing. */
+MGRC_GPU_API int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndims, const uint64_t* shape,
+                                           const double* const* coords, double tol, int norm, double smoothness,
+                                           int mode, int codec, uint64_t chunk_mem, uint8_t** out,
+                                           uint64_t* out_len);
+
+/* The CLI's multiblock decompress (tools/mgrc.cpp:490-542): offset
+ * validation, placement from the blocks' coordinate slices, decode. */
+MGRC_GPU_API int mgrc_gpu_decompress_chunked(const uint8_t* in, uint64_t len, void** out, int* dtype, int* ndims,
+                                             uint64_t* shape);
+
+/* Non-finite flag, min and max of an array (host or device) — the per-rank
+ * statistics of the multi-GPU driver's global REL normalisation. */
+MGRC_GPU_API int mgrc_gpu_field_stats(const void* data, int dtype, uint64_t n, double* min, double* max,
+                                      int* nonfinite);
+
+MGRC_GPU_API const char* mgrc_gpu_last_error(void);
+MGRC_GPU_API void mgrc_gpu_free(void* p);
+MGRC_GPU_API int mgrc_gpu_set_device(int device);
+/* Stream used by subsequent calls on this thread (a cudaStream_t; NULL = own stream). */
+MGRC_GPU_API int mgrc_gpu_set_stream(void* stream);
+/* Per-phase CUDA-event timing of the last call on this thread. */
+MGRC_GPU_API int mgrc_gpu_set_profiling(int on);
+MGRC_GPU_API int mgrc_gpu_profile_count(void);
+MGRC_GPU_API int mgrc_gpu_profile_entry(int i, const char** name, double* ms, double* bytes);
+MGRC_GPU_API const char* mgrc_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MGRC_GPU_H */

@@ -1,0 +1,349 @@
+"""B200-native (sm_100a) MGARD-style error-bounded compression.
+
+Python mirror of the reference's container API
+(``/root/reference/proj/include/mgrc/container.hpp:66-83``) over the C-ABI in
+``include/mgrc_gpu.h``.  All array work runs in the hand-written CUDA kernels
+of ``csrc/``; there is no CPU fallback — without the built library or a CUDA
+device every compute call raises.
+
+    grid  = make_grid((65, 65, 65))                       # grid.cpp:56
+    spec  = ErrorSpec(tol=1e-3, norm=Norm.inf, mode=Mode.rel)
+    blob  = compress(u, grid, spec, Codec.huffman)        # container.hpp:69-74
+    u_hat = decompress(blob)                              # container.hpp:76-77
+    print(describe(inspect(blob)))                        # container.hpp:79-83
+
+Arrays may be numpy arrays (host) or torch tensors (host or CUDA); CUDA
+inputs are compressed in place without a host round trip.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import ContainerInfoC, P
+
+__all__ = [
+    "Norm", "Mode", "Codec", "DType", "ErrorSpec", "TensorGrid", "ContainerInfo", "MgrcError", "make_grid",
+    "compress", "compress_to", "decompress", "decompress_into", "inspect", "describe", "plan_chunks",
+    "compress_chunked", "decompress_chunked", "field_stats", "set_device", "set_stream", "set_profiling",
+    "last_profile", "ERRC_NAMES",
+]
+
+
+class Norm(IntEnum):  # error_control.hpp:15
+    inf = 0
+    s = 1
+
+
+class Mode(IntEnum):  # error_control.hpp:16
+    abs = 0
+    rel = 1
+
+
+class Codec(IntEnum):  # codec.hpp:14
+    raw = 0
+    varint = 1
+    huffman = 2
+
+
+class DType(IntEnum):  # container.hpp:18
+    f32 = 0
+    f64 = 1
+
+
+ERRC_NAMES = [
+    "InvalidShape", "TooManyDims", "LevelOutOfRange", "ShapeMismatch", "NonFiniteInput", "DegenerateData",
+    "Overflow", "UnknownCodec", "CorruptStream", "BadMagic", "UnsupportedVersion", "ChecksumMismatch",
+    "ToleranceUnreachable", "PlaneCountOutOfRange", "UnsatisfiableTolerance", "InvalidState", "PrefixViolation",
+    "BudgetTooSmall", "IoError",
+]
+
+
+class MgrcError(RuntimeError):
+    """mgrc::error (error.hpp:34-47): ``code`` is the C-ABI status (errc ordinal + 1), ``name`` the errc name."""
+
+    def __init__(self, code: int, message: str):
+        self.code = code
+        if 1 <= code <= len(ERRC_NAMES):
+            self.name = ERRC_NAMES[code - 1]
+        else:
+            self.name = {100: "CudaError", 101: "InvalidArgument"}.get(code, f"E{code}")
+        super().__init__(message)
+
+
+@dataclass
+class ErrorSpec:  # error_control.hpp:19-24
+    tol: float = 0.0
+    norm: Norm = Norm.inf
+    smoothness: float = 0.0
+    mode: Mode = Mode.abs
+
+
+@dataclass
+class TensorGrid:  # grid.hpp:15-23
+    shape: tuple
+    coords: Optional[list] = None
+
+    @property
+    def explicit_coords(self) -> bool:
+        return self.coords is not None
+
+    def ndims(self) -> int:
+        return len(self.shape)
+
+    def element_count(self) -> int:
+        return int(np.prod(self.shape))
+
+
+@dataclass
+class ContainerInfo:  # container.hpp:37-51
+    version: int
+    constant_field: bool
+    coords_present: bool
+    dtype: DType
+    shape: tuple
+    spec: ErrorSpec
+    nlevels: int
+    bin_widths: list
+    codec_id: int
+    payload_len: int
+    checksum: int
+    header_size: int
+    raw: bytes = field(default=b"", repr=False)
+
+
+def make_grid(shape: Sequence[int], coords: Optional[Sequence[Sequence[float]]] = None) -> TensorGrid:
+    """make_grid (grid.cpp:56-98); validation happens in the library at compress time."""
+    return TensorGrid(tuple(int(s) for s in shape), None if coords is None else [np.asarray(c, np.float64)
+                                                                               for c in coords])
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise MgrcError(rc, _lib.lib().mgrc_gpu_last_error().decode(errors="replace"))
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _array_ptr(u):
+    """(pointer, dtype code, shape, keepalive) of a numpy array or torch tensor."""
+    if _is_torch(u):
+        import torch
+
+        if not u.is_contiguous():
+            u = u.contiguous()
+        if u.dtype == torch.float32:
+            dt = DType.f32
+        elif u.dtype == torch.float64:
+            dt = DType.f64
+        else:
+            raise TypeError(f"unsupported dtype {u.dtype}")
+        return u.data_ptr(), dt, tuple(u.shape), u
+    a = np.asarray(u)
+    if a.dtype == np.float32:
+        dt = DType.f32
+    elif a.dtype == np.float64:
+        dt = DType.f64
+    else:
+        raise TypeError(f"unsupported dtype {a.dtype} (f32 or f64)")
+    a = np.ascontiguousarray(a)
+    return a.ctypes.data, dt, a.shape, a
+
+
+def _bytes_ptr(blob):
+    if _is_torch(blob):
+        return blob.data_ptr(), blob.numel() * blob.element_size(), blob
+    if isinstance(blob, np.ndarray):
+        b = np.ascontiguousarray(blob).view(np.uint8)
+        return b.ctypes.data, b.nbytes, b
+    b = np.frombuffer(bytes(blob), dtype=np.uint8)
+    return b.ctypes.data, b.nbytes, b
+
+
+def _grid_args(grid: TensorGrid):
+    shape = np.asarray(grid.shape, dtype=np.uint64)
+    if grid.coords is None:
+        return shape, None, []
+    cs = [np.ascontiguousarray(c, dtype=np.float64) for c in grid.coords]
+    arr = (P * len(cs))(*[c.ctypes.data for c in cs])
+    return shape, arr, cs
+
+
+def compress(u, grid: Optional[TensorGrid] = None, spec: Optional[ErrorSpec] = None,
+             codec: Codec = Codec.huffman) -> bytes:
+    """mgrc::compress (container.hpp:69-74) on the GPU; returns the container bytes."""
+    ptr, dt, shape, keep = _array_ptr(u)
+    grid = grid or make_grid(shape)
+    spec = spec or ErrorSpec(tol=1e-3)
+    gshape, coords, ckeep = _grid_args(grid)
+    out = P()
+    n = C.c_uint64()
+    _check(_lib.lib().mgrc_gpu_compress(ptr, int(dt), len(gshape), gshape.ctypes.data, coords, spec.tol,
+                                        int(spec.norm), spec.smoothness, int(spec.mode), int(codec), C.byref(out),
+                                        C.byref(n)))
+    b = C.string_at(out, n.value)
+    _lib.lib().mgrc_gpu_free(out)
+    return b
+
+
+def compress_to(u, dst, grid: Optional[TensorGrid] = None, spec: Optional[ErrorSpec] = None,
+                codec: Codec = Codec.huffman) -> int:
+    """Compress into a caller buffer (host numpy / torch, or a CUDA torch uint8 tensor); returns the length.
+
+    With ``dst=None`` only the length is computed (the container stays staged on the device)."""
+    ptr, dt, shape, keep = _array_ptr(u)
+    grid = grid or make_grid(shape)
+    spec = spec or ErrorSpec(tol=1e-3)
+    gshape, coords, ckeep = _grid_args(grid)
+    if dst is None:
+        dptr, cap = None, 0
+    else:
+        dptr, cap, dkeep = _bytes_ptr(dst)
+    n = C.c_uint64()
+    _check(_lib.lib().mgrc_gpu_compress_to(ptr, int(dt), len(gshape), gshape.ctypes.data, coords, spec.tol,
+                                           int(spec.norm), spec.smoothness, int(spec.mode), int(codec), dptr, cap,
+                                           C.byref(n)))
+    return n.value
+
+
+def decompress(blob) -> np.ndarray:
+    """mgrc::decompress (container.hpp:76-77) on the GPU; returns a host numpy array."""
+    ptr, n, keep = _bytes_ptr(blob)
+    out = P()
+    dt = C.c_int()
+    nd = C.c_int()
+    shape = np.zeros(4, dtype=np.uint64)
+    _check(_lib.lib().mgrc_gpu_decompress(ptr, n, C.byref(out), C.byref(dt), C.byref(nd), shape.ctypes.data))
+    sh = tuple(int(s) for s in shape[: nd.value])
+    npdt = np.float32 if dt.value == 0 else np.float64
+    cnt = int(np.prod(sh))
+    arr = np.frombuffer(C.string_at(out, cnt * np.dtype(npdt).itemsize), dtype=npdt).reshape(sh).copy()
+    _lib.lib().mgrc_gpu_free(out)
+    return arr
+
+
+def decompress_into(blob, out) -> tuple:
+    """Decompress into a caller array (numpy or torch, host or CUDA); returns (dtype, shape)."""
+    ptr, n, keep = _bytes_ptr(blob)
+    if _is_torch(out):
+        optr, cap = out.data_ptr(), out.numel() * out.element_size()
+    else:
+        optr, cap = out.ctypes.data, out.nbytes
+    dt = C.c_int()
+    nd = C.c_int()
+    shape = np.zeros(4, dtype=np.uint64)
+    _check(_lib.lib().mgrc_gpu_decompress_into(ptr, n, optr, cap, C.byref(dt), C.byref(nd), shape.ctypes.data))
+    return DType(dt.value), tuple(int(s) for s in shape[: nd.value])
+
+
+def inspect(blob) -> ContainerInfo:
+    """mgrc::inspect (container.hpp:79-80): header-only parse (host)."""
+    b = bytes(blob) if not isinstance(blob, (bytes, bytearray)) else bytes(blob)
+    buf = np.frombuffer(b, dtype=np.uint8)
+    ci = ContainerInfoC()
+    _check(_lib.lib().mgrc_gpu_inspect(buf.ctypes.data, len(b), C.byref(ci)))
+    return ContainerInfo(
+        version=ci.version, constant_field=bool(ci.constant_field), coords_present=bool(ci.coords_present),
+        dtype=DType(ci.dtype), shape=tuple(int(ci.shape[a]) for a in range(ci.ndims)),
+        spec=ErrorSpec(ci.tol, Norm(ci.norm), ci.smoothness, Mode(ci.mode)), nlevels=ci.nlevels,
+        bin_widths=[ci.bin_widths[l] for l in range(ci.nlevels + 1)], codec_id=ci.codec_id,
+        payload_len=ci.payload_len, checksum=ci.checksum, header_size=ci.header_size, raw=b[: ci.header_size])
+
+
+def describe(info_or_blob) -> str:
+    """mgrc::describe (container.hpp:82-83): stable key:value text."""
+    raw = info_or_blob.raw if isinstance(info_or_blob, ContainerInfo) else bytes(info_or_blob)
+    buf = np.frombuffer(raw, dtype=np.uint8)
+    t = C.c_char_p()
+    _check(_lib.lib().mgrc_gpu_describe(buf.ctypes.data, len(raw), C.byref(t)))
+    s = t.value.decode()
+    _lib.lib().mgrc_gpu_free(C.cast(t, P))
+    return s
+
+
+def plan_chunks(shape: Sequence[int], dtype: DType, budget: int) -> np.ndarray:
+    """mgrc::plan_chunks (chunking.hpp:38-44): [nblocks, ndims, 2] ranges in block order."""
+    sh = np.asarray(shape, dtype=np.uint64)
+    nb = C.c_uint64()
+    _check(_lib.lib().mgrc_gpu_plan_chunks(len(sh), sh.ctypes.data, int(dtype), budget, C.byref(nb), None, 0))
+    out = np.zeros(int(nb.value) * len(sh) * 2, dtype=np.uint64)
+    _check(_lib.lib().mgrc_gpu_plan_chunks(len(sh), sh.ctypes.data, int(dtype), budget, C.byref(nb),
+                                           out.ctypes.data, nb.value))
+    return out.reshape(int(nb.value), len(sh), 2)
+
+
+def compress_chunked(u, spec: ErrorSpec, codec: Codec = Codec.huffman, chunk_mem: int = 0,
+                     coords=None) -> bytes:
+    """The CLI's multiblock compress (tools/mgrc.cpp:363-484) on one GPU."""
+    ptr, dt, shape, keep = _array_ptr(u)
+    grid = make_grid(shape, coords)
+    gshape, cs, ckeep = _grid_args(grid)
+    out = P()
+    n = C.c_uint64()
+    _check(_lib.lib().mgrc_gpu_compress_chunked(ptr, int(dt), len(gshape), gshape.ctypes.data, cs, spec.tol,
+                                                int(spec.norm), spec.smoothness, int(spec.mode), int(codec),
+                                                chunk_mem, C.byref(out), C.byref(n)))
+    b = C.string_at(out, n.value)
+    _lib.lib().mgrc_gpu_free(out)
+    return b
+
+
+def decompress_chunked(blob) -> np.ndarray:
+    """The CLI's multiblock decompress (tools/mgrc.cpp:490-542)."""
+    ptr, n, keep = _bytes_ptr(blob)
+    out = P()
+    dt = C.c_int()
+    nd = C.c_int()
+    shape = np.zeros(4, dtype=np.uint64)
+    _check(_lib.lib().mgrc_gpu_decompress_chunked(ptr, n, C.byref(out), C.byref(dt), C.byref(nd),
+                                                  shape.ctypes.data))
+    sh = tuple(int(s) for s in shape[: nd.value])
+    npdt = np.float32 if dt.value == 0 else np.float64
+    cnt = int(np.prod(sh))
+    arr = np.frombuffer(C.string_at(out, cnt * np.dtype(npdt).itemsize), dtype=npdt).reshape(sh).copy()
+    _lib.lib().mgrc_gpu_free(out)
+    return arr
+
+
+def field_stats(u) -> tuple:
+    """(min, max, nonfinite) of an array on the GPU."""
+    ptr, dt, shape, keep = _array_ptr(u)
+    mn = C.c_double()
+    mx = C.c_double()
+    nf = C.c_int()
+    _check(_lib.lib().mgrc_gpu_field_stats(ptr, int(dt), int(np.prod(shape)), C.byref(mn), C.byref(mx),
+                                           C.byref(nf)))
+    return mn.value, mx.value, bool(nf.value)
+
+
+def set_device(device: int) -> None:
+    _check(_lib.lib().mgrc_gpu_set_device(device))
+
+
+def set_stream(stream_handle: Optional[int]) -> None:
+    """Use a caller cudaStream_t (e.g. ``torch.cuda.current_stream().cuda_stream``) on this thread."""
+    _check(_lib.lib().mgrc_gpu_set_stream(stream_handle))
+
+
+def set_profiling(on: bool) -> None:
+    _check(_lib.lib().mgrc_gpu_set_profiling(1 if on else 0))
+
+
+def last_profile() -> list:
+    """[(phase, ms, algorithmic_bytes)] CUDA-event timings of the last call on this thread."""
+    L = _lib.lib()
+    out = []
+    for i in range(L.mgrc_gpu_profile_count()):
+        name = C.c_char_p()
+        ms = C.c_double()
+        by = C.c_double()
+        _check(L.mgrc_gpu_profile_entry(i, C.byref(name), C.byref(ms), C.byref(by)))
+        out.append((name.value.decode(), ms.value, by.value))
+    return out

@@ -1,0 +1,558 @@
+// extern "C" boundary (include/mgrc_gpu.h).  Exceptions never cross it: every
+// entry point maps mgrc_gpu::Error to its errc ordinal + 1 and keeps the
+// message in a thread-local slot, mirroring mgrc::error (error.hpp:34-47).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mgrc_gpu.h"
+#include "host.hpp"
+#include "pipeline.hpp"
+
+using namespace mgrc_gpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    g_last_error.clear();
+    return MGRC_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return static_cast<int>(e.code());
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return MGRC_E_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MGRC_E_CUDA;
+  }
+}
+
+void require(bool ok, const char* what) {
+  if (!ok) raise(Errc::invalid_argument, what);
+}
+
+DType to_dtype(int d) {
+  if (d != 0 && d != 1) raise(Errc::invalid_argument, "dtype must be 0 (f32) or 1 (f64)");
+  return static_cast<DType>(d);
+}
+
+ErrorSpec to_spec(double tol, int norm, double s, int mode) {
+  if (norm != 0 && norm != 1) raise(Errc::invalid_argument, "norm must be 0 (inf) or 1 (s)");
+  if (mode != 0 && mode != 1) raise(Errc::invalid_argument, "mode must be 0 (abs) or 1 (rel)");
+  ErrorSpec sp;
+  sp.tol = tol;
+  sp.norm = static_cast<Norm>(norm);
+  sp.smoothness = s;
+  sp.mode = static_cast<Mode>(mode);
+  return sp;
+}
+
+Codec to_codec(int c) {
+  if (c < 0 || c > 2) raise(Errc::unknown_codec, "codec " + std::to_string(c));
+  return static_cast<Codec>(c);
+}
+
+void ensure_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    raise(Errc::cuda, "no CUDA device available (the sm_100a path has no CPU fallback)");
+  }
+}
+
+// Writes a container (host head + device body + host tail) to dst (host or device).
+void emit_parts(Context& ctx, const ContainerParts& parts, uint8_t* dst, bool dst_dev) {
+  cudaStream_t s = context_stream(ctx);
+  const uint64_t h = parts.head.size();
+  if (dst_dev) {
+    if (h && cudaMemcpyAsync(dst, parts.head.data(), h, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      raise(Errc::cuda, "header copy failed");
+    if (parts.dev_len &&
+        cudaMemcpyAsync(dst + h, parts.dev, parts.dev_len, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      raise(Errc::cuda, "payload copy failed");
+    if (!parts.host_tail.empty() &&
+        cudaMemcpyAsync(dst + h + parts.dev_len, parts.host_tail.data(), parts.host_tail.size(),
+                        cudaMemcpyHostToDevice, s) != cudaSuccess)
+      raise(Errc::cuda, "tail copy failed");
+  } else {
+    std::memcpy(dst, parts.head.data(), h);
+    if (parts.dev_len &&
+        cudaMemcpyAsync(dst + h, parts.dev, parts.dev_len, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      raise(Errc::cuda, "payload copy failed");
+    if (!parts.host_tail.empty()) std::memcpy(dst + h + parts.dev_len, parts.host_tail.data(), parts.host_tail.size());
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess) raise(Errc::cuda, "stream synchronize failed");
+}
+
+Grid grid_from(int ndims, const uint64_t* shape, const double* const* coords) {
+  require(shape != nullptr, "shape is null");
+  if (ndims > kMaxDims) raise(Errc::too_many_dims, "grid has " + std::to_string(ndims) + " axes, max is 4");
+  return make_grid(ndims, shape, coords);
+}
+
+void fill_info(const ContainerInfo& ci, mgrc_container_info* info) {
+  std::memset(info, 0, sizeof *info);
+  info->version = ci.version;
+  info->constant_field = ci.constant_field;
+  info->coords_present = ci.coords_present;
+  info->dtype = static_cast<uint8_t>(ci.dtype);
+  info->ndims = static_cast<uint8_t>(ci.ndims);
+  info->nlevels = static_cast<uint8_t>(ci.nlevels);
+  info->codec_id = ci.codec_id;
+  for (int a = 0; a < ci.ndims; ++a) info->shape[a] = ci.shape[a];
+  info->mode = static_cast<uint8_t>(ci.spec.mode);
+  info->norm = static_cast<uint8_t>(ci.spec.norm);
+  info->smoothness = ci.spec.smoothness;
+  info->tol = ci.spec.tol;
+  for (size_t l = 0; l < ci.bin_widths.size() && l < 65; ++l) info->bin_widths[l] = ci.bin_widths[l];
+  info->payload_len = ci.payload_len;
+  info->checksum = ci.checksum;
+  info->header_size = ci.header_size;
+}
+
+// ---- multiblock framing (tools/mgrc.cpp:258-293) ----------------------------
+
+std::vector<std::pair<uint64_t, uint64_t>> split_multiblock(const uint8_t* f, uint64_t n) {
+  auto rd = [&](uint64_t at, int bytes) {
+    if (at + bytes > n) raise(Errc::corrupt_stream, "truncated stream");
+    uint64_t v = 0;
+    for (int i = bytes - 1; i >= 0; --i) v = (v << 8) | f[at + i];
+    return v;
+  };
+  const uint64_t count = rd(0, 4);
+  if (count == 0) raise(Errc::corrupt_stream, "no blocks");
+  const uint64_t hdr = 4 + 8 * count;
+  std::vector<uint64_t> off(count);
+  for (uint64_t i = 0; i < count; ++i) off[i] = rd(4 + 8 * i, 8);
+  std::vector<std::pair<uint64_t, uint64_t>> out(count);
+  for (uint64_t i = 0; i < count; ++i) {
+    const uint64_t b = off[i], e = i + 1 < count ? off[i + 1] : n;
+    if (b < hdr || e > n || b > e) raise(Errc::corrupt_stream, "bad block offsets");
+    out[i] = {b, e - b};
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mgrc_gpu_version(void) { return "mgrc_gpu 0.1 (sm_100a)"; }
+const char* mgrc_gpu_last_error(void) { return g_last_error.c_str(); }
+void mgrc_gpu_free(void* p) { std::free(p); }
+
+int mgrc_gpu_set_device(int device) {
+  return guarded([&] {
+    ensure_device();
+    if (cudaSetDevice(device) != cudaSuccess) raise(Errc::cuda, "cudaSetDevice failed");
+  });
+}
+
+int mgrc_gpu_set_stream(void* stream) {
+  return guarded([&] {
+    ensure_device();
+    Context& c = context_for_current_device();
+    if (stream) {
+      context_set_stream(c, static_cast<cudaStream_t>(stream));
+    } else {
+      cudaStream_t s;
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) raise(Errc::cuda, "stream create");
+      context_set_stream(c, s);
+    }
+  });
+}
+
+int mgrc_gpu_set_profiling(int on) {
+  return guarded([&] {
+    ensure_device();
+    context_set_profiling(context_for_current_device(), on != 0);
+  });
+}
+
+int mgrc_gpu_profile_count(void) {
+  int n = 0;
+  guarded([&] { n = static_cast<int>(context_profile(context_for_current_device()).size()); });
+  return n;
+}
+
+int mgrc_gpu_profile_entry(int i, const char** name, double* ms, double* bytes) {
+  return guarded([&] {
+    const auto& p = context_profile(context_for_current_device());
+    require(i >= 0 && i < static_cast<int>(p.size()), "profile index out of range");
+    *name = p[i].name.c_str();
+    *ms = p[i].ms;
+    *bytes = p[i].bytes;
+  });
+}
+
+int mgrc_gpu_compress_to(const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
+                         double tol, int norm, double smoothness, int mode, int codec, void* dst,
+                         uint64_t dst_capacity, uint64_t* out_len) {
+  return guarded([&] {
+    require(data != nullptr && out_len != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    const ErrorSpec sp = to_spec(tol, norm, smoothness, mode);
+    const Codec cd = to_codec(codec);
+    const DType dt = to_dtype(dtype);
+    ensure_device();
+    Context& ctx = context_for_current_device();
+    const ContainerParts parts = compress(ctx, data, dt, g, sp, cd);
+    *out_len = parts.total();
+    if (!dst) return;
+    if (dst_capacity < parts.total()) raise(Errc::invalid_argument, "destination buffer too small");
+    emit_parts(ctx, parts, static_cast<uint8_t*>(dst), is_device_pointer(dst));
+  });
+}
+
+int mgrc_gpu_compress(const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
+                      double tol, int norm, double smoothness, int mode, int codec, uint8_t** out,
+                      uint64_t* out_len) {
+  return guarded([&] {
+    require(data != nullptr && out != nullptr && out_len != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    const ErrorSpec sp = to_spec(tol, norm, smoothness, mode);
+    const Codec cd = to_codec(codec);
+    const DType dt = to_dtype(dtype);
+    ensure_device();
+    Context& ctx = context_for_current_device();
+    const ContainerParts parts = compress(ctx, data, dt, g, sp, cd);
+    uint8_t* buf = static_cast<uint8_t*>(std::malloc(parts.total() + 1));
+    if (!buf) throw std::bad_alloc();
+    try {
+      emit_parts(ctx, parts, buf, false);
+    } catch (...) {
+      std::free(buf);
+      throw;
+    }
+    *out = buf;
+    *out_len = parts.total();
+  });
+}
+
+int mgrc_gpu_decompress_into(const uint8_t* in, uint64_t len, void* dst, uint64_t dst_capacity, int* dtype,
+                             int* ndims, uint64_t* shape) {
+  return guarded([&] {
+    require(in != nullptr && dst != nullptr, "null argument");
+    ensure_device();
+    Context& ctx = context_for_current_device();
+    const DecodedInfo di = decompress_into(ctx, in, len, dst, dst_capacity);
+    if (dtype) *dtype = static_cast<int>(di.dtype);
+    if (ndims) *ndims = di.ndims;
+    if (shape)
+      for (int a = 0; a < di.ndims; ++a) shape[a] = di.shape[a];
+  });
+}
+
+int mgrc_gpu_decompress(const uint8_t* in, uint64_t len, void** out, int* dtype, int* ndims, uint64_t* shape) {
+  return guarded([&] {
+    require(in != nullptr && out != nullptr, "null argument");
+    ensure_device();
+    Context& ctx = context_for_current_device();
+    const ContainerInfo info = inspect_any(ctx, in, len);
+    uint64_t n = 1;
+    for (int a = 0; a < info.ndims; ++a) n *= info.shape[a];
+    const uint64_t bytes = n * dtype_size(info.dtype);
+    void* buf = std::malloc(bytes + 1);
+    if (!buf) throw std::bad_alloc();
+    try {
+      const DecodedInfo di = decompress_into(ctx, in, len, buf, bytes);
+      if (dtype) *dtype = static_cast<int>(di.dtype);
+      if (ndims) *ndims = di.ndims;
+      if (shape)
+        for (int a = 0; a < di.ndims; ++a) shape[a] = di.shape[a];
+    } catch (...) {
+      std::free(buf);
+      throw;
+    }
+    *out = buf;
+  });
+}
+
+int mgrc_gpu_inspect(const uint8_t* in, uint64_t len, mgrc_container_info* info) {
+  return guarded([&] {
+    require(in != nullptr && info != nullptr, "null argument");
+    fill_info(parse_header(in, len), info);
+  });
+}
+
+int mgrc_gpu_describe(const uint8_t* in, uint64_t len, char** text) {
+  return guarded([&] {
+    require(in != nullptr && text != nullptr, "null argument");
+    const std::string s = describe(parse_header(in, len));
+    char* t = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(t, s.c_str(), s.size() + 1);
+    *text = t;
+  });
+}
+
+int mgrc_gpu_plan_chunks(int ndims, const uint64_t* shape, int dtype, uint64_t budget, uint64_t* nblocks,
+                         uint64_t* ranges, uint64_t cap_blocks) {
+  return guarded([&] {
+    require(shape != nullptr && nblocks != nullptr, "null argument");
+    const ChunkPlan plan = plan_chunks(ndims, shape, to_dtype(dtype), budget);
+    *nblocks = plan.block_count();
+    if (ranges && plan.block_count() <= cap_blocks)
+      for (uint64_t b = 0; b < plan.block_count(); ++b) {
+        const auto r = plan.block(b);
+        for (int a = 0; a < ndims; ++a) {
+          ranges[(b * ndims + a) * 2] = r[a].begin;
+          ranges[(b * ndims + a) * 2 + 1] = r[a].end;
+        }
+      }
+  });
+}
+
+int mgrc_gpu_field_stats(const void* data, int dtype, uint64_t n, double* mn, double* mx, int* nonfinite) {
+  return guarded([&] {
+    require(data != nullptr && n > 0, "null argument");
+    ensure_device();
+    const FieldStats st = field_stats(context_for_current_device(), data, to_dtype(dtype), n);
+    if (mn) *mn = st.min;
+    if (mx) *mx = st.max;
+    if (nonfinite) *nonfinite = st.nonfinite;
+  });
+}
+
+// Multiblock compress on one GPU (tools/mgrc.cpp:363-484).  Blocks split only
+// along leading axes are contiguous sub-arrays and are compressed in place;
+// other blocks are gathered first.
+int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndims, const uint64_t* shape,
+                              const double* const* coords, double tol, int norm, double smoothness, int mode,
+                              int codec, uint64_t chunk_mem, uint8_t** out, uint64_t* out_len) {
+  return guarded([&] {
+    require(data != nullptr && out != nullptr && out_len != nullptr, "null argument");
+    const Grid whole = grid_from(ndims, shape, coords);
+    const DType dt = to_dtype(dtype);
+    const ErrorSpec spec = to_spec(tol, norm, smoothness, mode);
+    const Codec cd = to_codec(codec);
+    const ChunkPlan plan = plan_chunks(ndims, shape, dt, chunk_mem > 0 ? chunk_mem : UINT64_MAX);
+    const uint64_t nb = plan.block_count();
+    ensure_device();
+    Context& ctx = context_for_current_device();
+    const size_t unit = dtype_size(dt);
+    std::vector<std::vector<uint8_t>> blocks(nb);
+    if (nb == 1) {
+      const ContainerParts parts = compress(ctx, data, dt, whole, spec, cd);
+      blocks[0].resize(parts.total());
+      emit_parts(ctx, parts, blocks[0].data(), false);
+    } else {
+      ErrorSpec bspec = spec;
+      bspec.mode = Mode::abs;
+      const uint64_t count = whole.count();
+      if (spec.mode == Mode::rel) {  // global normalisation (tools/mgrc.cpp:405-418)
+        const FieldStats st = field_stats(ctx, data, dt, count);
+        if (st.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
+        double nrm = st.max - st.min;
+        if (spec.norm == Norm::s) {
+          // RMS over the whole array: 4096-block ordered sum (the CLI's scan is
+          // fully serial; this differs from it by rounding only).
+          std::vector<uint8_t> host;
+          const void* src = data;
+          double ss = 0.0;
+          if (is_device_pointer(data)) {
+            host.resize(count * unit);
+            if (cudaMemcpy(host.data(), data, count * unit, cudaMemcpyDeviceToHost) != cudaSuccess)
+              raise(Errc::cuda, "copy failed");
+            src = host.data();
+          }
+          for (uint64_t i = 0; i < count; ++i) {
+            const double v = dt == DType::f32 ? static_cast<double>(static_cast<const float*>(src)[i])
+                                              : static_cast<const double*>(src)[i];
+            ss += v * v;
+          }
+          nrm = std::sqrt(ss / static_cast<double>(count));
+        }
+        if (nrm == 0.0) raise(Errc::degenerate_data, "relative bound on a constant file");
+        bspec.tol = spec.tol * nrm;
+      }
+      const bool on_dev = is_device_pointer(data);
+      uint64_t stride[kMaxDims];
+      stride[ndims - 1] = 1;
+      for (int a = ndims - 1; a > 0; --a) stride[a - 1] = stride[a] * shape[a];
+      std::vector<uint8_t> gather;
+
+      for (uint64_t b = 0; b < nb; ++b) {
+        const auto rng = plan.block(b);
+        uint64_t bshape[kMaxDims];
+        std::vector<double> bc[kMaxDims];
+        const double* cptr[kMaxDims];
+        for (int a = 0; a < ndims; ++a) {
+          bshape[a] = rng[a].length();
+          bc[a].assign(whole.coords[a].begin() + rng[a].begin, whole.coords[a].begin() + rng[a].end);
+          cptr[a] = bc[a].data();
+        }
+        // contiguous iff all axes after the first partial one are whole
+        bool contiguous = true;
+        int first_partial = -1;
+        for (int a = 0; a < ndims; ++a)
+          if (bshape[a] != shape[a]) {
+            first_partial = a;
+            break;
+          }
+        for (int a = first_partial + 1; first_partial >= 0 && a < ndims; ++a)
+          if (bshape[a] != shape[a]) contiguous = false;
+        uint64_t origin = 0, bcount = 1;
+        for (int a = 0; a < ndims; ++a) {
+          origin += rng[a].begin * stride[a];
+          bcount *= bshape[a];
+        }
+        const void* bdata = static_cast<const uint8_t*>(data) + origin * unit;
+        if (!contiguous) {  // strided sub-box: gather rows
+          const uint64_t run = bshape[ndims - 1];
+          gather.resize(bcount * unit);
+          std::vector<uint64_t> pos(ndims, 0);
+          for (uint64_t row = 0; row < bcount / run; ++row) {
+            uint64_t off = rng[ndims - 1].begin;
+            for (int a = 0; a + 1 < ndims; ++a) off += (rng[a].begin + pos[a]) * stride[a];
+            const void* src = static_cast<const uint8_t*>(data) + off * unit;
+            if (on_dev) {
+              if (cudaMemcpy(gather.data() + row * run * unit, src, run * unit, cudaMemcpyDeviceToHost) !=
+                  cudaSuccess)
+                raise(Errc::cuda, "gather copy failed");
+            } else {
+              std::memcpy(gather.data() + row * run * unit, src, run * unit);
+            }
+            for (int a = ndims - 2; a >= 0; --a) {
+              if (++pos[a] < bshape[a]) break;
+              pos[a] = 0;
+            }
+          }
+          bdata = gather.data();
+        }
+
+        const Grid bg = make_grid(ndims, bshape, cptr);
+        const ContainerParts parts = compress(ctx, bdata, dt, bg, bspec, cd);
+        blocks[b].resize(parts.total());
+        emit_parts(ctx, parts, blocks[b].data(), false);
+      }
+    }
+    uint64_t total = 4 + 8 * nb;
+    for (const auto& b : blocks) total += b.size();
+    uint8_t* buf = static_cast<uint8_t*>(std::malloc(total));
+    uint64_t at = 0;
+    auto put = [&](uint64_t v, int bytes) {
+      for (int i = 0; i < bytes; ++i) buf[at++] = static_cast<uint8_t>(v >> (8 * i));
+    };
+    put(nb, 4);
+    uint64_t off = 4 + 8 * nb;
+    for (const auto& b : blocks) {
+      put(off, 8);
+      off += b.size();
+    }
+    for (const auto& b : blocks) {
+      std::memcpy(buf + at, b.data(), b.size());
+      at += b.size();
+    }
+    *out = buf;
+    *out_len = total;
+  });
+}
+
+// Multiblock decompress (tools/mgrc.cpp:490-542).
+int mgrc_gpu_decompress_chunked(const uint8_t* in, uint64_t len, void** out, int* dtype, int* ndims,
+                                uint64_t* shape) {
+  return guarded([&] {
+    require(in != nullptr && out != nullptr, "null argument");
+    ensure_device();
+    Context& ctx = context_for_current_device();
+    const auto blocks = split_multiblock(in, len);
+    std::vector<ContainerInfo> infos;
+    for (const auto& b : blocks) infos.push_back(parse_header(in + b.first, b.second));
+    const DType dt = infos[0].dtype;
+    for (const auto& i : infos)
+      if (i.dtype != dt) raise(Errc::corrupt_stream, "blocks disagree on dtype");
+    const int d = infos[0].ndims;
+    uint64_t gshape[kMaxDims] = {0, 0, 0, 0};
+    std::vector<std::vector<Range>> place(blocks.size());
+    if (blocks.size() == 1) {
+      for (int a = 0; a < d; ++a) {
+        gshape[a] = infos[0].shape[a];
+        place[0].push_back({0, gshape[a]});
+      }
+    } else {  // derive_placement (tools/mgrc.cpp:302-347)
+      for (int a = 0; a < d; ++a) {
+        std::vector<std::pair<double, uint64_t>> ranges;
+        for (const auto& info : infos) {
+          if (!info.coords_present || info.ndims != d)
+            raise(Errc::corrupt_stream, "multi-block container lacks placement coordinates");
+          const double start = info.coords[a][0];
+          const uint64_t l = info.shape[a];
+          bool found = false;
+          for (auto& r : ranges)
+            if (r.first == start) {
+              if (r.second != l) raise(Errc::corrupt_stream, "inconsistent block grid");
+              found = true;
+            }
+          if (!found) ranges.push_back({start, l});
+        }
+        std::sort(ranges.begin(), ranges.end());
+        uint64_t at = 0;
+        std::vector<std::pair<double, Range>> placed;
+        for (const auto& r : ranges) {
+          placed.push_back({r.first, {at, at + r.second}});
+          at += r.second;
+        }
+        gshape[a] = at;
+        for (size_t i = 0; i < infos.size(); ++i)
+          for (const auto& pr : placed)
+            if (pr.first == infos[i].coords[a][0]) {
+              place[i].push_back(pr.second);
+              break;
+            }
+        for (const auto& br : place)
+          if (static_cast<int>(br.size()) != a + 1) raise(Errc::corrupt_stream, "block placement failed");
+      }
+    }
+    uint64_t count = 1;
+    for (int a = 0; a < d; ++a) count *= gshape[a];
+    const size_t unit = dtype_size(dt);
+    uint8_t* buf = static_cast<uint8_t*>(std::malloc(count * unit + 1));
+    if (!buf) throw std::bad_alloc();
+    try {
+      uint64_t stride[kMaxDims];
+      stride[d - 1] = 1;
+      for (int a = d - 1; a > 0; --a) stride[a - 1] = stride[a] * gshape[a];
+      std::vector<uint8_t> tmp;
+      for (size_t b = 0; b < blocks.size(); ++b) {
+        const auto& r = place[b];
+        uint64_t bcount = 1;
+        for (int a = 0; a < d; ++a) bcount *= r[a].length();
+        tmp.resize(bcount * unit);
+        decompress_into(ctx, in + blocks[b].first, blocks[b].second, tmp.data(), tmp.size());
+        const uint64_t run = r[d - 1].length();
+        std::vector<uint64_t> pos(d, 0);
+        for (uint64_t row = 0; row < bcount / run; ++row) {  // write_block (tools/mgrc.cpp:148-190)
+          uint64_t off = r[d - 1].begin;
+          for (int a = 0; a + 1 < d; ++a) off += (r[a].begin + pos[a]) * stride[a];
+          std::memcpy(buf + off * unit, tmp.data() + row * run * unit, run * unit);
+          for (int a = d - 2; a >= 0; --a) {
+            if (++pos[a] < r[a].length()) break;
+            pos[a] = 0;
+          }
+        }
+      }
+    } catch (...) {
+      std::free(buf);
+      throw;
+    }
+    *out = buf;
+    if (dtype) *dtype = static_cast<int>(dt);
+    if (ndims) *ndims = d;
+    if (shape)
+      for (int a = 0; a < d; ++a) shape[a] = gshape[a];
+  });
+}
+
+}  // extern "C"

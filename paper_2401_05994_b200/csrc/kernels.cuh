@@ -1,0 +1,986 @@
+// sm_100a kernels for the compress / decompress hot path.
+//
+// Arithmetic contract: the reference computes in plain IEEE
+// double with no FMA contraction, and the order of the corner sum is part of
+// the result.  Every floating-point operation below is an explicit
+// round-to-nearest intrinsic (__dmul_rn / __dadd_rn / __dsub_rn / __ddiv_rn)
+// in the reference's order, and the TU is additionally compiled with
+// --fmad=false.  f32 data is widened to f64 on load (container.cpp:197-203).
+//
+// Layout: arrays are row-major, last axis fastest (grid.hpp:12-13).  Per-axis
+// tables (level of each index, bracketing neighbours, weights) are tiny and
+// live in L1/L2; the array traffic is streamed with 16-byte vector accesses.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mgrc_gpu {
+namespace dev {
+
+constexpr int kMaxL = 64;
+
+struct AxisTab {
+  const uint8_t* lvl;
+  const uint32_t* left;
+  const uint32_t* right;
+  const double* wl;
+  const double* wr;
+};
+
+struct GridDev {
+  int d, L;
+  uint32_t shape[4];
+  uint64_t stride[4];
+  uint64_t N;
+  AxisTab ax[4];
+};
+
+struct BoxDev {  // level-l box: the tensor product of the level-l index sets
+  const uint32_t* set[4];
+  uint32_t n[4];
+  uint64_t count;
+};
+
+struct Widths {
+  double w[kMaxL];
+};
+
+__device__ __forceinline__ uint64_t zigzag(long long q) {
+  return (static_cast<uint64_t>(q) << 1) ^ static_cast<uint64_t>(q >> 63);
+}
+__device__ __forceinline__ long long unzigzag(uint64_t z) {
+  return static_cast<long long>(z >> 1) ^ -static_cast<long long>(z & 1u);
+}
+
+// Order-preserving key of a double (for atomicMin/Max on min/max).
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  const unsigned long long b = __double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// ---------------------------------------------------------------------------
+// Multilinear corner interpolation of one node (transform.cpp:102-128).
+// Fresh axes are the axes whose index is new at `tag`; corners are visited in
+// binary order with bit k selecting the right neighbour of the k-th fresh
+// axis (ascending axis order), w = Π w_axis starting from 1.0, and the sum
+// starts at 0.0 and accumulates w·v.  Submasks of the fresh mask enumerated
+// with s = (s - F) & F come out in exactly that increasing order.
+template <int D, class Load>
+__device__ __forceinline__ double interp(const GridDev& g, const uint32_t (&i)[4], int tag, Load load) {
+  uint32_t F = 0;
+  uint64_t base = 0;
+  double wl[D], wr[D];
+  uint64_t ol[D], orr[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    wl[a] = wr[a] = 0.0;
+    ol[a] = orr[a] = 0;
+    if (__ldg(g.ax[a].lvl + i[a]) == tag) {
+      F |= 1u << a;
+      wl[a] = __ldg(g.ax[a].wl + i[a]);
+      wr[a] = __ldg(g.ax[a].wr + i[a]);
+      ol[a] = static_cast<uint64_t>(__ldg(g.ax[a].left + i[a])) * g.stride[a];
+      orr[a] = static_cast<uint64_t>(__ldg(g.ax[a].right + i[a])) * g.stride[a];
+    } else {
+      base += static_cast<uint64_t>(i[a]) * g.stride[a];
+    }
+  }
+  double acc = 0.0;
+  uint32_t s = 0;
+  do {
+    double w = 1.0;
+    uint64_t off = base;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+      if ((F >> a) & 1u) {
+        const bool right = (s >> a) & 1u;
+        w = __dmul_rn(w, right ? wr[a] : wl[a]);
+        off += right ? orr[a] : ol[a];
+      }
+    acc = __dadd_rn(acc, __dmul_rn(w, load(off)));
+    s = (s - F) & F;
+  } while (s);
+  return acc;
+}
+
+template <int D>
+__device__ __forceinline__ int node_tag(const GridDev& g, const uint32_t (&i)[4]) {
+  int t = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) t = max(t, static_cast<int>(__ldg(g.ax[a].lvl + i[a])));
+  return t;
+}
+
+template <int D>
+__device__ __forceinline__ void decompose(const GridDev& g, uint64_t e, uint32_t (&i)[4]) {
+#pragma unroll
+  for (int a = D - 1; a > 0; --a) {
+    const uint64_t q = e / g.shape[a];
+    i[a] = static_cast<uint32_t>(e - q * g.shape[a]);
+    e = q;
+  }
+  i[0] = static_cast<uint32_t>(e);
+}
+
+template <int D>
+__device__ __forceinline__ void advance(const GridDev& g, uint32_t (&i)[4]) {
+#pragma unroll
+  for (int a = D - 1; a >= 0; --a) {
+    if (++i[a] < g.shape[a]) return;
+    i[a] = 0;
+  }
+}
+
+// 4-element vector load/store helpers (16-byte transactions).
+template <typename T>
+__device__ __forceinline__ void load4(const T* p, double (&v)[4]);
+template <>
+__device__ __forceinline__ void load4<float>(const float* p, double (&v)[4]) {
+  const float4 x = __ldg(reinterpret_cast<const float4*>(p));
+  v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+}
+template <>
+__device__ __forceinline__ void load4<double>(const double* p, double (&v)[4]) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+}
+__device__ __forceinline__ void store4(double* p, const double (&v)[4]) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+  reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+}
+__device__ __forceinline__ void store4(float* p, const double (&v)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(__double2float_rn(v[0]), __double2float_rn(v[1]),
+                                              __double2float_rn(v[2]), __double2float_rn(v[3]));
+}
+template <typename Z>
+__device__ __forceinline__ void load4z(const Z* p, uint64_t (&z)[4]);
+template <>
+__device__ __forceinline__ void load4z<uint32_t>(const uint32_t* p, uint64_t (&z)[4]) {
+  const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+  z[0] = x.x, z[1] = x.y, z[2] = x.z, z[3] = x.w;
+}
+template <>
+__device__ __forceinline__ void load4z<unsigned long long>(const unsigned long long* p, uint64_t (&z)[4]) {
+  const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
+  const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+  z[0] = a.x, z[1] = a.y, z[2] = b.x, z[3] = b.y;
+}
+__device__ __forceinline__ void store4z(uint32_t* p, const uint64_t (&z)[4]) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(static_cast<uint32_t>(z[0]), static_cast<uint32_t>(z[1]),
+                                            static_cast<uint32_t>(z[2]), static_cast<uint32_t>(z[3]));
+}
+__device__ __forceinline__ void store4z(unsigned long long* p, const uint64_t (&z)[4]) {
+  reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(z[0], z[1]);
+  reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(z[2], z[3]);
+}
+
+// ---------------------------------------------------------------------------
+// K1: input statistics (exec.cpp:89-128): non-finite flag, min, max.
+// min/max are order-independent; the constant-field value the reference
+// stores (the last 4096-block's first element, see pipeline) is read apart.
+
+struct Stats {
+  unsigned long long min_key, max_key;
+  unsigned int nonfinite;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_stats(const T* __restrict__ u, uint64_t n, Stats* out, int vec_ok) {
+  double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+  unsigned bad = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t n4 = vec_ok ? n / 4 : 0;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n4; k += stride) {
+    double v[4];
+    load4<T>(u + 4 * k, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      bad |= !isfinite(v[j]);
+      mn = fmin(mn, v[j]);
+      mx = fmax(mx, v[j]);
+    }
+  }
+  for (uint64_t k = 4 * n4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += stride) {
+    const double v = static_cast<double>(u[k]);
+    bad |= !isfinite(v);
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  unsigned long long kmn = dkey(mn), kmx = dkey(mx);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+    kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&out->min_key, kmn);
+    atomicMax(&out->max_key, kmx);
+    if (bad) atomicOr(&out->nonfinite, 1u);
+  }
+}
+
+// Exact 4096-block sums of squares (exec.cpp:47-71, :108-117): one thread
+// per block, serial in index order, no FMA.  Partials are combined serially
+// on the host, exactly as blocked_reduce does.
+template <typename T>
+__global__ void __launch_bounds__(128) k_block_sumsq(const T* __restrict__ v, uint64_t n, double* __restrict__ partials,
+                                                     int vec_ok) {
+  const uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t nb = (n + 4095) / 4096;
+  if (b >= nb) return;
+  const uint64_t lo = b * 4096, hi = min(lo + 4096, n);
+  double s = 0.0;
+  uint64_t i = lo;
+  if (hi - lo == 4096 && vec_ok) {
+    for (; i < hi; i += 4) {
+      double x[4];
+      load4<T>(v + i, x);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s = __dadd_rn(s, __dmul_rn(x[j], x[j]));
+    }
+  }
+  for (; i < hi; ++i) {
+    const double x = static_cast<double>(v[i]);
+    s = __dadd_rn(s, __dmul_rn(x, x));
+  }
+  partials[b] = s;
+}
+
+// ---------------------------------------------------------------------------
+// K2: fused forward transform + level-wise quantisation + varint-byte
+// histogram.  One pass over the original array: the forward sweep only ever
+// reads coarse nodes that the sweep has not yet modified (transform.cpp:65-67,
+// L→1), so c(node) = u(node) − I(u)(node) with the node's own tag
+// (SURVEY §0.3).  Quantisation follows quantize.cpp:105-123.
+//   zz[n]   zigzag(q)            (Z = u32 with a "wide" flag, or u64)
+//   r[n]    c − q·δ              (residual, for the a-posteriori check)
+//   hist    256-bin counts of the LEB128 bytes of zz (codec.cpp:445-449)
+struct QuantFlags {
+  unsigned long long overflow;  // |c/δ| ≥ 2^63 (quantize.cpp:113-116)
+  unsigned int wide;            // some zz does not fit the u32 store
+};
+
+__device__ __forceinline__ void hist_flush(uint32_t* sh, uint32_t& sym, uint32_t& cnt) {
+  if (cnt) atomicAdd(&sh[sym], cnt);
+  cnt = 0;
+}
+
+__device__ __forceinline__ void hist_varint(uint32_t* sh, uint64_t z, uint32_t& sym, uint32_t& cnt) {
+  for (;;) {
+    const uint32_t b = z >= 0x80 ? static_cast<uint32_t>((z & 0x7F) | 0x80) : static_cast<uint32_t>(z);
+    if (b != sym) {
+      hist_flush(sh, sym, cnt);
+      sym = b;
+    }
+    ++cnt;
+    if (z < 0x80) return;
+    z >>= 7;
+  }
+}
+
+template <int D, typename T, typename Z>
+__global__ void __launch_bounds__(256) k_forward_quant(GridDev g, Widths W, const T* __restrict__ u,
+                                                       Z* __restrict__ zz, double* __restrict__ r,
+                                                       unsigned long long* __restrict__ hist, QuantFlags* flags,
+                                                       int vec_ok) {
+  __shared__ uint32_t sh[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
+  __syncthreads();
+  uint32_t hsym = 0, hcnt = 0;
+  unsigned long long ovf = 0;
+  unsigned wide = 0;
+  auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
+  const uint64_t nruns = (g.N + 3) / 4;
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t run = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; run < nruns; run += step) {
+    const uint64_t e0 = run * 4;
+    const int cnt = static_cast<int>(umin64(4, g.N - e0));
+    uint32_t i[4] = {0, 0, 0, 0};
+    decompose<D>(g, e0, i);
+    double cv[4] = {0, 0, 0, 0};
+    if (cnt == 4 && vec_ok) {
+      load4<T>(u + e0, cv);
+    } else {
+      for (int k = 0; k < cnt; ++k) cv[k] = static_cast<double>(u[e0 + k]);
+    }
+    uint64_t zv[4] = {0, 0, 0, 0};
+    double rv[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < cnt) {
+        const int tag = node_tag<D>(g, i);
+        double c = cv[k];
+        if (tag > 0) c = __dsub_rn(c, interp<D>(g, i, tag, ld));
+        const double delta = W.w[tag];
+        const double scaled = __ddiv_rn(c, delta);
+        if (!(fabs(scaled) < 9223372036854775808.0)) {
+          ++ovf;
+        } else {
+          const long long q = __double2ll_rn(scaled);
+          rv[k] = __dsub_rn(c, __dmul_rn(__ll2double_rn(q), delta));
+          const uint64_t z = zigzag(q);
+          if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
+          zv[k] = z;
+          hist_varint(sh, z, hsym, hcnt);
+        }
+        advance<D>(g, i);
+      }
+    }
+    if (cnt == 4 && vec_ok) {
+      store4z(zz + e0, zv);
+      store4(r + e0, rv);
+    } else {
+      for (int k = 0; k < cnt; ++k) {
+        zz[e0 + k] = static_cast<Z>(zv[k]);
+        r[e0 + k] = rv[k];
+      }
+    }
+  }
+  hist_flush(sh, hsym, hcnt);
+  if (ovf) atomicAdd(&flags->overflow, ovf);
+  if (wide) atomicOr(&flags->wide, 1u);
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
+}
+
+// ---------------------------------------------------------------------------
+// Inverse transform, coarse → fine (transform.cpp:155-159).  Level l ≥ 1
+// touches only nodes tagged l and reads only nodes of lower tag, which are
+// final by then.  The per-node source value is either a residual (the
+// a-posteriori check of container.cpp:93-119) or a dequantised code
+// (decompress, quantize.cpp:134-158): v = src + 1.0·I(v).
+
+struct SrcResidual {
+  const double* r;
+  __device__ __forceinline__ double operator()(uint64_t n, int) const { return r[n]; }
+};
+
+template <typename Z>
+struct SrcDequant {
+  const Z* zz;
+  Widths W;
+  __device__ __forceinline__ double operator()(uint64_t n, int tag) const {
+    return __dmul_rn(__ll2double_rn(unzigzag(static_cast<uint64_t>(zz[n]))), W.w[tag]);
+  }
+};
+
+// Box pass for level l < L (and level 0): enumerates the level-l box with
+// the level index sets and updates the nodes tagged l.
+template <int D, class Src>
+__global__ void __launch_bounds__(256) k_inverse_box(GridDev g, BoxDev box, int l, Src src, double* v) {
+  auto ld = [v](uint64_t off) { return v[off]; };
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < box.count; p += step) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    uint64_t q = p;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      const uint64_t qq = q / box.n[a];
+      i[a] = __ldg(box.set[a] + (q - qq * box.n[a]));
+      q = qq;
+    }
+    const int tag = node_tag<D>(g, i);
+    if (tag != l) continue;
+    uint64_t n = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) n += static_cast<uint64_t>(i[a]) * g.stride[a];
+    double val = src(n, l);
+    if (l > 0) val = __dadd_rn(val, interp<D>(g, i, l, ld));
+    v[n] = val;
+  }
+}
+
+// Epilogues of the finest pass.
+struct EpiMaxAbs {  // max|e| (error_control.cpp:105, exec.cpp:75-87)
+  double* dummy;
+  __device__ __forceinline__ void operator()(uint64_t, double e, double& red) const { red = fmax(red, fabs(e)); }
+};
+template <typename T>
+struct EpiCastMaxAbs {  // f32 bound on the cast-back output (container.cpp:96-107)
+  const T* src;
+  __device__ __forceinline__ void operator()(uint64_t n, double e, double& red) const {
+    const double s = static_cast<double>(src[n]);
+    const double ce = __dsub_rn(s, static_cast<double>(__double2float_rn(__dsub_rn(s, e))));
+    red = fmax(red, fabs(ce));
+  }
+};
+struct EpiStore64 {  // e (S(0) check) or decompressed f64 values
+  double* out;
+  __device__ __forceinline__ void operator()(uint64_t n, double e, double&) const { out[n] = e; }
+};
+template <typename T>
+struct EpiCastStore {  // f32 cast error, stored for the ordered RMS
+  const T* src;
+  double* out;
+  __device__ __forceinline__ void operator()(uint64_t n, double e, double&) const {
+    const double s = static_cast<double>(src[n]);
+    out[n] = __dsub_rn(s, static_cast<double>(__double2float_rn(__dsub_rn(s, e))));
+  }
+};
+struct EpiNarrow32 {  // decompressed f32 values (container.cpp:252-256)
+  float* out;
+  __device__ __forceinline__ void operator()(uint64_t n, double e, double&) const { out[n] = __double2float_rn(e); }
+};
+
+// Finest pass over the whole grid: nodes tagged L are reconstructed from
+// their source value plus the interpolation of the (final) coarse values,
+// coarser nodes are read back; the epilogue consumes every node's final
+// value (reduction, cast, narrowing).  With L == 0 every node is level 0.
+// SKIP_COARSE: the epilogue does not need coarse nodes (in-place f64 output).
+template <int D, class Src, class Epi, bool SKIP_COARSE>
+__global__ void __launch_bounds__(256) k_inverse_finest(GridDev g, Src src, const double* v, Epi epi,
+                                                        unsigned long long* red_out) {
+  auto ld = [v](uint64_t off) { return v[off]; };
+  double red = 0.0;
+  const uint64_t nruns = (g.N + 3) / 4;
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t run = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; run < nruns; run += step) {
+    const uint64_t e0 = run * 4;
+    const int cnt = static_cast<int>(umin64(4, g.N - e0));
+    uint32_t i[4] = {0, 0, 0, 0};
+    decompose<D>(g, e0, i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < cnt) {
+        const uint64_t n = e0 + k;
+        if (g.L == 0) {
+          epi(n, src(n, 0), red);
+        } else {
+          const int tag = node_tag<D>(g, i);
+          if (tag == g.L) {
+            epi(n, __dadd_rn(src(n, tag), interp<D>(g, i, tag, ld)), red);
+          } else if (!SKIP_COARSE) {
+            epi(n, v[n], red);
+          }
+        }
+        advance<D>(g, i);
+      }
+    }
+  }
+  if (red_out) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) red = fmax(red, __shfl_xor_sync(0xffffffffu, red, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
+  }
+}
+
+// Level-weighted residual aggregate for S(s≠0) (error_control.cpp:72-100):
+// Σ_n 2^{2s(tag−L)}·r² — deterministic fixed-order tree, not the reference's
+// serial sum (documented: the estimator is uncertified and only drives the
+// accept decision; it is never stored).
+template <int D>
+__global__ void __launch_bounds__(256) k_level_weighted(GridDev g, Widths lw, const double* __restrict__ r,
+                                                        double* __restrict__ partials) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  const uint64_t chunk = (g.N + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * chunk, hi = min(lo + chunk, g.N);
+  for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    decompose<D>(g, e, i);
+    const double x = r[e];
+    acc = __dadd_rn(acc, __dmul_rn(lw.w[node_tag<D>(g, i)], __dmul_rn(x, x)));
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+// ---------------------------------------------------------------------------
+// Lossless stage.  Codec 2 codes every LEB128 byte of zigzag(q) with the
+// canonical Huffman code (codec.cpp:399-418, MSB-first, zero padded); codec 1
+// is the same packer with the identity 8-bit code.
+
+constexpr int kPackThreads = 256;
+constexpr int kPackPerThread = 8;
+constexpr int kPackTile = kPackThreads * kPackPerThread;  // values per tile
+constexpr int kPackMaxWords = kPackTile * 150 / 32 + 2;   // ≤ 10 bytes × 15 bits per value
+
+__device__ __forceinline__ uint32_t varint_bits(uint64_t z, const uint8_t* len) {
+  uint32_t b = 0;
+  for (;;) {
+    if (z < 0x80) return b + len[z];
+    b += len[(z & 0x7F) | 0x80];
+    z >>= 7;
+  }
+}
+
+template <typename Z>
+__global__ void __launch_bounds__(kPackThreads) k_tile_bits(const Z* __restrict__ zz, uint64_t n,
+                                                            const uint8_t* __restrict__ len_g,
+                                                            unsigned long long* __restrict__ tile_bits) {
+  __shared__ uint8_t len[256];
+  __shared__ unsigned long long wsum[kPackThreads / 32];
+  len[threadIdx.x] = len_g[threadIdx.x];
+  __syncthreads();
+  const uint64_t base = blockIdx.x * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
+  unsigned long long s = 0;
+#pragma unroll
+  for (int k = 0; k < kPackPerThread; ++k)
+    if (base + k < n) s += varint_bits(static_cast<uint64_t>(zz[base + k]), len);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kPackThreads / 32; ++w) t += wsum[w];
+    tile_bits[blockIdx.x] = t;
+  }
+}
+
+// Exclusive scan of u64 in one CTA (used on per-tile / per-block counts,
+// which are ≤ ~10^6 entries).  out[n] receives the total.
+__global__ void __launch_bounds__(1024) k_scan_u64_single(const unsigned long long* __restrict__ in,
+                                                          unsigned long long* __restrict__ out, uint64_t n) {
+  __shared__ unsigned long long wsum[32];
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t base = 0; base < n; base += blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    const unsigned long long x = i < n ? in[i] : 0;
+    unsigned long long incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long w = lane < (blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const unsigned long long before = carry + (warp ? wsum[warp - 1] : 0) + incl - x;
+    if (i < n) out[i] = before;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+// Packs one tile of values: per-value bit counts → block exclusive scan →
+// codes OR-ed into a shared word buffer aligned to the output's 32-bit word
+// grid → interior words stored, the two edge words (shared with the
+// neighbouring tiles) OR-ed atomically.  Output words hold the stream
+// MSB-first in memory byte order (byte-swapped big-endian words).
+template <typename Z>
+__global__ void __launch_bounds__(kPackThreads) k_pack(const Z* __restrict__ zz, uint64_t n,
+                                                       const uint32_t* __restrict__ code_g,
+                                                       const uint8_t* __restrict__ len_g,
+                                                       const unsigned long long* __restrict__ tile_off,
+                                                       uint32_t* __restrict__ out) {
+  extern __shared__ uint32_t words[];
+  __shared__ uint32_t code[256];
+  __shared__ uint8_t len[256];
+  __shared__ unsigned long long wsum[kPackThreads / 32];
+  code[threadIdx.x] = code_g[threadIdx.x];
+  len[threadIdx.x] = len_g[threadIdx.x];
+  __syncthreads();
+  const uint64_t base = blockIdx.x * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
+  uint64_t z[kPackPerThread];
+  uint32_t bits[kPackPerThread];
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int k = 0; k < kPackPerThread; ++k) {
+    z[k] = base + k < n ? static_cast<uint64_t>(zz[base + k]) : 0;
+    bits[k] = base + k < n ? varint_bits(z[k], len) : 0;
+    mine += bits[k];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 1; w < kPackThreads / 32; ++w) wsum[w] += wsum[w - 1];
+  __syncthreads();
+  const unsigned long long tile_start = tile_off[blockIdx.x];
+  const unsigned long long tile_total = wsum[kPackThreads / 32 - 1];
+  const uint32_t shift0 = static_cast<uint32_t>(tile_start & 31);
+  const uint64_t nwords = (shift0 + tile_total + 31) >> 5;
+  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0;
+  __syncthreads();
+  // local bit position (relative to the first output word of the tile)
+  uint64_t p = shift0 + (warp ? wsum[warp - 1] : 0) + incl - mine;
+#pragma unroll
+  for (int k = 0; k < kPackPerThread; ++k) {
+    if (base + k >= n) break;
+    uint64_t v = z[k];
+    for (;;) {
+      const uint32_t sym = v >= 0x80 ? static_cast<uint32_t>((v & 0x7F) | 0x80) : static_cast<uint32_t>(v);
+      const uint32_t l = len[sym], c = code[sym];
+      const uint32_t w = static_cast<uint32_t>(p >> 5), o = static_cast<uint32_t>(p & 31);
+      if (o + l <= 32) {
+        atomicOr(&words[w], c << (32 - o - l));
+      } else {
+        const uint32_t spill = o + l - 32;
+        atomicOr(&words[w], c >> spill);
+        atomicOr(&words[w + 1], c << (32 - spill));
+      }
+      p += l;
+      if (v < 0x80) break;
+      v >>= 7;
+    }
+  }
+  __syncthreads();
+  if (tile_total == 0) return;
+  const uint64_t gw0 = tile_start >> 5;
+  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) {
+    const uint32_t val = bswap32(words[w]);
+    if (w == 0 || w == nwords - 1) {
+      if (val) atomicOr(out + gw0 + w, val);
+    } else {
+      out[gw0 + w] = val;
+    }
+  }
+}
+
+// Codec 0 (raw little-endian int64, codec.cpp:437-441).
+template <typename Z>
+__global__ void k_raw_encode(const Z* __restrict__ zz, uint64_t n, long long* __restrict__ out) {
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += step)
+    out[k] = unzigzag(static_cast<uint64_t>(zz[k]));
+}
+
+// ---------------------------------------------------------------------------
+// CRC-32 (codec.cpp:14-28): slicing-by-4 per segment, then a GF(2) tree
+// combine crc(A‖B) = crc(A)·x^{8|B|} ⊕ crc(B) (standard CRCs are affine, the
+// init/xorout terms cancel).
+
+__device__ __forceinline__ uint32_t gf2_mul(uint32_t a, uint32_t b) {
+  uint32_t prod = 0;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    if (a & (0x80000000u >> i)) prod ^= b;
+    b = (b & 1u) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+  }
+  return prod;
+}
+
+struct CrcConsts {
+  uint32_t x8n[64];  // x^(8·2^k) mod P
+};
+
+__device__ __forceinline__ uint32_t crc_shift(uint32_t crc, uint64_t nbytes, const CrcConsts& k) {
+  uint32_t m = 0x80000000u;
+  for (int b = 0; nbytes; ++b, nbytes >>= 1)
+    if (nbytes & 1) m = gf2_mul(m, k.x8n[b]);
+  return gf2_mul(m, crc);
+}
+
+constexpr int kCrcThreads = 256;
+constexpr int kCrcSeg = 1024;  // bytes per thread
+
+__global__ void __launch_bounds__(kCrcThreads) k_crc_blocks(const uint8_t* __restrict__ p, uint64_t n,
+                                                            const uint32_t* __restrict__ tab_g, CrcConsts K,
+                                                            uint32_t* __restrict__ blk_crc,
+                                                            unsigned long long* __restrict__ blk_len) {
+  __shared__ uint32_t tab[4][256];
+  __shared__ uint32_t scrc[kCrcThreads];
+  __shared__ unsigned long long slen[kCrcThreads];
+  for (int t = threadIdx.x; t < 1024; t += blockDim.x) tab[t >> 8][t & 255] = tab_g[t];
+  __syncthreads();
+  const uint64_t lo = (blockIdx.x * static_cast<uint64_t>(kCrcThreads) + threadIdx.x) * kCrcSeg;
+  const uint64_t hi = lo < n ? umin64(lo + kCrcSeg, n) : lo;
+  uint32_t c = 0xFFFFFFFFu;
+  uint64_t i = lo;
+  if (hi - lo == kCrcSeg && (reinterpret_cast<uintptr_t>(p + lo) & 15) == 0) {
+    for (; i < hi; i += 16) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p + i));
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        c ^= ws[j];
+        c = tab[3][c & 255] ^ tab[2][(c >> 8) & 255] ^ tab[1][(c >> 16) & 255] ^ tab[0][c >> 24];
+      }
+    }
+  }
+  for (; i < hi; ++i) c = tab[0][(c ^ p[i]) & 255] ^ (c >> 8);
+  scrc[threadIdx.x] = ~c;
+  slen[threadIdx.x] = hi - lo;
+  __syncthreads();
+  for (int s = 1; s < kCrcThreads; s <<= 1) {
+    uint32_t nc = 0;
+    unsigned long long nl = 0;
+    const bool act = (threadIdx.x % (2 * s)) == 0;
+    if (act) {
+      const unsigned long long lb = slen[threadIdx.x + s];
+      nc = lb ? crc_shift(scrc[threadIdx.x], lb, K) ^ scrc[threadIdx.x + s] : scrc[threadIdx.x];
+      nl = slen[threadIdx.x] + lb;
+    }
+    __syncthreads();
+    if (act) {
+      scrc[threadIdx.x] = nc;
+      slen[threadIdx.x] = nl;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    blk_crc[blockIdx.x] = scrc[0];
+    blk_len[blockIdx.x] = slen[0];
+  }
+}
+
+// Folds per-block (crc, len) pairs; iterated until one pair remains.
+__global__ void __launch_bounds__(kCrcThreads) k_crc_fold(const uint32_t* __restrict__ in_crc,
+                                                          const unsigned long long* __restrict__ in_len, uint64_t n,
+                                                          CrcConsts K, uint32_t* __restrict__ out_crc,
+                                                          unsigned long long* __restrict__ out_len) {
+  __shared__ uint32_t scrc[kCrcThreads];
+  __shared__ unsigned long long slen[kCrcThreads];
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(kCrcThreads) + threadIdx.x;
+  scrc[threadIdx.x] = i < n ? in_crc[i] : 0;
+  slen[threadIdx.x] = i < n ? in_len[i] : 0;
+  __syncthreads();
+  for (int s = 1; s < kCrcThreads; s <<= 1) {
+    uint32_t nc = 0;
+    unsigned long long nl = 0;
+    const bool act = (threadIdx.x % (2 * s)) == 0;
+    if (act) {
+      const unsigned long long lb = slen[threadIdx.x + s];
+      nc = lb ? crc_shift(scrc[threadIdx.x], lb, K) ^ scrc[threadIdx.x + s] : scrc[threadIdx.x];
+      nl = slen[threadIdx.x] + lb;
+    }
+    __syncthreads();
+    if (act) {
+      scrc[threadIdx.x] = nc;
+      slen[threadIdx.x] = nl;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out_crc[blockIdx.x] = scrc[0];
+    out_len[blockIdx.x] = slen[0];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Self-synchronising parallel Huffman decode of the varint byte stream.
+// The format has no sync points (codec.cpp:399-418), so the stream is cut
+// into fixed subsequences of kSeqBits bits; each subsequence is decoded from
+// a guessed start, and the start of subsequence j+1 is corrected to the exit
+// (first codeword boundary past its end) of subsequence j until every
+// boundary agrees (prefix codes resynchronise within a few codewords).
+
+constexpr int kSeqBits = 1024;
+constexpr int kDecThreads = 128;
+
+struct SeqInfo {
+  unsigned long long start, exit;
+  uint32_t nsym, nterm;
+  uint32_t last_cont;  // last decoded symbol has the continuation bit
+  uint32_t pad;
+};
+
+struct DecTab {
+  const uint16_t* lut;  // 2^maxlen entries: sym | len << 8
+  int maxlen;
+};
+
+__device__ __forceinline__ uint32_t peek32(const uint32_t* __restrict__ w, uint64_t p) {
+  const uint64_t wi = p >> 5;
+  const uint32_t hi = bswap32(__ldg(w + wi)), lo = bswap32(__ldg(w + wi + 1));
+  return __funnelshift_l(lo, hi, static_cast<uint32_t>(p & 31));
+}
+
+// Decode the codewords starting in [start, end) (end ≤ T); stops early at a
+// codeword that would run past T (incomplete tail).
+__device__ __forceinline__ void decode_seq(const uint32_t* __restrict__ w, uint64_t T, const uint16_t* lut,
+                                           int maxlen, uint64_t start, uint64_t end, SeqInfo& s) {
+  uint64_t p = start;
+  uint32_t nsym = 0, nterm = 0, last = 0;
+  while (p < end) {
+    const uint32_t ent = lut[peek32(w, p) >> (32 - maxlen)];
+    const uint32_t l = ent >> 8;
+    if (p + l > T) break;
+    const uint32_t sym = ent & 0xFF;
+    p += l;
+    ++nsym;
+    nterm += sym < 0x80;
+    last = sym;
+  }
+  s.start = start;
+  s.exit = p;
+  s.nsym = nsym;
+  s.nterm = nterm;
+  s.last_cont = last >= 0x80;
+}
+
+__global__ void __launch_bounds__(kDecThreads) k_huff_sync(const uint32_t* __restrict__ w, uint64_t T,
+                                                           const uint16_t* __restrict__ lut_g, int maxlen,
+                                                           uint64_t nseq, SeqInfo* __restrict__ seq) {
+  extern __shared__ uint16_t lut[];
+  __shared__ unsigned long long sexit[kDecThreads];
+  const int lutn = 1 << maxlen;
+  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
+  __syncthreads();
+  const uint64_t j = blockIdx.x * static_cast<uint64_t>(kDecThreads) + threadIdx.x;
+  const bool valid = j < nseq;
+  SeqInfo s{};
+  uint64_t end = 0;
+  if (valid) {
+    const uint64_t start = j * kSeqBits;
+    end = umin64(start + kSeqBits, T);
+    decode_seq(w, T, lut, maxlen, start, end, s);
+  }
+  sexit[threadIdx.x] = valid ? s.exit : 0;
+  // intra-block resynchronisation
+  for (;;) {
+    const unsigned long long pe = threadIdx.x > 0 ? sexit[threadIdx.x - 1] : 0;
+    __syncthreads();
+    bool changed = false;
+    if (valid && threadIdx.x > 0 && pe != s.start) {
+      decode_seq(w, T, lut, maxlen, pe, end, s);
+      sexit[threadIdx.x] = s.exit;
+      changed = true;
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  if (valid) seq[j] = s;
+}
+
+// Inter-block resynchronisation: the first subsequences of each block are
+// re-decoded from the previous block's exit until they agree.
+__global__ void k_huff_fix(const uint32_t* __restrict__ w, uint64_t T, const uint16_t* __restrict__ lut, int maxlen,
+                           uint64_t nseq, SeqInfo* seq, unsigned int* changed) {
+  const uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x + 1;
+  const uint64_t nblk = (nseq + kDecThreads - 1) / kDecThreads;
+  if (b >= nblk) return;
+  for (uint64_t j = b * kDecThreads; j < umin64((b + 1) * kDecThreads, nseq); ++j) {
+    const unsigned long long pe = *reinterpret_cast<volatile unsigned long long*>(&seq[j - 1].exit);
+    if (pe == seq[j].start) break;
+    SeqInfo s;
+    decode_seq(w, T, lut, maxlen, pe, umin64((j + 1) * kSeqBits, T), s);
+    seq[j] = s;
+    __threadfence();
+    atomicOr(changed, 1u);
+  }
+}
+
+__global__ void k_seq_counts(const SeqInfo* __restrict__ seq, uint64_t nseq, unsigned long long* __restrict__ nterm) {
+  const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (j < nseq) nterm[j] = seq[j].nterm;
+}
+
+struct DecodeStatus {
+  unsigned long long end_bit;  // bit position after the N-th varint (ULLONG_MAX: not reached)
+  unsigned int error;          // 1: varint overflow, 2: truncated value
+  unsigned int wide;           // a value does not fit the u32 store
+  unsigned int clean;          // only zero padding (< 8 bits) follows the N-th varint
+};
+
+// Emit: re-decode each synchronised subsequence and assemble the varints
+// that START in it (a value that runs past the subsequence is finished by
+// decoding on; ≤ 10 bytes).  Values beyond N (decoded zero padding) are
+// ignored, as the reference never reads them (codec.cpp:475-481).
+template <typename Z>
+__global__ void __launch_bounds__(kDecThreads) k_huff_emit(const uint32_t* __restrict__ w, uint64_t T,
+                                                           const uint16_t* __restrict__ lut_g, int maxlen,
+                                                           uint64_t nseq, const SeqInfo* __restrict__ seq,
+                                                           const unsigned long long* __restrict__ term_off,
+                                                           uint64_t N, Z* __restrict__ zz, DecodeStatus* st) {
+  extern __shared__ uint16_t lut[];
+  const int lutn = 1 << maxlen;
+  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
+  __syncthreads();
+  const uint64_t j = blockIdx.x * static_cast<uint64_t>(kDecThreads) + threadIdx.x;
+  if (j >= nseq) return;
+  const SeqInfo s = seq[j];
+  bool skipping = j > 0 && seq[j - 1].last_cont;
+  uint64_t k = term_off[j];
+  if (k >= N && !skipping) return;
+  uint64_t p = s.start;
+  uint64_t acc = 0;
+  int nb = 0;
+  unsigned err = 0, wide = 0;
+  // symbols of this subsequence, then continue past its exit to finish an
+  // open value
+  for (;;) {
+    const bool inside = p < s.exit;
+    if (!inside && nb == 0) break;
+    if (k >= N) break;
+    const uint32_t ent = lut[peek32(w, p) >> (32 - maxlen)];
+    const uint32_t l = ent >> 8;
+    if (p + l > T) {  // stream ends inside an open value
+      err = 2;
+      break;
+    }
+    const uint32_t b = ent & 0xFF;
+    p += l;
+    if (skipping) {
+      if (b < 0x80) {
+        skipping = false;
+        ++k;
+      }
+      continue;
+    }
+    if (nb == 9 && (b & 0xFE)) {  // varint overflows 64 bits (codec.cpp:80-81)
+      err = 1;
+      break;
+    }
+    acc |= static_cast<uint64_t>(b & 0x7F) << (7 * nb);
+    ++nb;
+    if (b < 0x80) {
+      if (sizeof(Z) == 4 && acc > 0xFFFFFFFFull) wide = 1;
+      zz[k] = static_cast<Z>(acc);
+      if (k == N - 1) {  // exhausted_clean (codec.cpp:370-375)
+        st->end_bit = p;
+        const uint64_t rest = T - p;
+        st->clean = rest < 8 && (rest == 0 || (peek32(w, p) >> (32 - rest)) == 0);
+      }
+      ++k;
+      acc = 0;
+      nb = 0;
+    }
+  }
+  if (err) atomicMax(&st->error, err);
+  if (wide) atomicOr(&st->wide, 1u);
+}
+
+// Codec 0 decode: raw little-endian int64 → zigzag.
+template <typename Z>
+__global__ void k_raw_decode(const long long* __restrict__ in, uint64_t n, Z* __restrict__ zz, unsigned int* wide) {
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  unsigned wd = 0;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += step) {
+    const uint64_t z = zigzag(in[k]);
+    if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wd = 1;
+    zz[k] = static_cast<Z>(z);
+  }
+  if (wd) atomicOr(wide, 1u);
+}
+
+template <typename T>
+__global__ void k_fill(T* __restrict__ out, uint64_t n, T value) {
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += step) out[k] = value;
+}
+
+}  // namespace dev
+}  // namespace mgrc_gpu

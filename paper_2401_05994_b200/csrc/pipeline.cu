@@ -1,0 +1,976 @@
+// Host orchestration of the sm_100a compress / decompress path.
+//
+//  compress   (container.cpp:71-131)
+//    K1  k_stats              non-finite / min / max  (+ k_block_sumsq for S-REL)
+//    K2  k_forward_quant      forward transform + quantise + varint histogram
+//    K3  k_inverse_box/finest a-posteriori error of the residuals (shrink loop)
+//    K4  (host)               Huffman lengths + canonical codes (256 symbols)
+//    K5  k_tile_bits/k_pack   bit-offset scan + MSB-first packing
+//    K5b k_crc_blocks/fold    CRC-32 of the payload
+//  decompress (container.cpp:210-261)
+//    CRC → k_huff_sync/fix (self-synchronising decode) → k_huff_emit
+//    → k_inverse_box (levels 0..L-1, dequantised) → k_inverse_finest (+narrow)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "pipeline.hpp"
+
+namespace mgrc_gpu {
+
+using namespace dev;
+
+#define CK(x)                                                                                        \
+  do {                                                                                               \
+    cudaError_t e_ = (x);                                                                            \
+    if (e_ != cudaSuccess) raise(Errc::cuda, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+static void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) raise(Errc::cuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool is_device_pointer(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------------------
+// workspace
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <typename T = void>
+  T* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      const size_t want = std::max(bytes, cap + cap / 4);
+      if (cudaMalloc(&p, want) != cudaSuccess) {
+        cudaGetLastError();
+        cap = 0;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+          cudaGetLastError();
+          p = nullptr;
+          raise(Errc::cuda, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+        }
+        cap = bytes;
+      } else {
+        cap = want;
+      }
+    }
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <typename T = void>
+  T* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      CK(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+      cap = bytes;
+    }
+    return static_cast<T*>(p);
+  }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// Device copy of a hierarchy's tables.
+struct DevHier {
+  std::string key;
+  Hierarchy h;
+  DevBuf buf;
+  GridDev g{};
+  std::vector<BoxDev> boxes;  // per level
+};
+
+struct Scratch {  // small device-side results read back at sync points
+  Stats stats;
+  QuantFlags qflags;
+  unsigned long long red_bits;
+  DecodeStatus dstat;
+  unsigned int fix_changed;
+  unsigned int raw_wide;
+  unsigned long long hist[256];
+};
+
+class Context {
+ public:
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool profiling = false;
+  std::vector<PhaseTime> profile;
+  // workspace
+  DevBuf in, zz, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial;
+  DevBuf scratch_d;
+  PinnedBuf scratch_h, partial_h;
+  std::unique_ptr<DevHier> hier;
+  CrcConsts crc_k{};
+  bool crc_ready = false;
+
+  Scratch* sd() { return scratch_d.get<Scratch>(sizeof(Scratch)); }
+  Scratch* sh() { return scratch_h.get<Scratch>(sizeof(Scratch)); }
+
+  ~Context() {
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+Context& context_for_current_device() {
+  thread_local std::map<int, std::unique_ptr<Context>> ctxs;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  auto& c = ctxs[dev];
+  if (!c) {
+    c = std::make_unique<Context>();
+    c->device = dev;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  return *c;
+}
+
+void context_set_stream(Context& c, cudaStream_t s) {
+  if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
+  c.own_stream = false;
+  c.stream = s;
+}
+cudaStream_t context_stream(Context& c) { return c.stream; }
+void context_set_profiling(Context& c, bool on) { c.profiling = on; }
+const std::vector<PhaseTime>& context_profile(Context& c) { return c.profile; }
+
+// Named CUDA-event brackets on the context stream (profiling mode only).
+class Prof {
+ public:
+  explicit Prof(Context& c) : c_(c) { c_.profile.clear(); }
+  void begin(const char* name, double bytes = 0) {
+    if (!c_.profiling) return;
+    Rec r;
+    r.name = name;
+    r.bytes = bytes;
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, c_.stream);
+    recs_.push_back(r);
+  }
+  void end() {
+    if (!c_.profiling || recs_.empty()) return;
+    cudaEventRecord(recs_.back().b, c_.stream);
+  }
+  ~Prof() {
+    if (!c_.profiling) return;
+    cudaStreamSynchronize(c_.stream);
+    for (auto& r : recs_) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      c_.profile.push_back({r.name, ms, r.bytes});
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  }
+
+ private:
+  struct Rec {
+    std::string name;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  Context& c_;
+  std::vector<Rec> recs_;
+};
+
+static int grid_blocks(uint64_t work_items, int threads, int per_sm = 8) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t need = (work_items + threads - 1) / threads;
+  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(need, static_cast<uint64_t>(sms) * per_sm)));
+}
+
+static std::string hier_key(const Grid& g) {
+  std::string k(reinterpret_cast<const char*>(&g.d), sizeof g.d);
+  k.append(reinterpret_cast<const char*>(g.shape), sizeof g.shape);
+  k.push_back(g.explicit_coords ? 1 : 0);
+  if (g.explicit_coords)
+    for (int a = 0; a < g.d; ++a)
+      k.append(reinterpret_cast<const char*>(g.coords[a].data()), g.coords[a].size() * sizeof(double));
+  return k;
+}
+
+static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
+  const std::string key = hier_key(grid);
+  if (ctx.hier && ctx.hier->key == key) return *ctx.hier;
+  auto dh = std::make_unique<DevHier>();
+  dh->key = key;
+  dh->h = build_hierarchy(grid);
+  const Hierarchy& h = dh->h;
+  const int d = grid.d;
+  // layout: per axis [wl f64][wr f64][left u32][right u32][lvl u8], then sets
+  size_t total = 0;
+  auto align = [](size_t x) { return (x + 15) & ~size_t{15}; };
+  size_t off_ax[kMaxDims][5];
+  for (int a = 0; a < d; ++a) {
+    const size_t n = grid.shape[a];
+    off_ax[a][0] = total, total = align(total + 8 * n);
+    off_ax[a][1] = total, total = align(total + 8 * n);
+    off_ax[a][2] = total, total = align(total + 4 * n);
+    off_ax[a][3] = total, total = align(total + 4 * n);
+    off_ax[a][4] = total, total = align(total + n);
+  }
+  std::vector<std::vector<size_t>> off_set(h.L + 1, std::vector<size_t>(d));
+  for (int l = 0; l <= h.L; ++l)
+    for (int a = 0; a < d; ++a) {
+      off_set[l][a] = total;
+      total = align(total + 4 * h.sets[a][l].size());
+    }
+  std::vector<uint8_t> host(total, 0);
+  for (int a = 0; a < d; ++a) {
+    const size_t n = grid.shape[a];
+    std::memcpy(&host[off_ax[a][0]], h.wl[a].data(), 8 * n);
+    std::memcpy(&host[off_ax[a][1]], h.wr[a].data(), 8 * n);
+    std::memcpy(&host[off_ax[a][2]], h.left[a].data(), 4 * n);
+    std::memcpy(&host[off_ax[a][3]], h.right[a].data(), 4 * n);
+    std::memcpy(&host[off_ax[a][4]], h.lvl[a].data(), n);
+  }
+  for (int l = 0; l <= h.L; ++l)
+    for (int a = 0; a < d; ++a)
+      std::memcpy(&host[off_set[l][a]], h.sets[a][l].data(), 4 * h.sets[a][l].size());
+  uint8_t* dp = dh->buf.get<uint8_t>(total);
+  CK(cudaMemcpyAsync(dp, host.data(), total, cudaMemcpyHostToDevice, ctx.stream));
+  CK(cudaStreamSynchronize(ctx.stream));
+  GridDev& g = dh->g;
+  std::memset(&g, 0, sizeof g);
+  g.d = d;
+  g.L = h.L;
+  g.N = grid.count();
+  uint64_t st = 1;
+  for (int a = d - 1; a >= 0; --a) {
+    g.shape[a] = static_cast<uint32_t>(grid.shape[a]);
+    g.stride[a] = st;
+    st *= grid.shape[a];
+    g.ax[a].wl = reinterpret_cast<const double*>(dp + off_ax[a][0]);
+    g.ax[a].wr = reinterpret_cast<const double*>(dp + off_ax[a][1]);
+    g.ax[a].left = reinterpret_cast<const uint32_t*>(dp + off_ax[a][2]);
+    g.ax[a].right = reinterpret_cast<const uint32_t*>(dp + off_ax[a][3]);
+    g.ax[a].lvl = dp + off_ax[a][4];
+  }
+  dh->boxes.resize(h.L + 1);
+  for (int l = 0; l <= h.L; ++l) {
+    BoxDev& b = dh->boxes[l];
+    std::memset(&b, 0, sizeof b);
+    b.count = 1;
+    for (int a = 0; a < d; ++a) {
+      b.set[a] = reinterpret_cast<const uint32_t*>(dp + off_set[l][a]);
+      b.n[a] = static_cast<uint32_t>(h.sets[a][l].size());
+      b.count *= b.n[a];
+    }
+  }
+  ctx.hier = std::move(dh);
+  return *ctx.hier;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static Widths to_widths(const std::vector<double>& w) {
+  Widths W{};
+  for (size_t l = 0; l < w.size() && l < static_cast<size_t>(kMaxL); ++l) W.w[l] = w[l];
+  return W;
+}
+
+
+// ---------------------------------------------------------------------------
+// dispatch helpers over the dimension count
+
+template <template <int> class F, class... Args>
+static void by_dim(int d, Args&&... args) {
+  switch (d) {
+    case 1: F<1>::run(args...); break;
+    case 2: F<2>::run(args...); break;
+    case 3: F<3>::run(args...); break;
+    case 4: F<4>::run(args...); break;
+    default: raise(Errc::too_many_dims, "unsupported dimension count");
+  }
+}
+
+template <typename T, typename Z>
+struct FwdQuant {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const T* u, Z* zz, double* r,
+                    unsigned long long* hist, QuantFlags* fl, int vec) {
+      const int blocks = grid_blocks((g.N + 3) / 4, 256);
+      k_forward_quant<D, T, Z><<<blocks, 256, 0, s>>>(g, W, u, zz, r, hist, fl, vec);
+      check_launch("k_forward_quant");
+    }
+  };
+};
+
+template <class Src>
+struct InvBox {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const BoxDev& b, int l, const Src& src, double* v) {
+      const int blocks = grid_blocks(b.count, 256);
+      k_inverse_box<D, Src><<<blocks, 256, 0, s>>>(g, b, l, src, v);
+      check_launch("k_inverse_box");
+    }
+  };
+};
+
+template <class Src, class Epi, bool SKIP>
+struct InvFinest {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Src& src, const double* v, const Epi& epi,
+                    unsigned long long* red) {
+      const int blocks = grid_blocks((g.N + 3) / 4, 256);
+      k_inverse_finest<D, Src, Epi, SKIP><<<blocks, 256, 0, s>>>(g, src, v, epi, red);
+      check_launch("k_inverse_finest");
+    }
+  };
+};
+
+struct LevelWeighted {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Widths& lw, const double* r, double* partials,
+                    int blocks) {
+      k_level_weighted<D><<<blocks, 256, 0, s>>>(g, lw, r, partials);
+      check_launch("k_level_weighted");
+    }
+  };
+};
+
+// Coarse levels 1..L-1 of the inverse (level 0 is the identity on the
+// residual buffer / handled by the caller for decompress).
+template <class Src>
+static void inverse_coarse_levels(Context& ctx, DevHier& dh, const Src& src, double* v, int first_level) {
+  for (int l = first_level; l < dh.h.L; ++l)
+    by_dim<InvBox<Src>::template L>(dh.g.d, ctx.stream, dh.g, dh.boxes[l], l, src, v);
+}
+
+// ---------------------------------------------------------------------------
+// CRC of a device byte range
+
+static void ensure_crc(Context& ctx) {
+  if (ctx.crc_ready) return;
+  uint32_t tab[4][256];
+  for (uint32_t i = 0; i < 256; ++i) {
+    uint32_t c = i;
+    for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+    tab[0][i] = c;
+  }
+  for (uint32_t i = 0; i < 256; ++i)
+    for (int t = 1; t < 4; ++t) tab[t][i] = (tab[t - 1][i] >> 8) ^ tab[0][tab[t - 1][i] & 0xFF];
+  uint32_t* d = ctx.crc_tab.get<uint32_t>(sizeof tab);
+  CK(cudaMemcpyAsync(d, tab, sizeof tab, cudaMemcpyHostToDevice, ctx.stream));
+  crc32_x8n_table(ctx.crc_k.x8n);
+  CK(cudaStreamSynchronize(ctx.stream));
+  ctx.crc_ready = true;
+}
+
+// Launches the CRC of [p, p+n) and leaves (crc, len) of the whole range in
+// the returned device slot (crc_a[0], crc_len in crc_b).  Caller syncs.
+struct CrcSlot {
+  uint32_t* crc;
+  unsigned long long* len;
+};
+
+static CrcSlot device_crc_launch(Context& ctx, const uint8_t* p, uint64_t n) {
+  ensure_crc(ctx);
+  const uint64_t per_block = static_cast<uint64_t>(kCrcThreads) * kCrcSeg;
+  uint64_t nb = std::max<uint64_t>(1, (n + per_block - 1) / per_block);
+  const size_t cap = ((nb + 1) * (4 + 8) + 1024 + 255) & ~size_t{255};
+  uint8_t* A = ctx.crc_a.get<uint8_t>(cap * 2);
+  uint32_t* c0 = reinterpret_cast<uint32_t*>(A);
+  unsigned long long* l0 = reinterpret_cast<unsigned long long*>(A + ((4 * (nb + 1) + 15) & ~size_t{15}));
+  uint8_t* B = A + cap;
+  uint32_t* c1 = reinterpret_cast<uint32_t*>(B);
+  unsigned long long* l1 = reinterpret_cast<unsigned long long*>(B + ((4 * (nb + 1) + 15) & ~size_t{15}));
+  k_crc_blocks<<<static_cast<unsigned>(nb), kCrcThreads, 0, ctx.stream>>>(p, n, ctx.crc_tab.get<uint32_t>(4096),
+                                                                          ctx.crc_k, c0, l0);
+  check_launch("k_crc_blocks");
+  while (nb > 1) {
+    const uint64_t nb2 = (nb + kCrcThreads - 1) / kCrcThreads;
+    k_crc_fold<<<static_cast<unsigned>(nb2), kCrcThreads, 0, ctx.stream>>>(c0, l0, nb, ctx.crc_k, c1, l1);
+    check_launch("k_crc_fold");
+    std::swap(c0, c1);
+    std::swap(l0, l1);
+    nb = nb2;
+  }
+  return {c0, l0};
+}
+
+// ---------------------------------------------------------------------------
+// input statistics
+
+template <typename T>
+static void launch_stats(Context& ctx, const T* u, uint64_t n, Stats* out) {
+  Stats init{~0ull, 0ull, 0u};
+  CK(cudaMemcpyAsync(out, &init, sizeof init, cudaMemcpyHostToDevice, ctx.stream));
+  k_stats<T><<<grid_blocks((n + 3) / 4, 256, 4), 256, 0, ctx.stream>>>(u, n, out, aligned16(u));
+  check_launch("k_stats");
+}
+
+static double key_to_double(unsigned long long k) {
+  const unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+// Serial sum of 4096-block partials (exec.cpp:68-70).
+template <typename T>
+static double blocked_sumsq(Context& ctx, const T* v, uint64_t n) {
+  const uint64_t nb = (n + 4095) / 4096;
+  double* part = ctx.partial.get<double>(nb * 8);
+  k_block_sumsq<T><<<static_cast<unsigned>((nb + 127) / 128), 128, 0, ctx.stream>>>(v, n, part, aligned16(v));
+  check_launch("k_block_sumsq");
+  double* hp = ctx.partial_h.get<double>(nb * 8);
+  CK(cudaMemcpyAsync(hp, part, nb * 8, cudaMemcpyDeviceToHost, ctx.stream));
+  CK(cudaStreamSynchronize(ctx.stream));
+  double acc = 0.0;
+  for (uint64_t b = 0; b < nb; ++b) acc = acc + hp[b];
+  return acc;
+}
+
+FieldStats field_stats(Context& ctx, const void* data, DType dtype, uint64_t n) {
+  Scratch* sd = ctx.sd();
+  Scratch* sh = ctx.sh();
+  if (dtype == DType::f32) launch_stats(ctx, static_cast<const float*>(data), n, &sd->stats);
+  else launch_stats(ctx, static_cast<const double*>(data), n, &sd->stats);
+  CK(cudaMemcpyAsync(&sh->stats, &sd->stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx.stream));
+  CK(cudaStreamSynchronize(ctx.stream));
+  return {key_to_double(sh->stats.min_key), key_to_double(sh->stats.max_key), sh->stats.nonfinite != 0};
+}
+
+// ---------------------------------------------------------------------------
+// compress
+
+template <typename T>
+static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DType dtype, const Grid& grid,
+                                 const ErrorSpec& spec, Codec codec) {
+  Prof prof(ctx);
+  cudaStream_t s = ctx.stream;
+  const uint64_t N = grid.count();
+  const T* u = u_in;
+  if (!on_device) {
+    prof.begin("h2d_input", static_cast<double>(N * sizeof(T)));
+    T* d = ctx.in.get<T>(N * sizeof(T));
+    CK(cudaMemcpyAsync(d, u_in, N * sizeof(T), cudaMemcpyHostToDevice, s));
+    prof.end();
+    u = d;
+  }
+  Scratch* sd = ctx.sd();
+  Scratch* sh = ctx.sh();
+
+  // K1: non-finite / min / max (container.cpp:78-84)
+  prof.begin("stats", static_cast<double>(N * sizeof(T)));
+  launch_stats(ctx, u, N, &sd->stats);
+  prof.end();
+  CK(cudaMemcpyAsync(&sh->stats, &sd->stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (sh->stats.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
+  if (!(spec.tol > 0.0)) raise(Errc::invalid_state, "tolerance must be > 0");
+  const double mn = key_to_double(sh->stats.min_key), mx = key_to_double(sh->stats.max_key);
+
+  ContainerParts out;
+  if (mx == mn) {
+    // Constant field (container.cpp:57-69).  blocked_reduce keeps the first
+    // element of each 4096-block and the later block on ties, so the stored
+    // value is the first element of the last block (sign of zero included).
+    T val;
+    CK(cudaMemcpyAsync(&val, u + 4096 * ((N - 1) / 4096), sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double v = static_cast<double>(val);
+    std::vector<uint8_t> payload(8);
+    std::memcpy(payload.data(), &v, 8);
+    append_header(out.head, grid, dtype, true, spec, {0.0}, codec, 8, crc32_host(payload.data(), 8));
+    out.host_tail = payload;
+    return out;
+  }
+
+  // absolute tolerance (error_control.cpp:25-40)
+  double tau;
+  if (spec.mode == Mode::abs) {
+    tau = spec.tol;
+  } else if (spec.norm == Norm::inf) {
+    tau = spec.tol * (mx - mn);
+  } else {
+    prof.begin("sumsq_input", static_cast<double>(N * sizeof(T)));
+    const double ss = blocked_sumsq(ctx, u, N);
+    prof.end();
+    const double rms = std::sqrt(ss / static_cast<double>(N));
+    if (rms == 0.0) raise(Errc::degenerate_data, "relative bound on a zero field");
+    tau = spec.tol * rms;
+  }
+
+  DevHier& dh = device_hierarchy(ctx, grid);
+  const GridDev& g = dh.g;
+  const int L = dh.h.L;
+  std::vector<double> widths = initial_bin_widths(tau, spec, grid.d, L);
+
+  double* r = ctx.r.get<double>(N * 8);
+  const bool level_weighted = spec.norm == Norm::s && spec.smoothness != 0.0;
+  bool wide = false;
+  bool accepted = false;
+  void* zzp = nullptr;
+  for (int pass = 0; pass < 10; ++pass) {
+    const Widths W = to_widths(widths);
+    for (;;) {  // u32 codes first; u64 when some |q| ≥ 2^31
+      CK(cudaMemsetAsync(&sd->qflags, 0, sizeof(QuantFlags), s));
+      CK(cudaMemsetAsync(sd->hist, 0, sizeof sd->hist, s));
+      const double zb = wide ? 8.0 : 4.0;
+      prof.begin("forward_quant", static_cast<double>(N) * (sizeof(T) + zb + 8));
+      if (wide) {
+        auto* zz = ctx.zz.get<unsigned long long>(N * 8);
+        zzp = zz;
+        const int vec = aligned16(u) && aligned16(zz) && aligned16(r);
+        by_dim<FwdQuant<T, unsigned long long>::template L>(grid.d, s, g, W, u, zz, r, sd->hist, &sd->qflags, vec);
+      } else {
+        auto* zz = ctx.zz.get<uint32_t>(N * 4);
+        zzp = zz;
+        const int vec = aligned16(u) && aligned16(zz) && aligned16(r);
+        by_dim<FwdQuant<T, uint32_t>::template L>(grid.d, s, g, W, u, zz, r, sd->hist, &sd->qflags, vec);
+      }
+      prof.end();
+      CK(cudaMemcpyAsync(&sh->qflags, &sd->qflags, sizeof(QuantFlags), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (sh->qflags.overflow)
+        raise(Errc::overflow, std::to_string(sh->qflags.overflow) + " coefficients exceed the 63-bit symbol range");
+      if (sh->qflags.wide && !wide) {
+        wide = true;
+        continue;
+      }
+      break;
+    }
+
+    // a-posteriori error (container.cpp:93-113, error_control.cpp:62-108)
+    double achieved;
+    prof.begin("check", static_cast<double>(N) * (8 + sizeof(T)));
+    if (level_weighted) {
+      Widths lw{};
+      for (int l = 0; l <= L; ++l)
+        lw.w[l] = std::exp2(2.0 * spec.smoothness * (static_cast<double>(l) - static_cast<double>(L)));
+      const int blocks = 1024;
+      double* part = ctx.partial.get<double>(blocks * 8);
+      by_dim<LevelWeighted::L>(grid.d, s, g, lw, r, part, blocks);
+      double* hp = ctx.partial_h.get<double>(blocks * 8);
+      CK(cudaMemcpyAsync(hp, part, blocks * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      double acc = 0.0;
+      for (int b = 0; b < blocks; ++b) acc = acc + hp[b];
+      achieved = std::sqrt(acc / static_cast<double>(N));
+    } else {
+      const SrcResidual src{r};
+      inverse_coarse_levels(ctx, dh, src, r, 1);  // in place: r becomes e on coarse nodes
+      if (spec.norm == Norm::inf) {
+        CK(cudaMemsetAsync(&sd->red_bits, 0, 8, s));
+        if (dtype == DType::f32)
+          by_dim<InvFinest<SrcResidual, EpiCastMaxAbs<T>, false>::template L>(
+              grid.d, s, g, src, r, EpiCastMaxAbs<T>{u}, &sd->red_bits);
+        else
+          by_dim<InvFinest<SrcResidual, EpiMaxAbs, false>::template L>(grid.d, s, g, src, r, EpiMaxAbs{nullptr},
+                                                                      &sd->red_bits);
+        CK(cudaMemcpyAsync(&sh->red_bits, &sd->red_bits, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::memcpy(&achieved, &sh->red_bits, 8);
+      } else {  // S(0): ordered RMS of e (or of the f32 cast error)
+        double* e = ctx.e.get<double>(N * 8);
+        if (dtype == DType::f32)
+          by_dim<InvFinest<SrcResidual, EpiCastStore<T>, false>::template L>(
+              grid.d, s, g, src, r, EpiCastStore<T>{u, e}, nullptr);
+        else
+          by_dim<InvFinest<SrcResidual, EpiStore64, false>::template L>(grid.d, s, g, src, r, EpiStore64{e},
+                                                                       nullptr);
+        achieved = std::sqrt(blocked_sumsq(ctx, static_cast<const double*>(e), N) / static_cast<double>(N));
+      }
+    }
+    prof.end();
+    if (achieved <= tau * (1.0 - 1e-9)) {
+      accepted = true;
+      break;
+    }
+    for (double& w : widths) w *= 0.5;
+  }
+  if (!accepted) raise(Errc::tolerance_unreachable, "bin shrink loop exhausted after 10 passes");
+
+  // lossless stage (codec.cpp:431-453)
+  std::vector<uint8_t> table_bytes;
+  const uint8_t* dev_payload = nullptr;
+  uint64_t dev_len = 0;
+  if (codec == Codec::raw) {
+    auto* raw = ctx.bits.get<long long>(N * 8 + 16);
+    prof.begin("raw_encode", static_cast<double>(N) * ((wide ? 8 : 4) + 8));
+    if (wide)
+      k_raw_encode<<<grid_blocks(N, 256), 256, 0, s>>>(static_cast<unsigned long long*>(zzp), N, raw);
+    else
+      k_raw_encode<<<grid_blocks(N, 256), 256, 0, s>>>(static_cast<uint32_t*>(zzp), N, raw);
+    check_launch("k_raw_encode");
+    prof.end();
+    dev_payload = reinterpret_cast<const uint8_t*>(raw);
+    dev_len = N * 8;
+  } else {
+    CodeTable table;
+    if (codec == Codec::huffman) {
+      CK(cudaMemcpyAsync(sh->hist, sd->hist, sizeof sh->hist, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      table = build_code_table(reinterpret_cast<const uint64_t*>(sh->hist));  // K4 on host: 256 symbols
+      write_table_header(table_bytes, table);
+    } else {
+      for (int b = 0; b < 256; ++b) {
+        table.lengths[b] = 8;
+        table.codes[b] = static_cast<uint32_t>(b);
+      }
+      table.nsym = 256;
+      table.max_len = 8;
+    }
+    if (codec == Codec::varint || table.nsym >= 2) {
+      struct {
+        uint32_t codes[256];
+        uint8_t lens[256];
+      } tab;
+      for (int b = 0; b < 256; ++b) {
+        tab.codes[b] = table.codes[b];
+        tab.lens[b] = table.lengths[b];
+      }
+      auto* dtab = ctx.codes.get<uint8_t>(sizeof tab);
+      CK(cudaMemcpyAsync(dtab, &tab, sizeof tab, cudaMemcpyHostToDevice, s));
+      const uint32_t* dcodes = reinterpret_cast<const uint32_t*>(dtab);
+      const uint8_t* dlens = dtab + 1024;
+      const uint64_t ntiles = (N + kPackTile - 1) / kPackTile;
+      auto* tb = ctx.tiles.get<unsigned long long>(ntiles * 8);
+      auto* toff = ctx.scan.get<unsigned long long>((ntiles + 1) * 8);
+      prof.begin("tile_bits", static_cast<double>(N) * (wide ? 8 : 4));
+      if (wide)
+        k_tile_bits<<<static_cast<unsigned>(ntiles), kPackThreads, 0, s>>>(
+            static_cast<unsigned long long*>(zzp), N, dlens, tb);
+      else
+        k_tile_bits<<<static_cast<unsigned>(ntiles), kPackThreads, 0, s>>>(static_cast<uint32_t*>(zzp), N, dlens,
+                                                                           tb);
+      check_launch("k_tile_bits");
+      k_scan_u64_single<<<1, 1024, 0, s>>>(tb, toff, ntiles);
+      check_launch("k_scan_u64_single");
+      prof.end();
+      unsigned long long total_bits = 0;
+      CK(cudaMemcpyAsync(&sh->red_bits, toff + ntiles, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      total_bits = sh->red_bits;
+      const uint64_t nbytes = (total_bits + 7) / 8;
+      const uint64_t nwords = (total_bits + 31) / 32 + 2;
+      auto* words = ctx.bits.get<uint32_t>(nwords * 4 + 16);
+      prof.begin("pack", static_cast<double>(N) * (wide ? 8 : 4) + static_cast<double>(nbytes));
+      CK(cudaMemsetAsync(words, 0, nwords * 4, s));
+      const size_t smem = static_cast<size_t>(kPackMaxWords) * 4;
+      if (wide)
+        k_pack<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<unsigned long long*>(zzp), N,
+                                                                        dcodes, dlens, toff, words);
+      else
+        k_pack<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<uint32_t*>(zzp), N, dcodes,
+                                                                        dlens, toff, words);
+      check_launch("k_pack");
+      prof.end();
+      dev_payload = reinterpret_cast<const uint8_t*>(words);
+      dev_len = nbytes;
+    }
+  }
+
+  // CRC-32 of the payload = crc(table header) ⊕-combined with the device part
+  uint32_t crc = crc32_host(table_bytes.data(), table_bytes.size());
+  if (dev_len) {
+    prof.begin("crc", static_cast<double>(dev_len));
+    CrcSlot slot = device_crc_launch(ctx, dev_payload, dev_len);
+    prof.end();
+    uint32_t dcrc = 0;
+    CK(cudaMemcpyAsync(&sh->fix_changed, slot.crc, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dcrc = sh->fix_changed;
+    crc = table_bytes.empty() ? dcrc : crc32_combine(crc, dcrc, dev_len);
+  }
+  const uint64_t payload_len = table_bytes.size() + dev_len;
+  append_header(out.head, grid, dtype, false, spec, widths, codec, payload_len, crc);
+  out.head.insert(out.head.end(), table_bytes.begin(), table_bytes.end());
+  out.dev = dev_payload;
+  out.dev_len = dev_len;
+  return out;
+}
+
+ContainerParts compress(Context& ctx, const void* data, DType dtype, const Grid& grid, const ErrorSpec& spec,
+                        Codec codec) {
+  if (static_cast<int>(codec) > 2) raise(Errc::unknown_codec, "codec " + std::to_string(static_cast<int>(codec)));
+  const bool on_dev = is_device_pointer(data);
+  if (dtype == DType::f32)
+    return compress_t(ctx, static_cast<const float*>(data), on_dev, dtype, grid, spec, codec);
+  return compress_t(ctx, static_cast<const double*>(data), on_dev, dtype, grid, spec, codec);
+}
+
+// ---------------------------------------------------------------------------
+// decompress
+
+ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len) {
+  if (!is_device_pointer(in)) return parse_header(in, len);
+  // device-resident container: fetch the header bytes (coords may make it long)
+  uint64_t want = std::min<uint64_t>(len, 4096);
+  for (;;) {
+    std::vector<uint8_t> h(want);
+    CK(cudaMemcpyAsync(h.data(), in, want, cudaMemcpyDeviceToHost, ctx.stream));
+    CK(cudaStreamSynchronize(ctx.stream));
+    try {
+      return parse_header(h.data(), want);
+    } catch (const Error& e) {
+      if (want == len || e.code() != Errc::corrupt_stream) throw;
+      want = std::min<uint64_t>(len, want * 8);
+    }
+  }
+}
+
+template <typename Z>
+static void decode_emit(Context& ctx, const uint32_t* w, uint64_t T, const uint16_t* lut, int maxlen, uint64_t nseq,
+                        const SeqInfo* seq, const unsigned long long* toff, uint64_t N, Z* zz, DecodeStatus* st) {
+  const size_t smem = sizeof(uint16_t) << maxlen;
+  k_huff_emit<Z><<<static_cast<unsigned>((nseq + kDecThreads - 1) / kDecThreads), kDecThreads, smem, ctx.stream>>>(
+      w, T, lut, maxlen, nseq, seq, toff, N, zz, st);
+  check_launch("k_huff_emit");
+}
+
+template <typename Z>
+static void run_recon(Context& ctx, DevHier& dh, const Z* zz, const Widths& W, DType dtype, void* out,
+                      uint64_t N) {
+  cudaStream_t s = ctx.stream;
+  const GridDev& g = dh.g;
+  const SrcDequant<Z> src{zz, W};
+  double* v = dtype == DType::f64 ? static_cast<double*>(out) : ctx.v.get<double>(N * 8);
+  if (g.L > 0) {
+    by_dim<InvBox<SrcDequant<Z>>::template L>(g.d, s, g, dh.boxes[0], 0, src, v);  // level 0: v = q·δ0
+    inverse_coarse_levels(ctx, dh, src, v, 1);
+  }
+  if (dtype == DType::f64)
+    by_dim<InvFinest<SrcDequant<Z>, EpiStore64, true>::template L>(g.d, s, g, src, v, EpiStore64{v}, nullptr);
+  else
+    by_dim<InvFinest<SrcDequant<Z>, EpiNarrow32, false>::template L>(g.d, s, g, src, v,
+                                                                    EpiNarrow32{static_cast<float*>(out)}, nullptr);
+}
+
+DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void* out, uint64_t out_cap) {
+  Prof prof(ctx);
+  cudaStream_t s = ctx.stream;
+  const bool in_dev = is_device_pointer(in);
+  const ContainerInfo info = inspect_any(ctx, in, len);
+  if (info.payload_len != len - info.header_size) raise(Errc::corrupt_stream, "payload length mismatch");
+  DecodedInfo di{};
+  di.dtype = info.dtype;
+  di.ndims = info.ndims;
+  uint64_t N = 1;
+  for (int a = 0; a < info.ndims; ++a) {
+    di.shape[a] = info.shape[a];
+    N *= info.shape[a];
+  }
+  const uint64_t out_bytes = N * dtype_size(info.dtype);
+  if (out_cap < out_bytes) raise(Errc::invalid_argument, "output buffer too small");
+  const bool out_dev = is_device_pointer(out);
+  void* dout = out;
+  if (!out_dev) dout = ctx.e.get<uint8_t>(out_bytes);
+
+  // split the payload: [head: Huffman table header, host-checked][body: device]
+  const uint8_t* payload = in + info.header_size;
+  const uint64_t plen = info.payload_len;
+  const uint64_t split = info.codec_id == 2 ? std::min<uint64_t>(plen, kHuffTableBytes) : 0;
+  std::vector<uint8_t> head(split);
+  const uint64_t body_len = plen - split;
+  // body in an aligned, zero-padded device buffer (the decoder reads ahead)
+  uint8_t* body = ctx.bits.get<uint8_t>(body_len + 64);
+  prof.begin("h2d_payload", static_cast<double>(body_len));
+  CK(cudaMemsetAsync(body + (body_len & ~uint64_t{15}), 0, 64, s));
+  if (in_dev) {
+    if (split) CK(cudaMemcpyAsync(head.data(), payload, split, cudaMemcpyDeviceToHost, s));
+    if (body_len) CK(cudaMemcpyAsync(body, payload + split, body_len, cudaMemcpyDeviceToDevice, s));
+  } else {
+    std::memcpy(head.data(), payload, split);
+    if (body_len) CK(cudaMemcpyAsync(body, payload + split, body_len, cudaMemcpyHostToDevice, s));
+  }
+  prof.end();
+  Scratch* sd = ctx.sd();
+  Scratch* sh = ctx.sh();
+  // CRC (container.cpp:217-218)
+  uint32_t crc = crc32_host(head.data(), split);
+  if (body_len) {
+    prof.begin("crc", static_cast<double>(body_len));
+    CrcSlot slot = device_crc_launch(ctx, body, body_len);
+    prof.end();
+    CK(cudaMemcpyAsync(&sh->fix_changed, slot.crc, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    crc = split ? crc32_combine(crc, sh->fix_changed, body_len) : sh->fix_changed;
+  } else {
+    CK(cudaStreamSynchronize(s));
+  }
+  if (crc != info.checksum) raise(Errc::checksum_mismatch, "payload checksum failed");
+
+  if (info.constant_field) {
+    if (plen != 8) raise(Errc::corrupt_stream, "constant payload must be 8 bytes");
+    uint8_t pb[8];
+    if (in_dev) {
+      CK(cudaMemcpyAsync(pb, payload, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    } else {
+      std::memcpy(pb, payload, 8);
+    }
+    double v;
+    std::memcpy(&v, pb, 8);
+    if (info.dtype == DType::f32)
+      k_fill<<<grid_blocks(N, 256), 256, 0, s>>>(static_cast<float*>(dout), N, static_cast<float>(v));
+    else
+      k_fill<<<grid_blocks(N, 256), 256, 0, s>>>(static_cast<double*>(dout), N, v);
+    check_launch("k_fill");
+  } else {
+    const double* cptr[kMaxDims];
+    for (int a = 0; a < info.ndims; ++a) cptr[a] = info.coords[a].data();
+    const Grid grid = make_grid(info.ndims, info.shape, info.coords_present ? cptr : nullptr);
+    DevHier& dh = device_hierarchy(ctx, grid);
+    if (info.nlevels != dh.h.L) raise(Errc::corrupt_stream, "level count does not match the shape");
+    const Widths W = to_widths(info.bin_widths);
+
+    bool wide = false;
+    if (info.codec_id == 0) {  // raw int64 (codec.cpp:459-466)
+      if (plen != N * 8) raise(Errc::corrupt_stream, "raw payload length mismatch");
+      CK(cudaMemsetAsync(&sd->raw_wide, 0, 4, s));
+      auto* zz = ctx.zz.get<uint32_t>(N * 4);
+      k_raw_decode<<<grid_blocks(N, 256), 256, 0, s>>>(reinterpret_cast<const long long*>(body), N, zz,
+                                                       &sd->raw_wide);
+      check_launch("k_raw_decode");
+      CK(cudaMemcpyAsync(&sh->raw_wide, &sd->raw_wide, 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (sh->raw_wide) {
+        wide = true;
+        auto* zz64 = ctx.zz.get<unsigned long long>(N * 8);
+        k_raw_decode<<<grid_blocks(N, 256), 256, 0, s>>>(reinterpret_cast<const long long*>(body), N, zz64,
+                                                         &sd->raw_wide);
+        check_launch("k_raw_decode");
+      }
+    } else {
+      // varint stream: either Huffman coded (codec 2) or plain bytes (codec 1)
+      CodeTable table;
+      if (info.codec_id == 2) {
+        uint64_t used = 0;
+        table = read_table_header(head.data(), split, &used);
+        if (table.nsym == 0) raise(Errc::corrupt_stream, "read past empty Huffman stream");
+      } else {
+        for (int b = 0; b < 256; ++b) {
+          table.lengths[b] = 8;
+          table.codes[b] = static_cast<uint32_t>(b);
+        }
+        table.nsym = 256;
+        table.max_len = 8;
+      }
+      if (table.nsym == 1) {
+        // Single-symbol stream: no data bits (codec.cpp:366, :413).
+        int sym = 0;
+        for (int b = 0; b < 256; ++b)
+          if (table.lengths[b]) sym = b;
+        if (sym >= 0x80) raise(Errc::corrupt_stream, "varint overflows 64 bits");
+        if (body_len != 0) raise(Errc::corrupt_stream, "trailing bits after Huffman stream");
+        auto* zz = ctx.zz.get<uint32_t>(N * 4);
+        k_fill<<<grid_blocks(N, 256), 256, 0, s>>>(zz, N, static_cast<uint32_t>(sym));
+        check_launch("k_fill");
+      } else {
+        const std::vector<uint16_t> lut_h = build_decode_lut(table);
+        auto* lut = ctx.lut.get<uint16_t>(lut_h.size() * 2);
+        CK(cudaMemcpyAsync(lut, lut_h.data(), lut_h.size() * 2, cudaMemcpyHostToDevice, s));
+        const int maxlen = table.max_len;
+        const uint64_t T = body_len * 8;
+        const uint64_t nseq = std::max<uint64_t>(1, (T + kSeqBits - 1) / kSeqBits);
+        auto* seq = ctx.seq.get<SeqInfo>(nseq * sizeof(SeqInfo));
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(body);
+        const size_t smem = sizeof(uint16_t) << maxlen;
+        if (smem > 48 * 1024) {
+          CK(cudaFuncSetAttribute(k_huff_sync, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          CK(cudaFuncSetAttribute(k_huff_emit<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+          CK(cudaFuncSetAttribute(k_huff_emit<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+        }
+        prof.begin("huff_sync", static_cast<double>(body_len));
+        k_huff_sync<<<static_cast<unsigned>((nseq + kDecThreads - 1) / kDecThreads), kDecThreads, smem, s>>>(
+            w, T, lut, maxlen, nseq, seq);
+        check_launch("k_huff_sync");
+        const uint64_t nblk = (nseq + kDecThreads - 1) / kDecThreads;
+        for (int it = 0; nblk > 1; ++it) {
+          CK(cudaMemsetAsync(&sd->fix_changed, 0, 4, s));
+          k_huff_fix<<<static_cast<unsigned>((nblk - 1 + 127) / 128), 128, 0, s>>>(w, T, lut, maxlen, nseq, seq,
+                                                                                  &sd->fix_changed);
+          check_launch("k_huff_fix");
+          CK(cudaMemcpyAsync(&sh->fix_changed, &sd->fix_changed, 4, cudaMemcpyDeviceToHost, s));
+          CK(cudaStreamSynchronize(s));
+          if (!sh->fix_changed) break;
+        }
+        prof.end();
+        auto* cnt = ctx.tiles.get<unsigned long long>(nseq * 8);
+        auto* toff = ctx.scan.get<unsigned long long>((nseq + 1) * 8);
+        k_seq_counts<<<static_cast<unsigned>((nseq + 255) / 256), 256, 0, s>>>(seq, nseq, cnt);
+        check_launch("k_seq_counts");
+        k_scan_u64_single<<<1, 1024, 0, s>>>(cnt, toff, nseq);
+        check_launch("k_scan_u64_single");
+        for (;;) {
+          DecodeStatus init{~0ull, 0u, 0u, 0u};
+          CK(cudaMemcpyAsync(&sd->dstat, &init, sizeof init, cudaMemcpyHostToDevice, s));
+          prof.begin("huff_emit", static_cast<double>(body_len) + static_cast<double>(N) * (wide ? 8 : 4));
+          if (wide)
+            decode_emit(ctx, w, T, lut, maxlen, nseq, seq, toff, N, ctx.zz.get<unsigned long long>(N * 8),
+                        &sd->dstat);
+          else
+            decode_emit(ctx, w, T, lut, maxlen, nseq, seq, toff, N, ctx.zz.get<uint32_t>(N * 4), &sd->dstat);
+          prof.end();
+          CK(cudaMemcpyAsync(&sh->dstat, &sd->dstat, sizeof(DecodeStatus), cudaMemcpyDeviceToHost, s));
+          CK(cudaStreamSynchronize(s));
+          if (sh->dstat.error == 1) raise(Errc::corrupt_stream, "varint overflows 64 bits");
+          if (sh->dstat.error == 2 || sh->dstat.end_bit == ~0ull)
+            raise(Errc::corrupt_stream, info.codec_id == 2 ? "Huffman stream truncated" : "truncated varint stream");
+          if (!sh->dstat.clean)
+            raise(Errc::corrupt_stream, info.codec_id == 2 ? "trailing bits after Huffman stream"
+                                                           : "trailing bytes after varint stream");
+          if (sh->dstat.wide && !wide) {
+            wide = true;
+            continue;
+          }
+          break;
+        }
+      }
+    }
+    prof.begin("recon", static_cast<double>(N) * ((wide ? 8 : 4) + dtype_size(info.dtype)));
+    if (wide)
+      run_recon(ctx, dh, ctx.zz.get<unsigned long long>(N * 8), W, info.dtype, dout, N);
+    else
+      run_recon(ctx, dh, ctx.zz.get<uint32_t>(N * 4), W, info.dtype, dout, N);
+    prof.end();
+  }
+  if (!out_dev) {
+    prof.begin("d2h_output", static_cast<double>(out_bytes));
+    CK(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, s));
+    prof.end();
+  }
+  CK(cudaStreamSynchronize(s));
+  return di;
+}
+
+}  // namespace mgrc_gpu

@@ -1,0 +1,64 @@
+// Device pipeline: compress / decompress of one container on one GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+
+namespace mgrc_gpu {
+
+struct PhaseTime {
+  std::string name;
+  double ms;
+  double bytes;  // algorithmic bytes moved by the phase (0 when not a kernel of interest)
+};
+
+// A compressed container split into a host part (container header, plus the
+// Huffman table header for codec 2) and a device part (the coded stream).
+struct ContainerParts {
+  std::vector<uint8_t> head;   // host bytes
+  const uint8_t* dev = nullptr;  // device bytes (owned by the context workspace)
+  uint64_t dev_len = 0;
+  std::vector<uint8_t> host_tail;  // tail bytes kept on the host (constant field payload)
+  uint64_t total() const { return head.size() + dev_len + host_tail.size(); }
+};
+
+struct DecodedInfo {
+  DType dtype;
+  int ndims;
+  uint64_t shape[kMaxDims];
+};
+
+class Context;
+
+// Per-thread, per-device context (streams + grow-only workspace); calls are
+// reentrant across threads because no state is shared between contexts.
+Context& context_for_current_device();
+void context_set_stream(Context& c, cudaStream_t s);
+cudaStream_t context_stream(Context& c);
+void context_set_profiling(Context& c, bool on);
+const std::vector<PhaseTime>& context_profile(Context& c);
+
+// data: host or device pointer (auto-detected), N elements of dtype.
+ContainerParts compress(Context& ctx, const void* data, DType dtype, const Grid& grid, const ErrorSpec& spec,
+                        Codec codec);
+
+// Parses and validates; decodes into `out` (host or device, capacity checked).
+DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void* out, uint64_t out_capacity_bytes);
+ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len);
+
+bool is_device_pointer(const void* p);
+
+// Input statistics used by the multi-GPU driver for global REL normalisation.
+struct FieldStats {
+  double min, max;
+  bool nonfinite;
+};
+FieldStats field_stats(Context& ctx, const void* data, DType dtype, uint64_t n);
+
+}  // namespace mgrc_gpu

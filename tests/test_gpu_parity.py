@@ -1,0 +1,152 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle.
+
+Bar (north_star / SURVEY §8): containers byte-identical to the reference's
+(which implies bit-exact quantised codes, identical Huffman bytes and an
+identical ratio), decompressed arrays bit-identical to the reference's
+decompressor, and every reconstruction within the requested bound.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# (shape, dtype, tol, norm, s, mode, field)
+CASES = [
+    ((65, 65, 65), np.float64, 1e-3, 0, 0.0, 1, "multisine"),        # config 1
+    ((33, 17, 9), np.float32, 1e-4, 0, 0.0, 1, "noisy"),
+    ((129, 130), np.float64, 1e-3, 1, 1.0, 1, "noisy"),             # S(1), level-weighted estimator
+    ((129, 130), np.float64, 1e-3, 1, 0.0, 1, "noisy"),             # S(0) = RMS
+    ((257, 256), np.float32, 1e-5, 0, 0.0, 1, "noisy"),
+    ((12, 7, 10), np.float32, 1e-3, 1, 0.0, 0, "noisy"),
+    ((6, 5, 4, 3), np.float64, 1e-2, 0, 0.0, 0, "noisy"),           # 4-D
+    ((17,), np.float64, 1e-3, 0, 0.0, 1, "noisy"),                  # 1-D
+    ((6,), np.float64, 1e-3, 0, 0.0, 0, "noisy"),
+    ((2, 2), np.float64, 1e-3, 0, 0.0, 0, "noisy"),                 # L = 0
+    ((2, 9), np.float32, 1e-3, 0, 0.0, 0, "noisy"),
+    ((256, 33), np.float32, 1e-4, 1, 0.0, 1, "noisy"),              # f32 S(0): cast-error RMS
+    ((100, 3, 40), np.float64, 1e-6, 0, 0.0, 0, "random"),         # wide codes
+    ((65, 65), np.float64, 1e-14, 0, 0.0, 0, "random"),            # |q| > 2^31 (u64 path)
+]
+
+
+def field(oracle, kind, shape, dtype):
+    if kind == "multisine":
+        u = oracle.multisine(shape)
+    elif kind == "noisy":
+        u = oracle.multisine_noisy(shape, 42, 0.05)
+    else:
+        u = oracle.random_field(shape, 7, -3.0, 3.0)
+    return u.astype(dtype)
+
+
+@pytest.mark.parametrize("codec", [2, 1, 0])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[0])) + f"-{c[1].__name__}-n{c[3]}s{c[4]}")
+def test_container_parity(mg, oracle, case, codec):
+    shape, dt, tol, norm, s, mode, kind = case
+    u = field(oracle, kind, shape, dt)
+    want = oracle.compress(u, tol, norm, s, mode, codec)
+    got = mg.compress(u, mg.make_grid(shape), mg.ErrorSpec(tol, mg.Norm(norm), s, mg.Mode(mode)), mg.Codec(codec))
+    assert len(got) == len(want)
+    assert got == want
+    # decompress on the GPU == reference decompressor, bit for bit
+    back = mg.decompress(got)
+    ref_back = oracle.decompress(want)
+    assert back.dtype == ref_back.dtype and back.shape == ref_back.shape
+    assert np.array_equal(back.view(np.uint8), ref_back.view(np.uint8))
+
+
+def test_decompress_accepts_device_buffers(mg, oracle):
+    import torch
+
+    u = field(oracle, "noisy", (33, 40, 21), np.float32)
+    blob = oracle.compress(u, 1e-4, 0, 0.0, 1, 2)
+    dblob = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda()
+    out = torch.empty(u.shape, dtype=torch.float32, device="cuda")
+    mg.decompress_into(dblob, out)
+    assert np.array_equal(out.cpu().numpy(), oracle.decompress(blob))
+    # compress from a device tensor into a device buffer
+    du = torch.from_numpy(u).cuda()
+    n = mg.compress_to(du, None, mg.make_grid(u.shape), mg.ErrorSpec(1e-4, mg.Norm.inf, 0.0, mg.Mode.rel))
+    dst = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    mg.compress_to(du, dst, mg.make_grid(u.shape), mg.ErrorSpec(1e-4, mg.Norm.inf, 0.0, mg.Mode.rel))
+    assert bytes(dst.cpu().numpy()) == blob
+
+
+def test_explicit_coords(mg, oracle):
+    rng = np.random.default_rng(3)
+    shape = (17, 12, 9)
+    coords = [np.cumsum(rng.uniform(0.05, 1.0, n)) - 1.0 for n in shape]
+    u = field(oracle, "noisy", shape, np.float64)
+    want = oracle.compress(u, 1e-3, 0, 0.0, 0, 2, coords=coords)
+    got = mg.compress(u, mg.make_grid(shape, coords), mg.ErrorSpec(1e-3))
+    assert got == want
+    assert np.array_equal(mg.decompress(got), oracle.decompress(want))
+
+
+@pytest.mark.parametrize("value", [3.25, 0.0, -0.0])
+def test_constant_field(mg, oracle, value):
+    u = np.full((9, 33), value)
+    want = oracle.compress(u, 1e-3, 0, 0.0, 1, 2)
+    got = mg.compress(u, mg.make_grid(u.shape), mg.ErrorSpec(1e-3, mg.Norm.inf, 0.0, mg.Mode.rel))
+    assert got == want
+    assert np.array_equal(mg.decompress(got).view(np.uint64), oracle.decompress(want).view(np.uint64))
+
+
+def test_error_paths(mg, oracle):
+    u = field(oracle, "noisy", (9, 17), np.float64)
+    grid = mg.make_grid(u.shape)
+    bad = u.copy()
+    bad[3, 3] = np.nan
+    with pytest.raises(mg.MgrcError) as e:
+        mg.compress(bad, grid, mg.ErrorSpec(1e-3))
+    assert e.value.name == "NonFiniteInput"
+    with pytest.raises(mg.MgrcError) as e:
+        mg.compress(u, grid, mg.ErrorSpec(0.0))
+    assert e.value.name == "InvalidState"
+    with pytest.raises(mg.MgrcError) as e:
+        mg.compress(u, mg.make_grid((9, 1)), mg.ErrorSpec(1e-3))
+    assert e.value.name == "InvalidShape"
+    with pytest.raises(mg.MgrcError) as e:
+        mg.compress(u, grid, mg.ErrorSpec(1e-300, mg.Norm.inf))
+    assert e.value.name == "Overflow"
+    blob = oracle.compress(u, 1e-3, 0, 0.0, 0, 2)
+    flipped = bytearray(blob)
+    flipped[-5] ^= 0x10
+    with pytest.raises(mg.MgrcError) as e:
+        mg.decompress(bytes(flipped))
+    assert e.value.name == "ChecksumMismatch"
+    with pytest.raises(mg.MgrcError) as e:
+        mg.decompress(blob[:-1])
+    assert e.value.name == "CorruptStream"
+
+
+def test_corrupt_streams_match_reference_errors(mg, oracle):
+    """Byte-flip fuzzing of codec-2 payloads with the CRC recomputed, so the
+    decoder itself must detect the damage exactly where the reference does."""
+    import zlib
+
+    u = field(oracle, "noisy", (33, 20), np.float64)
+    blob = bytearray(oracle.compress(u, 1e-3, 0, 0.0, 0, 2))
+    info = oracle.inspect(bytes(blob))
+    hs, pl = info.header_size, info.payload_len
+    rng = np.random.default_rng(11)
+    for trial in range(60):
+        b = bytearray(blob)
+        k = int(rng.integers(3 + 128, pl))  # inside the code stream
+        b[hs + k] ^= int(rng.integers(1, 256))
+        crc = zlib.crc32(bytes(b[hs:hs + pl]))
+        b[hs - 4:hs] = crc.to_bytes(4, "little")
+        b = bytes(b)
+        try:
+            want = oracle.decompress(b)
+            werr = None
+        except Exception as e:  # noqa: BLE001
+            werr = e.name
+        try:
+            got = mg.decompress(b)
+            gerr = None
+        except mg.MgrcError as e:
+            gerr = e.name
+        assert gerr == werr, (trial, gerr, werr)
+        if werr is None:
+            assert np.array_equal(got, want)
