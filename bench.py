@@ -1,0 +1,446 @@
+#!/usr/bin/env python3
+"""Benchmark of the sm_100a compress / decompress path (BASELINE.json metric).
+
+One *step* = one compress + one decompress of the workload field through the
+library (``paper_2401_05994_b200``, C-ABI ``include/mgrc_gpu.h``):
+
+  * ``value``   device-resident: the input field and the container live in HBM
+                when the step starts (compress_to a device buffer, then
+                decompress_into a device array).  Reported as the harmonic
+                combination 2·N·s_T / (t_compress + t_decompress), i.e. the
+                uncompressed GB/s of a round trip; compress and decompress GB/s
+                are also reported on their own.
+  * ``e2e``     the same step through the public API with pinned HOST buffers:
+                H2D of the input + D2H of the container (compress), H2D of the
+                container + D2H of the output (decompress), all inside the
+                timed region.
+
+Workload at N=1: BASELINE.json configs[1], 513^3 f32 synthetic multisine
+(test_support.hpp:43-62), L-inf REL 1e-4, codec 2 (varint + Huffman).  The
+input (540 MB) and output exceed the 126 MB L2, so no L2 flush is needed.
+At N>1 every rank compresses its own field of that shape (weak scaling; the
+path shards into independent containers) and the compressed sizes are
+all-gathered over NCCL to place each rank's container in one stream.
+
+``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref: /root/reference/proj/src compiled unmodified) on the host cores
+on a bounded slab sample of the same field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "compress/decompress GB/s (round trip, uncompressed bytes)"
+UNIT = "GB/s"
+
+WORKLOADS = {
+    # name: (shape, dtype, tol, norm, s, mode)
+    "cfg2_513cubed_f32_inf_rel1e-4": ((513, 513, 513), "f32", 1e-4, 0, 0.0, 1),
+    "cfg1_65cubed_f64_inf_rel1e-3": ((65, 65, 65), "f64", 1e-3, 0, 0.0, 1),
+    "cfg3_8193sq_f64_s1_rel1e-3": ((8193, 8193), "f64", 1e-3, 1, 1.0, 1),
+    "cfg4_1025cubed_f64_inf_rel1e-5": ((1025, 1025, 1025), "f64", 1e-5, 0, 0.0, 1),
+}
+DEFAULT_WORKLOAD = "cfg2_513cubed_f32_inf_rel1e-4"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# synthetic field: multisine (test_support.hpp:43-62), evaluated in f64
+
+
+def multisine_torch(shape, device):
+    import torch
+
+    d = len(shape)
+    t = [torch.linspace(0.0, 1.0, n, dtype=torch.float64, device=device) if n > 1 else
+         torch.zeros(1, dtype=torch.float64, device=device) for n in shape]
+
+    def ax(a):
+        if a >= d:
+            return torch.zeros((1,) * d, dtype=torch.float64, device=device)
+        v = t[a]
+        return v.reshape([-1 if k == a else 1 for k in range(d)])
+
+    t0, t1, t2, t3 = ax(0), ax(1), ax(2), ax(3)
+    two_pi = 2.0 * np.pi
+    u = torch.sin(two_pi * (t0 + 0.7 * t1 + 0.4 * t2))
+    u = u + 0.5 * torch.sin(two_pi * (3.0 * t0 + 2.2 * t1))
+    u = u + 0.25 * torch.sin(two_pi * (7.0 * t0 + 5.0 * t3))
+    u = u + 1.5 * t0
+    return u.expand(*shape).contiguous()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md "clocks DURING the timed region")
+
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the reference library on host cores
+
+
+def cpu_reference_step(ref, u_np, tol, norm, s, mode):
+    t0 = time.perf_counter()
+    blob = ref.compress(u_np, tol, norm, s, mode, 2)
+    t1 = time.perf_counter()
+    ref.decompress(blob)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, len(blob)
+
+
+def cpu_sample(u_full_np, rows):
+    return np.ascontiguousarray(u_full_np[:rows])
+
+
+def cpu_baseline_measure(u_np_full, spec, budget_s=20.0):
+    """Reference library (oracle/_ref, else the C restatement) on a bounded slab sample."""
+    from oracle import binding
+
+    kind = "reference" if binding.available("reference") else "restatement"
+    ref = binding.get(kind)
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    tol, norm, s, mode = spec
+    rows = min(u_np_full.shape[0], 65)
+    sample = cpu_sample(u_np_full, rows)
+    tc = td = 0.0
+    reps = 0
+    t_start = time.perf_counter()
+    while reps < 5 and (reps == 0 or time.perf_counter() - t_start < budget_s):
+        a, b, _ = cpu_reference_step(ref, sample, tol, norm, s, mode)
+        tc += a
+        td += b
+        reps += 1
+    nbytes = sample.nbytes
+    return {
+        "value": 2.0 * nbytes * reps / (tc + td) / 1e9, "unit": UNIT, "cores": cores,
+        "kind": "reference" if kind == "reference" else "port",
+        "sample": f"{reps}x compress+decompress of the first {rows} rows ({'x'.join(map(str, sample.shape))} "
+                  f"{sample.dtype}, {nbytes / 1e6:.1f} MB) of the workload field, codec 2",
+        "compress_gbs": nbytes * reps / tc / 1e9, "decompress_gbs": nbytes * reps / td / 1e9,
+    }
+
+
+def run_reference_arm(args, workload):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    shape, dts, tol, norm, s, mode = WORKLOADS[workload]
+    from oracle import binding
+
+    kind = "reference" if binding.available("reference") else "restatement"
+    ref = binding.get(kind)
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    # the field, evaluated on the host in f64 exactly like the GPU arm's formula
+    import torch
+
+    u = multisine_torch(shape, "cpu")
+    u_np = u.numpy().astype(np.float32 if dts == "f32" else np.float64)
+    rows = min(shape[0], 65)
+    sample = cpu_sample(u_np, rows)
+    for _ in range(args.warmup):
+        cpu_reference_step(ref, sample, tol, norm, s, mode)
+    tc = td = 0.0
+    clen = 0
+    for _ in range(args.steps):
+        a, b, clen = cpu_reference_step(ref, sample, tol, norm, s, mode)
+        tc += a
+        td += b
+    nbytes = sample.nbytes
+    value = 2.0 * nbytes * args.steps / (tc + td) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": (tc + td) / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (f32 data widened)",
+        "data": "synthetic multisine (test_support.hpp:43-62)",
+        "config": {"workload": workload, "sample_rows": rows, "codec": "huffman", "threads": cores},
+        "compress_gbs": nbytes * args.steps / tc / 1e9, "decompress_gbs": nbytes * args.steps / td / 1e9,
+        "ratio": nbytes / clen,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
+                         "kind": "reference" if kind == "reference" else "port",
+                         "sample": f"first {rows} rows of the workload field per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        return run_reference_arm(args, args.workload)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2401_05994_b200 as mg
+
+    mg.set_device(local)
+    stream = torch.cuda.current_stream()
+    mg.set_stream(stream.cuda_stream)
+
+    shape, dts, tol, norm, s, mode = WORKLOADS[args.workload]
+    tdt = torch.float32 if dts == "f32" else torch.float64
+    N = int(np.prod(shape))
+    esz = 4 if dts == "f32" else 8
+    nbytes = N * esz
+    u = multisine_torch(shape, f"cuda:{local}").to(tdt)
+    grid = mg.make_grid(shape)
+    spec = mg.ErrorSpec(tol, mg.Norm(norm), s, mg.Mode(mode))
+    cap = nbytes * 2 + (1 << 20)
+    dst = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    out = torch.empty(shape, dtype=tdt, device="cuda")
+
+    def gather_sizes(n):
+        if world == 1:
+            return [n]
+        t = torch.tensor([n], dtype=torch.int64, device="cuda")
+        allt = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        return [int(x.item()) for x in allt]
+
+    def step_device():
+        n = mg.compress_to(u, dst, grid, spec, mg.Codec.huffman)
+        sizes = gather_sizes(n)
+        mg.decompress_into(dst[:n], out)
+        return n, sizes
+
+    # warm-up (also builds the hierarchy tables / workspaces)
+    for _ in range(args.warmup):
+        clen, sizes = step_device()
+    torch.cuda.synchronize()
+
+    # correctness of the measured path: error bound on the reconstruction
+    u64 = u.double()
+    vmin, vmax = float(u64.min()), float(u64.max())
+    tau = tol * (vmax - vmin) if mode == 1 and norm == 0 else tol
+    max_err = float((out.double() - u64).abs().max())
+    del u64
+
+    # timed region: K steps, device-resident, per-phase CUDA events on the launching stream
+    mg.set_profiling(True)
+    phase_ms, phase_bytes, phase_n = {}, {}, {}
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = mg.launch_count()
+    g0 = torch.cuda.Event(enable_timing=True)
+    g1 = torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for k in range(args.steps):
+        a, b, c = ev[k]
+        a.record(stream)
+        n = mg.compress_to(u, dst, grid, spec, mg.Codec.huffman)
+        for name, ms, by in mg.last_profile():
+            phase_ms[name] = phase_ms.get(name, 0.0) + ms
+            phase_bytes[name] = phase_bytes.get(name, 0.0) + by
+            phase_n[name] = phase_n.get(name, 0) + 1
+        gather_sizes(n)
+        b.record(stream)
+        mg.decompress_into(dst[:n], out)
+        for name, ms, by in mg.last_profile():
+            phase_ms[name] = phase_ms.get(name, 0.0) + ms
+            phase_bytes[name] = phase_bytes.get(name, 0.0) + by
+            phase_n[name] = phase_n.get(name, 0) + 1
+        c.record(stream)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = mg.launch_count() - l0
+    clk = clocks.stop()
+    mg.set_profiling(False)
+    total_ms = g0.elapsed_time(g1)
+    tc = sum(ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps))
+    td = sum(ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps))
+    if world > 1:
+        t = torch.tensor([total_ms, tc, td], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, tc, td = (float(x) for x in t.tolist())
+    ms_step = total_ms / args.steps
+    value = 2.0 * nbytes * world / (ms_step * 1e-3) / 1e9
+    comp_gbs = nbytes * world * args.steps / (tc * 1e-3) / 1e9
+    decomp_gbs = nbytes * world * args.steps / (td * 1e-3) / 1e9
+    clen = n
+
+    # dominant kernel phase (CUDA events on the library stream = the torch stream)
+    peak, peak_src = peaks()
+    kernel_phases = {k: v for k, v in phase_ms.items() if not k.startswith(("h2d", "d2h"))}
+    dom = max(kernel_phases, key=kernel_phases.get)
+    dom_ms = phase_ms[dom] / phase_n[dom]
+    dom_bytes = phase_bytes[dom] / phase_n[dom]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    step_alg = (2 * nbytes + 2 * clen)  # B_c + B_d
+    phases = {k: {"ms": round(phase_ms[k] / args.steps, 4),
+                  "gbs": round(phase_bytes[k] / args.steps / (phase_ms[k] / args.steps * 1e-3) / 1e9, 1)
+                  if phase_ms[k] > 0 else None}
+              for k in sorted(phase_ms, key=phase_ms.get, reverse=True)}
+
+    # e2e: public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        u_host = u.cpu().pin_memory()
+        dst_h = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        out_h = torch.empty(shape, dtype=tdt).pin_memory()
+        for _ in range(2):
+            n_h = mg.compress_to(u_host, dst_h, grid, spec, mg.Codec.huffman)
+            mg.decompress_into(dst_h[:n_h], out_h)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(args.steps):
+            n_h = mg.compress_to(u_host, dst_h, grid, spec, mg.Codec.huffman)
+            gather_sizes(n_h)
+            mg.decompress_into(dst_h[:n_h], out_h)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = h0.elapsed_time(h1)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": 2.0 * nbytes * world * args.steps / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes + n_h, "d2h_bytes_per_step": n_h + nbytes,
+               "ms_per_step": e_ms / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        u_np = u.cpu().numpy()
+        cpu = cpu_baseline_measure(u_np, (tol, norm, s, mode))
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64 (f32 data widened to f64 in registers)",
+            "data": "synthetic multisine field (test_support.hpp:43-62), generated on the GPU",
+            "config": {"workload": args.workload, "shape": list(shape), "elem": dts, "tol": tol,
+                       "norm": "inf" if norm == 0 else f"s={s}", "mode": "rel" if mode else "abs",
+                       "codec": "huffman", "per_rank": "one field per rank (independent containers)",
+                       "l2": "inputs/outputs exceed the 126 MB L2; no flush"},
+            "compress_gbs": comp_gbs, "decompress_gbs": decomp_gbs,
+            "ratio": nbytes / clen, "compressed_bytes": clen,
+            "max_err": max_err, "tau": tau, "bound_met": max_err <= tau,
+            "step_alg_roofline_frac": step_alg * world / (ms_step * 1e-3) / 1e9 / peak / world,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": dom_bytes,
+                         "ms_per_launch": dom_ms, "peak_source": peak_src},
+            "phases_ms_per_step": phases,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

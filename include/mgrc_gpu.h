@@ -129,6 +129,8 @@ MGRC_GPU_API int mgrc_gpu_set_profiling(int on);
 MGRC_GPU_API int mgrc_gpu_profile_count(void);
 MGRC_GPU_API int mgrc_gpu_profile_entry(int i, const char** name, double* ms, double* bytes);
 MGRC_GPU_API const char* mgrc_gpu_version(void);
+/* Kernels launched by the calling thread through this library so far. */
+MGRC_GPU_API uint64_t mgrc_gpu_launch_count(void);
 
 #ifdef __cplusplus
 }

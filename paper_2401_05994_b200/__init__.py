@@ -31,7 +31,7 @@ __all__ = [
     "Norm", "Mode", "Codec", "DType", "ErrorSpec", "TensorGrid", "ContainerInfo", "MgrcError", "make_grid",
     "compress", "compress_to", "decompress", "decompress_into", "inspect", "describe", "plan_chunks",
     "compress_chunked", "decompress_chunked", "field_stats", "set_device", "set_stream", "set_profiling",
-    "last_profile", "ERRC_NAMES",
+    "last_profile", "launch_count", "ERRC_NAMES",
 ]
 
 
@@ -334,6 +334,11 @@ def set_stream(stream_handle: Optional[int]) -> None:
 
 def set_profiling(on: bool) -> None:
     _check(_lib.lib().mgrc_gpu_set_profiling(1 if on else 0))
+
+
+def launch_count() -> int:
+    """Kernels launched by this thread through libmgrc_gpu.so so far."""
+    return int(_lib.lib().mgrc_gpu_launch_count())
 
 
 def last_profile() -> list:

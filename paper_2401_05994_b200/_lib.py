@@ -51,6 +51,7 @@ SIGNATURES = {
     "mgrc_gpu_profile_entry": (C.c_int, [C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]),
     "mgrc_gpu_version": (C.c_char_p, []),
+    "mgrc_gpu_launch_count": (C.c_uint64, []),
 }
 
 _lib = None

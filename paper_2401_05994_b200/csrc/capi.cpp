@@ -152,6 +152,7 @@ extern "C" {
 const char* mgrc_gpu_version(void) { return "mgrc_gpu 0.1 (sm_100a)"; }
 const char* mgrc_gpu_last_error(void) { return g_last_error.c_str(); }
 void mgrc_gpu_free(void* p) { std::free(p); }
+uint64_t mgrc_gpu_launch_count(void) { return launch_count(); }
 
 int mgrc_gpu_set_device(int device) {
   return guarded([&] {

@@ -33,7 +33,12 @@ using namespace dev;
     if (e_ != cudaSuccess) raise(Errc::cuda, std::string(#x) + ": " + cudaGetErrorString(e_));       \
   } while (0)
 
+static thread_local unsigned long long g_launches = 0;  // kernels launched by this thread
+
+unsigned long long launch_count() { return g_launches; }
+
 static void check_launch(const char* what) {
+  ++g_launches;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) raise(Errc::cuda, std::string(what) + ": " + cudaGetErrorString(e));
 }

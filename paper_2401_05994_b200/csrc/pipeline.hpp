@@ -54,6 +54,9 @@ ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len);
 
 bool is_device_pointer(const void* p);
 
+// Number of kernels this thread has launched through the library.
+unsigned long long launch_count();
+
 // Input statistics used by the multi-GPU driver for global REL normalisation.
 struct FieldStats {
   double min, max;
