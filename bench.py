@@ -271,7 +271,10 @@ def main():
     import paper_2401_05994_b200 as mg
 
     mg.set_device(local)
-    stream = torch.cuda.current_stream()
+    # one non-default stream shared by torch and the library, so the CUDA
+    # events below are recorded on the stream the kernels are launched on
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     mg.set_stream(stream.cuda_stream)
 
     shape, dts, tol, norm, s, mode = WORKLOADS[args.workload]

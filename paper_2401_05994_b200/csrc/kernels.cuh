@@ -26,6 +26,12 @@ struct AxisTab {
   const uint32_t* right;
   const double* wl;
   const double* wr;
+  // Compact level-(L-1) box ("coarse box"): every node with tag < L lies in
+  // it, and so does every corner of a tag-L node.
+  const uint32_t* cpos;   // finest index -> position in the level-(L-1) set (coarse indices only)
+  const uint32_t* cl;     // tag-L-fresh index -> cpos[left]
+  const uint32_t* cr;     // tag-L-fresh index -> cpos[right]
+  const uint32_t* cset;   // position in the level-(L-1) set -> finest index
 };
 
 struct GridDev {
@@ -34,6 +40,9 @@ struct GridDev {
   uint64_t stride[4];
   uint64_t N;
   AxisTab ax[4];
+  uint32_t cshape[4];    // coarse-box shape
+  uint64_t cstride[4];
+  uint64_t Nc;
 };
 
 struct BoxDev {  // level-l box: the tensor product of the level-l index sets
@@ -498,6 +507,293 @@ __global__ void __launch_bounds__(256) k_level_weighted(GridDev g, Widths lw, co
 }
 
 // ---------------------------------------------------------------------------
+// Compress, v2: the a-posteriori check without a full residual array.
+//
+// The inverse of the residuals (container.cpp:96-110, error_control.cpp:103)
+// only needs e on the coarse box (tag < L, 1/2^d of the grid) before the
+// finest level: e(tag L node) = r + I(e)(node), and every corner of a tag-L
+// node lies in the coarse box.  So
+//   (a) k_coarse_resid   r on the coarse box, compact (Nc doubles)
+//   (b) inverse levels 1..L-1 on the compact box (k_inverse_box/finest on the
+//       compact GridDev), in place: ec = e on the coarse box
+//   (c) k_fine           ONE pass over u: forward + quantise + zigzag store +
+//       varint histogram + e = r + I(ec) (or ec) + the check epilogue.
+// The residual array of v1 (8 B/elt written and read back) disappears.
+
+__device__ __forceinline__ uint64_t coarse_index(const GridDev& g, const uint32_t (&i)[4], int D) {
+  uint64_t o = 0;
+  for (int a = 0; a < D; ++a) o += static_cast<uint64_t>(__ldg(g.ax[a].cpos + i[a])) * g.cstride[a];
+  return o;
+}
+
+// interp() of a tag-L node over the compact coarse box (same corner order).
+template <int D>
+__device__ __forceinline__ double interp_coarse(const GridDev& g, const uint32_t (&i)[4], int tag,
+                                                const double* __restrict__ ec) {
+  uint32_t F = 0;
+  uint64_t base = 0;
+  double wl[D], wr[D];
+  uint64_t ol[D], orr[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    wl[a] = wr[a] = 0.0;
+    ol[a] = orr[a] = 0;
+    if (__ldg(g.ax[a].lvl + i[a]) == tag) {
+      F |= 1u << a;
+      wl[a] = __ldg(g.ax[a].wl + i[a]);
+      wr[a] = __ldg(g.ax[a].wr + i[a]);
+      ol[a] = static_cast<uint64_t>(__ldg(g.ax[a].cl + i[a])) * g.cstride[a];
+      orr[a] = static_cast<uint64_t>(__ldg(g.ax[a].cr + i[a])) * g.cstride[a];
+    } else {
+      base += static_cast<uint64_t>(__ldg(g.ax[a].cpos + i[a])) * g.cstride[a];
+    }
+  }
+  double acc = 0.0;
+  uint32_t s = 0;
+  do {
+    double w = 1.0;
+    uint64_t off = base;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+      if ((F >> a) & 1u) {
+        const bool right = (s >> a) & 1u;
+        w = __dmul_rn(w, right ? wr[a] : wl[a]);
+        off += right ? orr[a] : ol[a];
+      }
+    acc = __dadd_rn(acc, __dmul_rn(w, ec[off]));
+    s = (s - F) & F;
+  } while (s);
+  return acc;
+}
+
+// (a) residuals of the coarse-box nodes, compact layout.
+template <int D, typename T>
+__global__ void __launch_bounds__(256) k_coarse_resid(GridDev g, Widths W, const T* __restrict__ u,
+                                                      double* __restrict__ ec) {
+  auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < g.Nc; j += step) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    uint64_t q = j, n = 0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      const uint64_t qq = q / g.cshape[a];
+      i[a] = __ldg(g.ax[a].cset + (q - qq * g.cshape[a]));
+      n += static_cast<uint64_t>(i[a]) * g.stride[a];
+      q = qq;
+    }
+    const int tag = node_tag<D>(g, i);
+    double c = static_cast<double>(u[n]);
+    if (tag > 0) c = __dsub_rn(c, interp<D>(g, i, tag, ld));
+    const double delta = W.w[tag];
+    const double scaled = __ddiv_rn(c, delta);
+    double r = 0.0;
+    if (fabs(scaled) < 9223372036854775808.0)
+      r = __dsub_rn(c, __dmul_rn(__ll2double_rn(__double2ll_rn(scaled)), delta));
+    ec[j] = r;
+  }
+}
+
+// Check epilogues of the fused pass: (n, e, source value widened, reduction).
+struct ChkMaxAbs {  // max|e| (error_control.cpp:105, exec.cpp:75-87)
+  __device__ __forceinline__ void operator()(uint64_t, double e, double, double& red) const {
+    red = fmax(red, fabs(e));
+  }
+};
+struct ChkCastMaxAbs {  // f32: max|src − (double)(float)(u − e)| (container.cpp:96-107)
+  __device__ __forceinline__ void operator()(uint64_t, double e, double s, double& red) const {
+    red = fmax(red, fabs(__dsub_rn(s, static_cast<double>(__double2float_rn(__dsub_rn(s, e))))));
+  }
+};
+struct ChkStore {  // S(0): e stored for the ordered 4096-block RMS
+  double* out;
+  __device__ __forceinline__ void operator()(uint64_t n, double e, double, double&) const { out[n] = e; }
+};
+struct ChkCastStore {  // S(0), f32: the cast error stored
+  double* out;
+  __device__ __forceinline__ void operator()(uint64_t n, double e, double s, double&) const {
+    out[n] = __dsub_rn(s, static_cast<double>(__double2float_rn(__dsub_rn(s, e))));
+  }
+};
+struct ChkLevelWeighted {  // S(s≠0): Σ 2^{2s(tag−L)} r² (error_control.cpp:72-100), r passed as e
+  __device__ __forceinline__ void operator()(uint64_t, double, double, double&) const {}
+};
+
+// (c) the fused pass.  LW: level-weighted estimator (no inverse needed).
+template <int D, typename T, typename Z, class Chk, bool LW>
+__global__ void __launch_bounds__(256) k_fine(GridDev g, Widths W, const T* __restrict__ u, Z* __restrict__ zz,
+                                              unsigned long long* __restrict__ hist, QuantFlags* flags,
+                                              const double* __restrict__ ec, Chk chk,
+                                              unsigned long long* __restrict__ red_out, Widths lw,
+                                              double* __restrict__ partials, int vec_ok) {
+  __shared__ uint32_t sh[256];
+  __shared__ double sred[256 / 32];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
+  __syncthreads();
+  uint32_t hsym = 0, hcnt = 0;
+  unsigned long long ovf = 0;
+  unsigned wide = 0;
+  double red = 0.0;
+  auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
+  const uint64_t nruns = (g.N + 3) / 4;
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t run = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; run < nruns; run += step) {
+    const uint64_t e0 = run * 4;
+    const int cnt = static_cast<int>(umin64(4, g.N - e0));
+    uint32_t i[4] = {0, 0, 0, 0};
+    decompose<D>(g, e0, i);
+    double cv[4] = {0, 0, 0, 0};
+    if (cnt == 4 && vec_ok) {
+      load4<T>(u + e0, cv);
+    } else {
+      for (int k = 0; k < cnt; ++k) cv[k] = static_cast<double>(u[e0 + k]);
+    }
+    uint64_t zv[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < cnt) {
+        const int tag = node_tag<D>(g, i);
+        double c = cv[k];
+        if (tag > 0) c = __dsub_rn(c, interp<D>(g, i, tag, ld));
+        const double delta = W.w[tag];
+        const double scaled = __ddiv_rn(c, delta);
+        double r = 0.0;
+        if (!(fabs(scaled) < 9223372036854775808.0)) {
+          ++ovf;
+        } else {
+          const long long q = __double2ll_rn(scaled);
+          r = __dsub_rn(c, __dmul_rn(__ll2double_rn(q), delta));
+          const uint64_t z = zigzag(q);
+          if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
+          zv[k] = z;
+          hist_varint(sh, z, hsym, hcnt);
+        }
+        if (LW) {
+          red = __dadd_rn(red, __dmul_rn(lw.w[tag], __dmul_rn(r, r)));
+        } else {
+          double e;
+          if (g.L == 0) e = r;
+          else if (tag == g.L) e = __dadd_rn(r, interp_coarse<D>(g, i, tag, ec));
+          else e = ec[coarse_index(g, i, D)];
+          chk(e0 + k, e, cv[k], red);
+        }
+        advance<D>(g, i);
+      }
+    }
+    if (cnt == 4 && vec_ok) {
+      store4z(zz + e0, zv);
+    } else {
+      for (int k = 0; k < cnt; ++k) zz[e0 + k] = static_cast<Z>(zv[k]);
+    }
+  }
+  hist_flush(sh, hsym, hcnt);
+  if (ovf) atomicAdd(&flags->overflow, ovf);
+  if (wide) atomicOr(&flags->wide, 1u);
+  if (LW) {  // fixed-order block sum → partials[block] (deterministic for a fixed grid)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) red = __dadd_rn(red, __shfl_down_sync(0xffffffffu, red, o));
+    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = red;
+  } else if (red_out) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) red = fmax(red, __shfl_xor_sync(0xffffffffu, red, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
+  }
+  __syncthreads();
+  if (LW && threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 256 / 32; ++w) t = __dadd_rn(t, sred[w]);
+    partials[blockIdx.x] = t;
+  }
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back (single-pass prefix) helpers.  A tile publishes
+// (flag << 62 | value): 1 = its own aggregate, 2 = inclusive prefix.
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = (1ull << 62) - 1;
+
+// Called by warp 0 of the tile; returns the exclusive prefix of tile t.
+__device__ __forceinline__ unsigned long long lookback(unsigned long long* status, uint64_t t,
+                                                       unsigned long long aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (t == 0) {
+    if (lane == 0) atomicExch(status, kLbInc | aggregate);
+    return 0;
+  }
+  if (lane == 0) atomicExch(status + t, kLbAgg | aggregate);
+  unsigned long long excl = 0;
+  int64_t base = static_cast<int64_t>(t) - 1;
+  for (;;) {
+    const int64_t j = base - lane;
+    unsigned long long v = kLbInc;  // beyond tile 0: acts as a zero inclusive
+    if (j >= 0) {
+      do {
+        v = *reinterpret_cast<volatile unsigned long long*>(status + j);
+      } while ((v >> 62) == 0);
+    }
+    // lanes ordered from nearest predecessor; find the first inclusive
+    const unsigned inc_mask = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+    const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+    unsigned long long contrib = lane <= first_inc ? (v & kLbMask) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+    excl += contrib;
+    if (first_inc < 32) break;
+    base -= 32;
+  }
+  if (lane == 0) atomicExch(status + t, kLbInc | (excl + aggregate));
+  return excl;
+}
+
+// Single-pass exclusive scan of u64 counts (values < 2^62); out[n] = total.
+// Tiles are claimed through a ticket so that predecessors always run first.
+constexpr int kScanThreads = 256, kScanPer = 8, kScanTile = kScanThreads * kScanPer;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_lb(const unsigned long long* __restrict__ in,
+                                                          unsigned long long* __restrict__ out, uint64_t n,
+                                                          unsigned long long* status, unsigned int* ticket) {
+  __shared__ unsigned long long wsum[kScanThreads / 32];
+  __shared__ unsigned long long s_prefix;
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint64_t t = s_tile;
+  const uint64_t base = t * kScanTile + threadIdx.x * kScanPer;
+  unsigned long long v[kScanPer], mine = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    v[k] = base + k < n ? in[base + k] : 0;
+    mine += v[k];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 1; w < kScanThreads / 32; ++w) wsum[w] += wsum[w - 1];
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long p = lookback(status, t, wsum[kScanThreads / 32 - 1]);
+    if (lane == 0) s_prefix = p;
+  }
+  __syncthreads();
+  unsigned long long run = s_prefix + (warp ? wsum[warp - 1] : 0) + incl - mine;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += v[k];
+  }
+  const uint64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  if (t == ntiles - 1 && threadIdx.x == 0) out[n] = s_prefix + wsum[kScanThreads / 32 - 1];
+}
+
+// ---------------------------------------------------------------------------
 // Lossless stage.  Codec 2 codes every LEB128 byte of zigzag(q) with the
 // canonical Huffman code (codec.cpp:399-418, MSB-first, zero padded); codec 1
 // is the same packer with the identity 8-bit code.
@@ -657,6 +953,129 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const Z* __restrict__ zz,
     } else {
       out[gw0 + w] = val;
     }
+  }
+}
+
+// Single-pass Huffman / varint packer: per-value bit counts → block scan →
+// look-back for the tile's start bit → codes OR-ed into a shared-memory word
+// image → interior words stored directly; the first and last word of the
+// tile (possibly shared with a neighbour) go to edge slots merged by
+// k_pack_edges.  Output words hold the stream MSB-first in memory byte order.
+template <typename Z>
+__global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ zz, uint64_t n,
+                                                          const uint32_t* __restrict__ code_g,
+                                                          const uint8_t* __restrict__ len_g,
+                                                          unsigned long long* status, unsigned int* ticket,
+                                                          unsigned long long* __restrict__ tile_start,
+                                                          uint32_t* __restrict__ edge_first,
+                                                          uint32_t* __restrict__ edge_last,
+                                                          uint32_t* __restrict__ out) {
+  extern __shared__ uint32_t words[];
+  __shared__ uint32_t code[256];
+  __shared__ uint8_t len[256];
+  __shared__ unsigned long long wsum[kPackThreads / 32];
+  __shared__ unsigned long long s_prefix;
+  __shared__ uint32_t s_tile;
+  code[threadIdx.x] = code_g[threadIdx.x];
+  len[threadIdx.x] = len_g[threadIdx.x];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint64_t t = s_tile;
+  const uint64_t base = t * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
+  uint64_t z[kPackPerThread];
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int k = 0; k < kPackPerThread; ++k) {
+    z[k] = base + k < n ? static_cast<uint64_t>(zz[base + k]) : 0;
+    if (base + k < n) mine += varint_bits(z[k], len);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 1; w < kPackThreads / 32; ++w) wsum[w] += wsum[w - 1];
+  __syncthreads();
+  const unsigned long long tile_total = wsum[kPackThreads / 32 - 1];
+  if (warp == 0) {
+    const unsigned long long p = lookback(status, t, tile_total);
+    if (lane == 0) s_prefix = p;
+  }
+  __syncthreads();
+  const unsigned long long tile_start_bit = s_prefix;
+  const uint32_t shift0 = static_cast<uint32_t>(tile_start_bit & 31);
+  const uint64_t nwords = (shift0 + tile_total + 31) >> 5;
+  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0;
+  __syncthreads();
+  uint64_t p = shift0 + (warp ? wsum[warp - 1] : 0) + incl - mine;
+#pragma unroll
+  for (int k = 0; k < kPackPerThread; ++k) {
+    if (base + k >= n) break;
+    uint64_t v = z[k];
+    for (;;) {
+      const uint32_t sym = v >= 0x80 ? static_cast<uint32_t>((v & 0x7F) | 0x80) : static_cast<uint32_t>(v);
+      const uint32_t l = len[sym], c = code[sym];
+      const uint32_t w = static_cast<uint32_t>(p >> 5), o = static_cast<uint32_t>(p & 31);
+      if (o + l <= 32) {
+        atomicOr(&words[w], c << (32 - o - l));
+      } else {
+        const uint32_t spill = o + l - 32;
+        atomicOr(&words[w], c >> spill);
+        atomicOr(&words[w + 1], c << (32 - spill));
+      }
+      p += l;
+      if (v < 0x80) break;
+      v >>= 7;
+    }
+  }
+  __syncthreads();
+  const uint64_t gw0 = tile_start_bit >> 5;
+  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) {
+    const uint32_t val = bswap32(words[w]);
+    if (w == 0) edge_first[t] = val;
+    else if (w == nwords - 1) edge_last[t] = val;
+    else out[gw0 + w] = val;
+  }
+  if (threadIdx.x == 0) {
+    tile_start[t] = tile_start_bit;
+    if (nwords <= 1) edge_last[t] = 0;
+    if (nwords == 0) edge_first[t] = 0;
+  }
+}
+
+// Merges the edge words: word W receives the OR of every tile's first / last
+// word that falls on W (only neighbours can share a word: a full tile spans
+// ≥ 2048 bits).  tile_start has ntiles+1 entries (the last = total bits).
+__global__ void k_pack_edges(const unsigned long long* __restrict__ tile_start, uint64_t ntiles,
+                             const uint32_t* __restrict__ edge_first, const uint32_t* __restrict__ edge_last,
+                             uint32_t* __restrict__ out) {
+  const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (t >= ntiles) return;
+  auto first_w = [&](uint64_t s) { return tile_start[s] >> 5; };
+  auto last_w = [&](uint64_t s) {  // word of the tile's last bit (tile non-empty)
+    return (tile_start[s + 1] - 1) >> 5;
+  };
+  auto nonempty = [&](uint64_t s) { return tile_start[s + 1] > tile_start[s]; };
+  auto contrib = [&](uint64_t s, uint64_t W) -> uint32_t {
+    if (!nonempty(s)) return 0;
+    if (first_w(s) == W) return edge_first[s];
+    if (last_w(s) == W) return edge_last[s];
+    return 0;
+  };
+  if (!nonempty(t)) return;
+  const uint64_t Ws[2] = {first_w(t), last_w(t)};
+  for (int k = 0; k < 2; ++k) {
+    if (k == 1 && Ws[1] == Ws[0]) break;
+    const uint64_t W = Ws[k];
+    uint32_t v = contrib(t, W);
+    if (t > 0) v |= contrib(t - 1, W);
+    if (t + 1 < ntiles) v |= contrib(t + 1, W);
+    out[W] = v;
   }
 }
 
@@ -850,6 +1269,7 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync(const uint32_t* __res
     decode_seq(w, T, lut, maxlen, start, end, s);
   }
   sexit[threadIdx.x] = valid ? s.exit : 0;
+  __syncthreads();  // every exit published before any neighbour reads it
   // intra-block resynchronisation
   for (;;) {
     const unsigned long long pe = threadIdx.x > 0 ? sexit[threadIdx.x - 1] : 0;

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <type_traits>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -101,13 +102,17 @@ struct PinnedBuf {
   }
 };
 
-// Device copy of a hierarchy's tables.
+// Device copy of a hierarchy's tables: the finest grid (g, boxes) and the
+// compact coarse box = the level-(L-1) box as a grid of its own (gc, cboxes)
+// carrying the same stencils, on which the coarse part of the inverse runs.
 struct DevHier {
   std::string key;
   Hierarchy h;
   DevBuf buf;
   GridDev g{};
-  std::vector<BoxDev> boxes;  // per level
+  std::vector<BoxDev> boxes;   // per level, finest-grid indices
+  GridDev gc{};                // coarse box (valid when h.L >= 1)
+  std::vector<BoxDev> cboxes;  // per level 0..L-1, compact indices
 };
 
 struct Scratch {  // small device-side results read back at sync points
@@ -128,7 +133,7 @@ class Context {
   bool profiling = false;
   std::vector<PhaseTime> profile;
   // workspace
-  DevBuf in, zz, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial;
+  DevBuf in, zz, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws;
   DevBuf scratch_d;
   PinnedBuf scratch_h, partial_h;
   std::unique_ptr<DevHier> hier;
@@ -232,64 +237,135 @@ static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
   dh->h = build_hierarchy(grid);
   const Hierarchy& h = dh->h;
   const int d = grid.d;
-  // layout: per axis [wl f64][wr f64][left u32][right u32][lvl u8], then sets
-  size_t total = 0;
+  const int L = h.L;
+  // host image of every table, then one upload
+  std::vector<uint8_t> host;
   auto align = [](size_t x) { return (x + 15) & ~size_t{15}; };
-  size_t off_ax[kMaxDims][5];
+  auto put = [&](const void* p, size_t n) {
+    const size_t off = host.size();
+    host.resize(align(off + n), 0);
+    if (n) std::memcpy(&host[off], p, n);
+    return off;
+  };
+  struct Off {
+    size_t wl, wr, left, right, lvl, cpos, cl, cr, cset;
+    size_t c_wl, c_wr, c_left, c_right, c_lvl;
+  } off[kMaxDims];
+  std::vector<std::vector<size_t>> off_set(L + 1, std::vector<size_t>(d)), off_cset(L + 1, std::vector<size_t>(d));
+  std::vector<uint32_t> csz(d, 0);
   for (int a = 0; a < d; ++a) {
     const size_t n = grid.shape[a];
-    off_ax[a][0] = total, total = align(total + 8 * n);
-    off_ax[a][1] = total, total = align(total + 8 * n);
-    off_ax[a][2] = total, total = align(total + 4 * n);
-    off_ax[a][3] = total, total = align(total + 4 * n);
-    off_ax[a][4] = total, total = align(total + n);
-  }
-  std::vector<std::vector<size_t>> off_set(h.L + 1, std::vector<size_t>(d));
-  for (int l = 0; l <= h.L; ++l)
-    for (int a = 0; a < d; ++a) {
-      off_set[l][a] = total;
-      total = align(total + 4 * h.sets[a][l].size());
+    off[a].wl = put(h.wl[a].data(), 8 * n);
+    off[a].wr = put(h.wr[a].data(), 8 * n);
+    off[a].left = put(h.left[a].data(), 4 * n);
+    off[a].right = put(h.right[a].data(), 4 * n);
+    off[a].lvl = put(h.lvl[a].data(), n);
+    if (L >= 1) {
+      const auto& cs = h.sets[a][L - 1];
+      csz[a] = static_cast<uint32_t>(cs.size());
+      std::vector<uint32_t> cpos(n, 0), cl(n, 0), cr(n, 0);
+      for (size_t p = 0; p < cs.size(); ++p) cpos[cs[p]] = static_cast<uint32_t>(p);
+      std::vector<double> cwl(cs.size()), cwr(cs.size());
+      std::vector<uint32_t> cleft(cs.size()), cright(cs.size());
+      std::vector<uint8_t> clvl(cs.size());
+      for (size_t i = 0; i < n; ++i)
+        if (h.lvl[a][i] == L) {  // finest-fresh: both neighbours are coarse
+          cl[i] = cpos[h.left[a][i]];
+          cr[i] = cpos[h.right[a][i]];
+        }
+      for (size_t p = 0; p < cs.size(); ++p) {
+        const uint32_t i = cs[p];
+        clvl[p] = h.lvl[a][i];
+        cwl[p] = h.wl[a][i];
+        cwr[p] = h.wr[a][i];
+        cleft[p] = h.lvl[a][i] > 0 ? cpos[h.left[a][i]] : 0;
+        cright[p] = h.lvl[a][i] > 0 ? cpos[h.right[a][i]] : 0;
+      }
+      off[a].cpos = put(cpos.data(), 4 * n);
+      off[a].cl = put(cl.data(), 4 * n);
+      off[a].cr = put(cr.data(), 4 * n);
+      off[a].cset = put(cs.data(), 4 * cs.size());
+      off[a].c_wl = put(cwl.data(), 8 * cs.size());
+      off[a].c_wr = put(cwr.data(), 8 * cs.size());
+      off[a].c_left = put(cleft.data(), 4 * cs.size());
+      off[a].c_right = put(cright.data(), 4 * cs.size());
+      off[a].c_lvl = put(clvl.data(), cs.size());
+      for (int l = 0; l < L; ++l) {
+        std::vector<uint32_t> cset_l;
+        for (uint32_t i : h.sets[a][l]) cset_l.push_back(cpos[i]);
+        off_cset[l][a] = put(cset_l.data(), 4 * cset_l.size());
+      }
     }
-  std::vector<uint8_t> host(total, 0);
-  for (int a = 0; a < d; ++a) {
-    const size_t n = grid.shape[a];
-    std::memcpy(&host[off_ax[a][0]], h.wl[a].data(), 8 * n);
-    std::memcpy(&host[off_ax[a][1]], h.wr[a].data(), 8 * n);
-    std::memcpy(&host[off_ax[a][2]], h.left[a].data(), 4 * n);
-    std::memcpy(&host[off_ax[a][3]], h.right[a].data(), 4 * n);
-    std::memcpy(&host[off_ax[a][4]], h.lvl[a].data(), n);
   }
-  for (int l = 0; l <= h.L; ++l)
-    for (int a = 0; a < d; ++a)
-      std::memcpy(&host[off_set[l][a]], h.sets[a][l].data(), 4 * h.sets[a][l].size());
-  uint8_t* dp = dh->buf.get<uint8_t>(total);
-  CK(cudaMemcpyAsync(dp, host.data(), total, cudaMemcpyHostToDevice, ctx.stream));
+  for (int l = 0; l <= L; ++l)
+    for (int a = 0; a < d; ++a) off_set[l][a] = put(h.sets[a][l].data(), 4 * h.sets[a][l].size());
+  uint8_t* dp = dh->buf.get<uint8_t>(std::max<size_t>(host.size(), 16));
+  CK(cudaMemcpyAsync(dp, host.data(), host.size(), cudaMemcpyHostToDevice, ctx.stream));
   CK(cudaStreamSynchronize(ctx.stream));
+  auto P64 = [&](size_t o) { return reinterpret_cast<const double*>(dp + o); };
+  auto P32 = [&](size_t o) { return reinterpret_cast<const uint32_t*>(dp + o); };
   GridDev& g = dh->g;
   std::memset(&g, 0, sizeof g);
   g.d = d;
-  g.L = h.L;
+  g.L = L;
   g.N = grid.count();
-  uint64_t st = 1;
+  uint64_t st = 1, cst = 1;
   for (int a = d - 1; a >= 0; --a) {
     g.shape[a] = static_cast<uint32_t>(grid.shape[a]);
     g.stride[a] = st;
     st *= grid.shape[a];
-    g.ax[a].wl = reinterpret_cast<const double*>(dp + off_ax[a][0]);
-    g.ax[a].wr = reinterpret_cast<const double*>(dp + off_ax[a][1]);
-    g.ax[a].left = reinterpret_cast<const uint32_t*>(dp + off_ax[a][2]);
-    g.ax[a].right = reinterpret_cast<const uint32_t*>(dp + off_ax[a][3]);
-    g.ax[a].lvl = dp + off_ax[a][4];
+    g.ax[a].wl = P64(off[a].wl);
+    g.ax[a].wr = P64(off[a].wr);
+    g.ax[a].left = P32(off[a].left);
+    g.ax[a].right = P32(off[a].right);
+    g.ax[a].lvl = dp + off[a].lvl;
+    if (L >= 1) {
+      g.cshape[a] = csz[a];
+      g.cstride[a] = cst;
+      cst *= csz[a];
+      g.ax[a].cpos = P32(off[a].cpos);
+      g.ax[a].cl = P32(off[a].cl);
+      g.ax[a].cr = P32(off[a].cr);
+      g.ax[a].cset = P32(off[a].cset);
+    }
   }
-  dh->boxes.resize(h.L + 1);
-  for (int l = 0; l <= h.L; ++l) {
+  g.Nc = L >= 1 ? cst : 0;
+  dh->boxes.resize(L + 1);
+  for (int l = 0; l <= L; ++l) {
     BoxDev& b = dh->boxes[l];
     std::memset(&b, 0, sizeof b);
     b.count = 1;
     for (int a = 0; a < d; ++a) {
-      b.set[a] = reinterpret_cast<const uint32_t*>(dp + off_set[l][a]);
+      b.set[a] = P32(off_set[l][a]);
       b.n[a] = static_cast<uint32_t>(h.sets[a][l].size());
       b.count *= b.n[a];
+    }
+  }
+  if (L >= 1) {
+    GridDev& c = dh->gc;
+    std::memset(&c, 0, sizeof c);
+    c.d = d;
+    c.L = L - 1;
+    c.N = g.Nc;
+    for (int a = 0; a < d; ++a) {
+      c.shape[a] = g.cshape[a];
+      c.stride[a] = g.cstride[a];
+      c.ax[a].wl = P64(off[a].c_wl);
+      c.ax[a].wr = P64(off[a].c_wr);
+      c.ax[a].left = P32(off[a].c_left);
+      c.ax[a].right = P32(off[a].c_right);
+      c.ax[a].lvl = dp + off[a].c_lvl;
+    }
+    dh->cboxes.resize(L);
+    for (int l = 0; l < L; ++l) {
+      BoxDev& b = dh->cboxes[l];
+      std::memset(&b, 0, sizeof b);
+      b.count = 1;
+      for (int a = 0; a < d; ++a) {
+        b.set[a] = P32(off_cset[l][a]);
+        b.n[a] = static_cast<uint32_t>(h.sets[a][l].size());
+        b.count *= b.n[a];
+      }
     }
   }
   ctx.hier = std::move(dh);
@@ -353,6 +429,30 @@ struct InvFinest {
       const int blocks = grid_blocks((g.N + 3) / 4, 256);
       k_inverse_finest<D, Src, Epi, SKIP><<<blocks, 256, 0, s>>>(g, src, v, epi, red);
       check_launch("k_inverse_finest");
+    }
+  };
+};
+
+template <typename T>
+struct CoarseResid {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const T* u, double* ec) {
+      k_coarse_resid<D, T><<<grid_blocks(g.Nc, 256), 256, 0, s>>>(g, W, u, ec);
+      check_launch("k_coarse_resid");
+    }
+  };
+};
+
+template <typename T, typename Z, class Chk, bool LW>
+struct Fine {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const T* u, Z* zz,
+                    unsigned long long* hist, QuantFlags* fl, const double* ec, const Chk& chk,
+                    unsigned long long* red, const Widths& lw, double* partials, int blocks, int vec) {
+      k_fine<D, T, Z, Chk, LW><<<blocks, 256, 0, s>>>(g, W, u, zz, hist, fl, ec, chk, red, lw, partials, vec);
+      check_launch("k_fine");
     }
   };
 };
@@ -537,31 +637,67 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
   const int L = dh.h.L;
   std::vector<double> widths = initial_bin_widths(tau, spec, grid.d, L);
 
-  double* r = ctx.r.get<double>(N * 8);
   const bool level_weighted = spec.norm == Norm::s && spec.smoothness != 0.0;
+  const bool s0 = spec.norm == Norm::s && !level_weighted;
+  double* ec = L >= 1 ? ctx.r.get<double>(std::max<uint64_t>(g.Nc, 1) * 8) : nullptr;
+  Widths lw{};
+  if (level_weighted)
+    for (int l = 0; l <= L; ++l)
+      lw.w[l] = std::exp2(2.0 * spec.smoothness * (static_cast<double>(l) - static_cast<double>(L)));
+  const int fine_blocks = grid_blocks((N + 3) / 4, 256);
+  double* part = ctx.partial.get<double>(static_cast<size_t>(fine_blocks) * 8);
   bool wide = false;
   bool accepted = false;
   void* zzp = nullptr;
   for (int pass = 0; pass < 10; ++pass) {
     const Widths W = to_widths(widths);
+    // (a)+(b): e on the coarse box (container.cpp:93-113, error_control.cpp:103)
+    if (!level_weighted && L >= 1) {
+      prof.begin("coarse_check", static_cast<double>(g.Nc) * 16);
+      by_dim<CoarseResid<T>::template L>(grid.d, s, g, W, u, ec);
+      const SrcResidual csrc{ec};
+      for (int l = 1; l < dh.gc.L; ++l)
+        by_dim<InvBox<SrcResidual>::template L>(grid.d, s, dh.gc, dh.cboxes[l], l, csrc, ec);
+      by_dim<InvFinest<SrcResidual, EpiStore64, true>::template L>(grid.d, s, dh.gc, csrc, ec, EpiStore64{ec},
+                                                                   nullptr);
+      prof.end();
+    }
     for (;;) {  // u32 codes first; u64 when some |q| ≥ 2^31
       CK(cudaMemsetAsync(&sd->qflags, 0, sizeof(QuantFlags), s));
       CK(cudaMemsetAsync(sd->hist, 0, sizeof sd->hist, s));
+      CK(cudaMemsetAsync(&sd->red_bits, 0, 8, s));
       const double zb = wide ? 8.0 : 4.0;
-      prof.begin("forward_quant", static_cast<double>(N) * (sizeof(T) + zb + 8));
-      if (wide) {
-        auto* zz = ctx.zz.get<unsigned long long>(N * 8);
+      double* estore = s0 ? ctx.e.get<double>(N * 8) : nullptr;
+      prof.begin("fine", static_cast<double>(N) * (sizeof(T) + zb + (s0 ? 8 : 0)));
+      auto launch = [&](auto* zz) {
+        using Z = std::remove_pointer_t<decltype(zz)>;
         zzp = zz;
-        const int vec = aligned16(u) && aligned16(zz) && aligned16(r);
-        by_dim<FwdQuant<T, unsigned long long>::template L>(grid.d, s, g, W, u, zz, r, sd->hist, &sd->qflags, vec);
-      } else {
-        auto* zz = ctx.zz.get<uint32_t>(N * 4);
-        zzp = zz;
-        const int vec = aligned16(u) && aligned16(zz) && aligned16(r);
-        by_dim<FwdQuant<T, uint32_t>::template L>(grid.d, s, g, W, u, zz, r, sd->hist, &sd->qflags, vec);
-      }
+        const int vec = aligned16(u) && aligned16(zz);
+        if (level_weighted)
+          by_dim<Fine<T, Z, ChkLevelWeighted, true>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags,
+                                                                 ec, ChkLevelWeighted{}, nullptr, lw, part,
+                                                                 fine_blocks, vec);
+        else if (s0 && dtype == DType::f32)
+          by_dim<Fine<T, Z, ChkCastStore, false>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags, ec,
+                                                              ChkCastStore{estore}, nullptr, lw, part, fine_blocks,
+                                                              vec);
+        else if (s0)
+          by_dim<Fine<T, Z, ChkStore, false>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags, ec,
+                                                          ChkStore{estore}, nullptr, lw, part, fine_blocks, vec);
+        else if (dtype == DType::f32)
+          by_dim<Fine<T, Z, ChkCastMaxAbs, false>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags, ec,
+                                                               ChkCastMaxAbs{}, &sd->red_bits, lw, part,
+                                                               fine_blocks, vec);
+        else
+          by_dim<Fine<T, Z, ChkMaxAbs, false>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags, ec,
+                                                           ChkMaxAbs{}, &sd->red_bits, lw, part, fine_blocks, vec);
+      };
+      if (wide) launch(ctx.zz.get<unsigned long long>(N * 8));
+      else launch(ctx.zz.get<uint32_t>(N * 4));
       prof.end();
       CK(cudaMemcpyAsync(&sh->qflags, &sd->qflags, sizeof(QuantFlags), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&sh->red_bits, &sd->red_bits, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(sh->hist, sd->hist, sizeof sh->hist, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (sh->qflags.overflow)
         raise(Errc::overflow, std::to_string(sh->qflags.overflow) + " coefficients exceed the 63-bit symbol range");
@@ -572,48 +708,22 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
       break;
     }
 
-    // a-posteriori error (container.cpp:93-113, error_control.cpp:62-108)
     double achieved;
-    prof.begin("check", static_cast<double>(N) * (8 + sizeof(T)));
-    if (level_weighted) {
-      Widths lw{};
-      for (int l = 0; l <= L; ++l)
-        lw.w[l] = std::exp2(2.0 * spec.smoothness * (static_cast<double>(l) - static_cast<double>(L)));
-      const int blocks = 1024;
-      double* part = ctx.partial.get<double>(blocks * 8);
-      by_dim<LevelWeighted::L>(grid.d, s, g, lw, r, part, blocks);
-      double* hp = ctx.partial_h.get<double>(blocks * 8);
-      CK(cudaMemcpyAsync(hp, part, blocks * 8, cudaMemcpyDeviceToHost, s));
+    if (level_weighted) {  // error_control.cpp:72-100 (fixed-order tree)
+      double* hp = ctx.partial_h.get<double>(static_cast<size_t>(fine_blocks) * 8);
+      CK(cudaMemcpyAsync(hp, part, static_cast<size_t>(fine_blocks) * 8, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       double acc = 0.0;
-      for (int b = 0; b < blocks; ++b) acc = acc + hp[b];
+      for (int b = 0; b < fine_blocks; ++b) acc = acc + hp[b];
       achieved = std::sqrt(acc / static_cast<double>(N));
+    } else if (s0) {  // ordered RMS of e / of the f32 cast error (exec.cpp:47-71)
+      prof.begin("sumsq_check", static_cast<double>(N) * 8);
+      achieved = std::sqrt(blocked_sumsq(ctx, static_cast<const double*>(ctx.e.get<double>(N * 8)), N) /
+                           static_cast<double>(N));
+      prof.end();
     } else {
-      const SrcResidual src{r};
-      inverse_coarse_levels(ctx, dh, src, r, 1);  // in place: r becomes e on coarse nodes
-      if (spec.norm == Norm::inf) {
-        CK(cudaMemsetAsync(&sd->red_bits, 0, 8, s));
-        if (dtype == DType::f32)
-          by_dim<InvFinest<SrcResidual, EpiCastMaxAbs<T>, false>::template L>(
-              grid.d, s, g, src, r, EpiCastMaxAbs<T>{u}, &sd->red_bits);
-        else
-          by_dim<InvFinest<SrcResidual, EpiMaxAbs, false>::template L>(grid.d, s, g, src, r, EpiMaxAbs{nullptr},
-                                                                      &sd->red_bits);
-        CK(cudaMemcpyAsync(&sh->red_bits, &sd->red_bits, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        std::memcpy(&achieved, &sh->red_bits, 8);
-      } else {  // S(0): ordered RMS of e (or of the f32 cast error)
-        double* e = ctx.e.get<double>(N * 8);
-        if (dtype == DType::f32)
-          by_dim<InvFinest<SrcResidual, EpiCastStore<T>, false>::template L>(
-              grid.d, s, g, src, r, EpiCastStore<T>{u, e}, nullptr);
-        else
-          by_dim<InvFinest<SrcResidual, EpiStore64, false>::template L>(grid.d, s, g, src, r, EpiStore64{e},
-                                                                       nullptr);
-        achieved = std::sqrt(blocked_sumsq(ctx, static_cast<const double*>(e), N) / static_cast<double>(N));
-      }
+      std::memcpy(&achieved, &sh->red_bits, 8);
     }
-    prof.end();
     if (achieved <= tau * (1.0 - 1e-9)) {
       accepted = true;
       break;
@@ -640,8 +750,6 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
   } else {
     CodeTable table;
     if (codec == Codec::huffman) {
-      CK(cudaMemcpyAsync(sh->hist, sd->hist, sizeof sh->hist, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
       table = build_code_table(reinterpret_cast<const uint64_t*>(sh->hist));  // K4 on host: 256 symbols
       write_table_header(table_bytes, table);
     } else {
@@ -653,6 +761,9 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
       table.max_len = 8;
     }
     if (codec == Codec::varint || table.nsym >= 2) {
+      // total bits = Σ_sym count·len, known before packing
+      unsigned long long total_bits = 0;
+      for (int b = 0; b < 256; ++b) total_bits += sh->hist[b] * table.lengths[b];
       struct {
         uint32_t codes[256];
         uint8_t lens[256];
@@ -666,36 +777,32 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
       const uint32_t* dcodes = reinterpret_cast<const uint32_t*>(dtab);
       const uint8_t* dlens = dtab + 1024;
       const uint64_t ntiles = (N + kPackTile - 1) / kPackTile;
-      auto* tb = ctx.tiles.get<unsigned long long>(ntiles * 8);
-      auto* toff = ctx.scan.get<unsigned long long>((ntiles + 1) * 8);
-      prof.begin("tile_bits", static_cast<double>(N) * (wide ? 8 : 4));
-      if (wide)
-        k_tile_bits<<<static_cast<unsigned>(ntiles), kPackThreads, 0, s>>>(
-            static_cast<unsigned long long*>(zzp), N, dlens, tb);
-      else
-        k_tile_bits<<<static_cast<unsigned>(ntiles), kPackThreads, 0, s>>>(static_cast<uint32_t*>(zzp), N, dlens,
-                                                                           tb);
-      check_launch("k_tile_bits");
-      k_scan_u64_single<<<1, 1024, 0, s>>>(tb, toff, ntiles);
-      check_launch("k_scan_u64_single");
-      prof.end();
-      unsigned long long total_bits = 0;
-      CK(cudaMemcpyAsync(&sh->red_bits, toff + ntiles, 8, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      total_bits = sh->red_bits;
+      // workspace: status[ntiles] | tile_start[ntiles+1] | edge_first | edge_last | ticket
+      const size_t ws = ntiles * 8 + (ntiles + 1) * 8 + ntiles * 4 * 2 + 16;
+      auto* wsp = ctx.tiles.get<uint8_t>(ws);
+      auto* status = reinterpret_cast<unsigned long long*>(wsp);
+      auto* tstart = status + ntiles;
+      auto* efirst = reinterpret_cast<uint32_t*>(tstart + ntiles + 1);
+      auto* elast = efirst + ntiles;
+      auto* ticket = elast + ntiles;
+      CK(cudaMemsetAsync(status, 0, ntiles * 8, s));
+      CK(cudaMemsetAsync(ticket, 0, 4, s));
+      CK(cudaMemcpyAsync(tstart + ntiles, &total_bits, 8, cudaMemcpyHostToDevice, s));
       const uint64_t nbytes = (total_bits + 7) / 8;
       const uint64_t nwords = (total_bits + 31) / 32 + 2;
       auto* words = ctx.bits.get<uint32_t>(nwords * 4 + 16);
       prof.begin("pack", static_cast<double>(N) * (wide ? 8 : 4) + static_cast<double>(nbytes));
-      CK(cudaMemsetAsync(words, 0, nwords * 4, s));
       const size_t smem = static_cast<size_t>(kPackMaxWords) * 4;
       if (wide)
-        k_pack<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<unsigned long long*>(zzp), N,
-                                                                        dcodes, dlens, toff, words);
+        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(
+            static_cast<unsigned long long*>(zzp), N, dcodes, dlens, status, ticket, tstart, efirst, elast, words);
       else
-        k_pack<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<uint32_t*>(zzp), N, dcodes,
-                                                                        dlens, toff, words);
-      check_launch("k_pack");
+        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(
+            static_cast<uint32_t*>(zzp), N, dcodes, dlens, status, ticket, tstart, efirst, elast, words);
+      check_launch("k_pack_lb");
+      k_pack_edges<<<static_cast<unsigned>((ntiles + 255) / 256), 256, 0, s>>>(tstart, ntiles, efirst, elast,
+                                                                              words);
+      check_launch("k_pack_edges");
       prof.end();
       dev_payload = reinterpret_cast<const uint8_t*>(words);
       dev_len = nbytes;
@@ -934,8 +1041,14 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         auto* toff = ctx.scan.get<unsigned long long>((nseq + 1) * 8);
         k_seq_counts<<<static_cast<unsigned>((nseq + 255) / 256), 256, 0, s>>>(seq, nseq, cnt);
         check_launch("k_seq_counts");
-        k_scan_u64_single<<<1, 1024, 0, s>>>(cnt, toff, nseq);
-        check_launch("k_scan_u64_single");
+        {
+          const uint64_t nt = (nseq + kScanTile - 1) / kScanTile;
+          auto* st = ctx.lbws.get<unsigned long long>(nt * 8 + 16);
+          auto* ticket = reinterpret_cast<unsigned int*>(st + nt);
+          CK(cudaMemsetAsync(st, 0, nt * 8 + 16, s));
+          k_scan_lb<<<static_cast<unsigned>(nt), kScanThreads, 0, s>>>(cnt, toff, nseq, st, ticket);
+          check_launch("k_scan_lb");
+        }
         for (;;) {
           DecodeStatus init{~0ull, 0u, 0u, 0u};
           CK(cudaMemcpyAsync(&sd->dstat, &init, sizeof init, cudaMemcpyHostToDevice, s));
