@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "rows.cuh"
 #include "pipeline.hpp"
 
 namespace mgrc_gpu {
@@ -133,7 +134,7 @@ class Context {
   bool profiling = false;
   std::vector<PhaseTime> profile;
   // workspace
-  DevBuf in, zz, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws;
+  DevBuf in, zz, zc, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws;
   DevBuf scratch_d;
   PinnedBuf scratch_h, partial_h;
   std::unique_ptr<DevHier> hier;
@@ -210,6 +211,17 @@ class Prof {
   Context& c_;
   std::vector<Rec> recs_;
 };
+
+static int num_sms() {
+  static thread_local int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
 
 static int grid_blocks(uint64_t work_items, int threads, int per_sm = 8) {
   int dev = 0, sms = 148;
@@ -457,6 +469,68 @@ struct Fine {
   };
 };
 
+static RowTiling row_tiling(const GridDev& g) {
+  RowTiling rt{};
+  rt.n_last = g.shape[g.d - 1];
+  rt.nrows = g.N / rt.n_last;
+  rt.K = std::min<uint32_t>(rt.n_last, kRowTileElems);
+  rt.ncol_tiles = (rt.n_last + rt.K - 1) / rt.K;
+  rt.R = rt.ncol_tiles == 1 ? std::max<uint32_t>(1, std::min<uint32_t>(kRowMaxR, kRowTileElems / rt.n_last)) : 1;
+  rt.invK = 1.0f / static_cast<float>(rt.K);
+  return rt;
+}
+
+static uint64_t row_tiles(const RowTiling& rt) { return ((rt.nrows + rt.R - 1) / rt.R) * rt.ncol_tiles; }
+
+template <typename T, typename Z>
+struct CoarseQuant {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const T* u, double* ec, Z* zc,
+                    QuantFlags* fl) {
+      k_coarse_quant<D, T, Z><<<grid_blocks(g.Nc, 256), 256, 0, s>>>(g, W, u, ec, zc, fl);
+      check_launch("k_coarse_quant");
+    }
+  };
+};
+
+template <typename T, typename Z, class Chk, bool LW>
+struct FineRows {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const RowTiling& rt, const Widths& W, const T* u, Z* zz,
+                    unsigned long long* hist, QuantFlags* fl, const double* ec, const Z* zc, const Chk& chk,
+                    unsigned long long* red, const Widths& lw, double* partials, int blocks) {
+      k_fine_rows<D, T, Z, Chk, LW><<<blocks, kRowThreads, 0, s>>>(g, rt, W, u, zz, hist, fl, ec, zc, chk, red, lw,
+                                                                   partials);
+      check_launch("k_fine_rows");
+    }
+  };
+};
+
+template <typename Z>
+struct ReconCoarse {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const Z* zz, double* vc) {
+      k_recon_coarse<D, Z><<<grid_blocks(g.Nc, 256), 256, 0, s>>>(g, W, zz, vc);
+      check_launch("k_recon_coarse");
+    }
+  };
+};
+
+template <typename Z, class Out>
+struct ReconRows {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const RowTiling& rt, const Widths& W, const Z* zz,
+                    const double* vc, const Out& out) {
+      k_recon_rows<D, Z, Out><<<static_cast<unsigned>(row_tiles(rt)), kRowThreads, 0, s>>>(g, rt, W, zz, vc, out);
+      check_launch("k_recon_rows");
+    }
+  };
+};
+
 struct LevelWeighted {
   template <int D>
   struct L {
@@ -644,57 +718,62 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
   if (level_weighted)
     for (int l = 0; l <= L; ++l)
       lw.w[l] = std::exp2(2.0 * spec.smoothness * (static_cast<double>(l) - static_cast<double>(L)));
-  const int fine_blocks = grid_blocks((N + 3) / 4, 256);
+  const RowTiling rt = row_tiling(g);
+  const int fine_blocks = static_cast<int>(std::min<uint64_t>(row_tiles(rt), static_cast<uint64_t>(num_sms()) * 4));
   double* part = ctx.partial.get<double>(static_cast<size_t>(fine_blocks) * 8);
   bool wide = false;
   bool accepted = false;
   void* zzp = nullptr;
   for (int pass = 0; pass < 10; ++pass) {
     const Widths W = to_widths(widths);
-    // (a)+(b): e on the coarse box (container.cpp:93-113, error_control.cpp:103)
-    if (!level_weighted && L >= 1) {
-      prof.begin("coarse_check", static_cast<double>(g.Nc) * 16);
-      by_dim<CoarseResid<T>::template L>(grid.d, s, g, W, u, ec);
-      const SrcResidual csrc{ec};
-      for (int l = 1; l < dh.gc.L; ++l)
-        by_dim<InvBox<SrcResidual>::template L>(grid.d, s, dh.gc, dh.cboxes[l], l, csrc, ec);
-      by_dim<InvFinest<SrcResidual, EpiStore64, true>::template L>(grid.d, s, dh.gc, csrc, ec, EpiStore64{ec},
-                                                                   nullptr);
-      prof.end();
-    }
     for (;;) {  // u32 codes first; u64 when some |q| ≥ 2^31
       CK(cudaMemsetAsync(&sd->qflags, 0, sizeof(QuantFlags), s));
       CK(cudaMemsetAsync(sd->hist, 0, sizeof sd->hist, s));
       CK(cudaMemsetAsync(&sd->red_bits, 0, 8, s));
       const double zb = wide ? 8.0 : 4.0;
       double* estore = s0 ? ctx.e.get<double>(N * 8) : nullptr;
-      prof.begin("fine", static_cast<double>(N) * (sizeof(T) + zb + (s0 ? 8 : 0)));
-      auto launch = [&](auto* zz) {
+      auto launch = [&](auto* zz, auto* zc) {
         using Z = std::remove_pointer_t<decltype(zz)>;
         zzp = zz;
-        const int vec = aligned16(u) && aligned16(zz);
+        // (a) r and codes of the coarse box; (b) its inverse (container.cpp:93-113)
+        if (L >= 1) {
+          prof.begin("coarse_check", static_cast<double>(g.Nc) * (sizeof(T) + 8 + zb));
+          by_dim<CoarseQuant<T, Z>::template L>(grid.d, s, g, W, u, ec, zc, &sd->qflags);
+          if (!level_weighted) {
+            const SrcResidual csrc{ec};
+            for (int l = 1; l < dh.gc.L; ++l)
+              by_dim<InvBox<SrcResidual>::template L>(grid.d, s, dh.gc, dh.cboxes[l], l, csrc, ec);
+            by_dim<InvFinest<SrcResidual, EpiStore64, true>::template L>(grid.d, s, dh.gc, csrc, ec,
+                                                                         EpiStore64{ec}, nullptr);
+          }
+          prof.end();
+        }
+        // (c) the fused row pass
+        prof.begin("fine", static_cast<double>(N) * (sizeof(T) + zb + (s0 ? 8 : 0)));
         if (level_weighted)
-          by_dim<Fine<T, Z, ChkLevelWeighted, true>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags,
-                                                                 ec, ChkLevelWeighted{}, nullptr, lw, part,
-                                                                 fine_blocks, vec);
+          by_dim<FineRows<T, Z, ChkLevelWeighted, true>::template L>(grid.d, s, g, rt, W, u, zz, sd->hist,
+                                                                     &sd->qflags, ec, zc, ChkLevelWeighted{}, nullptr,
+                                                                     lw, part, fine_blocks);
         else if (s0 && dtype == DType::f32)
-          by_dim<Fine<T, Z, ChkCastStore, false>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags, ec,
-                                                              ChkCastStore{estore}, nullptr, lw, part, fine_blocks,
-                                                              vec);
+          by_dim<FineRows<T, Z, ChkCastStore, false>::template L>(grid.d, s, g, rt, W, u, zz, sd->hist, &sd->qflags,
+                                                                  ec, zc, ChkCastStore{estore}, nullptr, lw, part,
+                                                                  fine_blocks);
         else if (s0)
-          by_dim<Fine<T, Z, ChkStore, false>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags, ec,
-                                                          ChkStore{estore}, nullptr, lw, part, fine_blocks, vec);
+          by_dim<FineRows<T, Z, ChkStore, false>::template L>(grid.d, s, g, rt, W, u, zz, sd->hist, &sd->qflags, ec,
+                                                              zc, ChkStore{estore}, nullptr, lw, part, fine_blocks);
         else if (dtype == DType::f32)
-          by_dim<Fine<T, Z, ChkCastMaxAbs, false>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags, ec,
-                                                               ChkCastMaxAbs{}, &sd->red_bits, lw, part,
-                                                               fine_blocks, vec);
+          by_dim<FineRows<T, Z, ChkCastMaxAbs, false>::template L>(grid.d, s, g, rt, W, u, zz, sd->hist,
+                                                                   &sd->qflags, ec, zc, ChkCastMaxAbs{},
+                                                                   &sd->red_bits, lw, part, fine_blocks);
         else
-          by_dim<Fine<T, Z, ChkMaxAbs, false>::template L>(grid.d, s, g, W, u, zz, sd->hist, &sd->qflags, ec,
-                                                           ChkMaxAbs{}, &sd->red_bits, lw, part, fine_blocks, vec);
+          by_dim<FineRows<T, Z, ChkMaxAbs, false>::template L>(grid.d, s, g, rt, W, u, zz, sd->hist, &sd->qflags,
+                                                               ec, zc, ChkMaxAbs{}, &sd->red_bits, lw, part,
+                                                               fine_blocks);
+        prof.end();
       };
-      if (wide) launch(ctx.zz.get<unsigned long long>(N * 8));
-      else launch(ctx.zz.get<uint32_t>(N * 4));
-      prof.end();
+      const uint64_t nc = std::max<uint64_t>(g.Nc, 1);
+      if (wide) launch(ctx.zz.get<unsigned long long>(N * 8), ctx.zc.get<unsigned long long>(nc * 8));
+      else launch(ctx.zz.get<uint32_t>(N * 4), ctx.zc.get<uint32_t>(nc * 4));
       CK(cudaMemcpyAsync(&sh->qflags, &sd->qflags, sizeof(QuantFlags), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(&sh->red_bits, &sd->red_bits, 8, cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(sh->hist, sd->hist, sizeof sh->hist, cudaMemcpyDeviceToHost, s));
@@ -872,17 +951,20 @@ static void run_recon(Context& ctx, DevHier& dh, const Z* zz, const Widths& W, D
                       uint64_t N) {
   cudaStream_t s = ctx.stream;
   const GridDev& g = dh.g;
-  const SrcDequant<Z> src{zz, W};
-  double* v = dtype == DType::f64 ? static_cast<double*>(out) : ctx.v.get<double>(N * 8);
-  if (g.L > 0) {
-    by_dim<InvBox<SrcDequant<Z>>::template L>(g.d, s, g, dh.boxes[0], 0, src, v);  // level 0: v = q·δ0
-    inverse_coarse_levels(ctx, dh, src, v, 1);
+  double* vc = nullptr;
+  if (g.L >= 1) {  // coarse box: dequantise (compact), then levels 1..L-1 in place
+    vc = ctx.v.get<double>(std::max<uint64_t>(g.Nc, 1) * 8);
+    by_dim<ReconCoarse<Z>::template L>(g.d, s, g, W, zz, vc);
+    const SrcResidual csrc{vc};
+    for (int l = 1; l < dh.gc.L; ++l)
+      by_dim<InvBox<SrcResidual>::template L>(g.d, s, dh.gc, dh.cboxes[l], l, csrc, vc);
+    by_dim<InvFinest<SrcResidual, EpiStore64, true>::template L>(g.d, s, dh.gc, csrc, vc, EpiStore64{vc}, nullptr);
   }
+  const RowTiling rt = row_tiling(g);
   if (dtype == DType::f64)
-    by_dim<InvFinest<SrcDequant<Z>, EpiStore64, true>::template L>(g.d, s, g, src, v, EpiStore64{v}, nullptr);
+    by_dim<ReconRows<Z, OutF64>::template L>(g.d, s, g, rt, W, zz, vc, OutF64{static_cast<double*>(out)});
   else
-    by_dim<InvFinest<SrcDequant<Z>, EpiNarrow32, false>::template L>(g.d, s, g, src, v,
-                                                                    EpiNarrow32{static_cast<float*>(out)}, nullptr);
+    by_dim<ReconRows<Z, OutF32>::template L>(g.d, s, g, rt, W, zz, vc, OutF32{static_cast<float*>(out)});
 }
 
 DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void* out, uint64_t out_cap) {

@@ -27,7 +27,7 @@ def _free_port():
 CASES = {
     "inf_rel_f32": dict(shape=(40, 33, 17), dtype="f32", tol=1e-4, norm=0, s=0.0, mode=1, chunk=17 * 33 * 17 * 4),
     "inf_abs_f64_2d": dict(shape=(70, 65), dtype="f64", tol=1e-3, norm=0, s=0.0, mode=0, chunk=20 * 65 * 8),
-    "s0_abs_f64": dict(shape=(50, 9, 9), dtype="f64", tol=1e-3, norm=1, s=0.0, mode=0, chunk=12 * 81 * 8),
+    "s0_abs_f64": dict(shape=(60, 20, 20), dtype="f64", tol=1e-3, norm=1, s=0.0, mode=0, chunk=17 * 400 * 8),
     "single_block": dict(shape=(33, 17), dtype="f64", tol=1e-3, norm=0, s=0.0, mode=1, chunk=0),
 }
 
