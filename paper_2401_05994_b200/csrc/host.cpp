@@ -462,7 +462,7 @@ std::vector<uint16_t> build_decode_lut(const CodeTable& t) {
     const int l = t.lengths[s];
     if (!l) continue;
     const uint32_t lo = t.codes[s] << (t.max_len - l), hi = (t.codes[s] + 1) << (t.max_len - l);
-    for (uint32_t k = lo; k < hi; ++k) lut[k] = static_cast<uint16_t>(s | (l << 8));
+    for (uint32_t k = lo; k < hi; ++k) lut[k] = static_cast<uint16_t>(s | (l << 8) | ((s < 0x80 ? 1 : 0) << 12));
   }
   return lut;
 }

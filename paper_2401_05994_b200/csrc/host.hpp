@@ -131,7 +131,7 @@ void write_table_header(std::vector<uint8_t>& out, const CodeTable& t);
 // Parses + validates the table header exactly like read_table_header and the
 // HuffmanDecoder constructor; returns the lengths.  Throws CorruptStream.
 CodeTable read_table_header(const uint8_t* p, uint64_t n, uint64_t* consumed);
-// Decode LUT: 2^max_len entries, entry = symbol | (length << 8).
+// Decode LUT: 2^max_len entries, entry = symbol | (length << 8) | (symbol < 0x80) << 12.
 std::vector<uint16_t> build_decode_lut(const CodeTable& t);
 
 // ---- CRC-32 (codec.cpp:14-28) host helpers ---------------------------------

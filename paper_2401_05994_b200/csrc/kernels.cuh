@@ -32,6 +32,8 @@ struct AxisTab {
   const uint32_t* cl;     // tag-L-fresh index -> cpos[left]
   const uint32_t* cr;     // tag-L-fresh index -> cpos[right]
   const uint32_t* cset;   // position in the level-(L-1) set -> finest index
+  const uint32_t* colc;   // uint2 per index: {cpos[i-1], cpos[i+1]} if fresh at L, else {cpos[i], 0xFFFFFFFF}
+  const double* colw;     // double2 per index: {w_left, w_right} if fresh at L
 };
 
 struct GridDev {
@@ -70,6 +72,7 @@ __device__ __forceinline__ unsigned long long dkey(double x) {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
 // ---------------------------------------------------------------------------
 // Multilinear corner interpolation of one node (transform.cpp:102-128).
@@ -1217,92 +1220,6 @@ struct SeqInfo {
   uint32_t pad;
 };
 
-struct DecTab {
-  const uint16_t* lut;  // 2^maxlen entries: sym | len << 8
-  int maxlen;
-};
-
-__device__ __forceinline__ uint32_t peek32(const uint32_t* __restrict__ w, uint64_t p) {
-  const uint64_t wi = p >> 5;
-  const uint32_t hi = bswap32(__ldg(w + wi)), lo = bswap32(__ldg(w + wi + 1));
-  return __funnelshift_l(lo, hi, static_cast<uint32_t>(p & 31));
-}
-
-// Decode the codewords starting in [start, end) (end ≤ T); stops early at a
-// codeword that would run past T (incomplete tail).
-__device__ __forceinline__ void decode_seq(const uint32_t* __restrict__ w, uint64_t T, const uint16_t* lut,
-                                           int maxlen, uint64_t start, uint64_t end, SeqInfo& s) {
-  uint64_t p = start;
-  uint32_t nsym = 0, nterm = 0, last = 0;
-  while (p < end) {
-    const uint32_t ent = lut[peek32(w, p) >> (32 - maxlen)];
-    const uint32_t l = ent >> 8;
-    if (p + l > T) break;
-    const uint32_t sym = ent & 0xFF;
-    p += l;
-    ++nsym;
-    nterm += sym < 0x80;
-    last = sym;
-  }
-  s.start = start;
-  s.exit = p;
-  s.nsym = nsym;
-  s.nterm = nterm;
-  s.last_cont = last >= 0x80;
-}
-
-__global__ void __launch_bounds__(kDecThreads) k_huff_sync(const uint32_t* __restrict__ w, uint64_t T,
-                                                           const uint16_t* __restrict__ lut_g, int maxlen,
-                                                           uint64_t nseq, SeqInfo* __restrict__ seq) {
-  extern __shared__ uint16_t lut[];
-  __shared__ unsigned long long sexit[kDecThreads];
-  const int lutn = 1 << maxlen;
-  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
-  __syncthreads();
-  const uint64_t j = blockIdx.x * static_cast<uint64_t>(kDecThreads) + threadIdx.x;
-  const bool valid = j < nseq;
-  SeqInfo s{};
-  uint64_t end = 0;
-  if (valid) {
-    const uint64_t start = j * kSeqBits;
-    end = umin64(start + kSeqBits, T);
-    decode_seq(w, T, lut, maxlen, start, end, s);
-  }
-  sexit[threadIdx.x] = valid ? s.exit : 0;
-  __syncthreads();  // every exit published before any neighbour reads it
-  // intra-block resynchronisation
-  for (;;) {
-    const unsigned long long pe = threadIdx.x > 0 ? sexit[threadIdx.x - 1] : 0;
-    __syncthreads();
-    bool changed = false;
-    if (valid && threadIdx.x > 0 && pe != s.start) {
-      decode_seq(w, T, lut, maxlen, pe, end, s);
-      sexit[threadIdx.x] = s.exit;
-      changed = true;
-    }
-    if (!__syncthreads_or(changed)) break;
-  }
-  if (valid) seq[j] = s;
-}
-
-// Inter-block resynchronisation: the first subsequences of each block are
-// re-decoded from the previous block's exit until they agree.
-__global__ void k_huff_fix(const uint32_t* __restrict__ w, uint64_t T, const uint16_t* __restrict__ lut, int maxlen,
-                           uint64_t nseq, SeqInfo* seq, unsigned int* changed) {
-  const uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x + 1;
-  const uint64_t nblk = (nseq + kDecThreads - 1) / kDecThreads;
-  if (b >= nblk) return;
-  for (uint64_t j = b * kDecThreads; j < umin64((b + 1) * kDecThreads, nseq); ++j) {
-    const unsigned long long pe = *reinterpret_cast<volatile unsigned long long*>(&seq[j - 1].exit);
-    if (pe == seq[j].start) break;
-    SeqInfo s;
-    decode_seq(w, T, lut, maxlen, pe, umin64((j + 1) * kSeqBits, T), s);
-    seq[j] = s;
-    __threadfence();
-    atomicOr(changed, 1u);
-  }
-}
-
 __global__ void k_seq_counts(const SeqInfo* __restrict__ seq, uint64_t nseq, unsigned long long* __restrict__ nterm) {
   const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (j < nseq) nterm[j] = seq[j].nterm;
@@ -1314,74 +1231,6 @@ struct DecodeStatus {
   unsigned int wide;           // a value does not fit the u32 store
   unsigned int clean;          // only zero padding (< 8 bits) follows the N-th varint
 };
-
-// Emit: re-decode each synchronised subsequence and assemble the varints
-// that START in it (a value that runs past the subsequence is finished by
-// decoding on; ≤ 10 bytes).  Values beyond N (decoded zero padding) are
-// ignored, as the reference never reads them (codec.cpp:475-481).
-template <typename Z>
-__global__ void __launch_bounds__(kDecThreads) k_huff_emit(const uint32_t* __restrict__ w, uint64_t T,
-                                                           const uint16_t* __restrict__ lut_g, int maxlen,
-                                                           uint64_t nseq, const SeqInfo* __restrict__ seq,
-                                                           const unsigned long long* __restrict__ term_off,
-                                                           uint64_t N, Z* __restrict__ zz, DecodeStatus* st) {
-  extern __shared__ uint16_t lut[];
-  const int lutn = 1 << maxlen;
-  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
-  __syncthreads();
-  const uint64_t j = blockIdx.x * static_cast<uint64_t>(kDecThreads) + threadIdx.x;
-  if (j >= nseq) return;
-  const SeqInfo s = seq[j];
-  bool skipping = j > 0 && seq[j - 1].last_cont;
-  uint64_t k = term_off[j];
-  if (k >= N && !skipping) return;
-  uint64_t p = s.start;
-  uint64_t acc = 0;
-  int nb = 0;
-  unsigned err = 0, wide = 0;
-  // symbols of this subsequence, then continue past its exit to finish an
-  // open value
-  for (;;) {
-    const bool inside = p < s.exit;
-    if (!inside && nb == 0) break;
-    if (k >= N) break;
-    const uint32_t ent = lut[peek32(w, p) >> (32 - maxlen)];
-    const uint32_t l = ent >> 8;
-    if (p + l > T) {  // stream ends inside an open value
-      err = 2;
-      break;
-    }
-    const uint32_t b = ent & 0xFF;
-    p += l;
-    if (skipping) {
-      if (b < 0x80) {
-        skipping = false;
-        ++k;
-      }
-      continue;
-    }
-    if (nb == 9 && (b & 0xFE)) {  // varint overflows 64 bits (codec.cpp:80-81)
-      err = 1;
-      break;
-    }
-    acc |= static_cast<uint64_t>(b & 0x7F) << (7 * nb);
-    ++nb;
-    if (b < 0x80) {
-      if (sizeof(Z) == 4 && acc > 0xFFFFFFFFull) wide = 1;
-      zz[k] = static_cast<Z>(acc);
-      if (k == N - 1) {  // exhausted_clean (codec.cpp:370-375)
-        st->end_bit = p;
-        const uint64_t rest = T - p;
-        st->clean = rest < 8 && (rest == 0 || (peek32(w, p) >> (32 - rest)) == 0);
-      }
-      ++k;
-      acc = 0;
-      nb = 0;
-    }
-  }
-  if (err) atomicMax(&st->error, err);
-  if (wide) atomicOr(&st->wide, 1u);
-}
 
 // Codec 0 decode: raw little-endian int64 → zigzag.
 template <typename Z>

@@ -23,6 +23,7 @@
 
 #include "kernels.cuh"
 #include "rows.cuh"
+#include "huff.cuh"
 #include "pipeline.hpp"
 
 namespace mgrc_gpu {
@@ -260,7 +261,7 @@ static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
     return off;
   };
   struct Off {
-    size_t wl, wr, left, right, lvl, cpos, cl, cr, cset;
+    size_t wl, wr, left, right, lvl, cpos, cl, cr, cset, colc, colw;
     size_t c_wl, c_wr, c_left, c_right, c_lvl;
   } off[kMaxDims];
   std::vector<std::vector<size_t>> off_set(L + 1, std::vector<size_t>(d)), off_cset(L + 1, std::vector<size_t>(d));
@@ -293,6 +294,23 @@ static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
         cleft[p] = h.lvl[a][i] > 0 ? cpos[h.left[a][i]] : 0;
         cright[p] = h.lvl[a][i] > 0 ? cpos[h.right[a][i]] : 0;
       }
+      std::vector<uint32_t> colc(2 * n);
+      std::vector<double> colw(2 * n, 0.0);
+      for (size_t i = 0; i < n; ++i) {
+        if (h.lvl[a][i] == L) {
+          if (h.left[a][i] != i - 1 || h.right[a][i] != i + 1)
+            raise(Errc::invalid_state, "internal: finest-level stencil is not the adjacent pair");
+          colc[2 * i] = cl[i];
+          colc[2 * i + 1] = cr[i];
+          colw[2 * i] = h.wl[a][i];
+          colw[2 * i + 1] = h.wr[a][i];
+        } else {
+          colc[2 * i] = cpos[i];
+          colc[2 * i + 1] = 0xFFFFFFFFu;
+        }
+      }
+      off[a].colc = put(colc.data(), 8 * n);
+      off[a].colw = put(colw.data(), 16 * n);
       off[a].cpos = put(cpos.data(), 4 * n);
       off[a].cl = put(cl.data(), 4 * n);
       off[a].cr = put(cr.data(), 4 * n);
@@ -339,6 +357,8 @@ static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
       g.ax[a].cl = P32(off[a].cl);
       g.ax[a].cr = P32(off[a].cr);
       g.ax[a].cset = P32(off[a].cset);
+      g.ax[a].colc = P32(off[a].colc);
+      g.ax[a].colw = P64(off[a].colw);
     }
   }
   g.Nc = L >= 1 ? cst : 0;
@@ -937,13 +957,29 @@ ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len) {
   }
 }
 
+static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords) * 4 + (sizeof(uint16_t) << maxlen); }
+
+static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
+
+static void huff_smem_optin() {
+  static thread_local bool done = false;
+  if (done) return;
+  const int mx = static_cast<int>(huff_smem(kMaxCodeLen));
+  CK(cudaFuncSetAttribute(k_huff_sync_s, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(k_huff_fix_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(fix_smem(kMaxCodeLen))));
+  done = true;
+}
+
 template <typename Z>
-static void decode_emit(Context& ctx, const uint32_t* w, uint64_t T, const uint16_t* lut, int maxlen, uint64_t nseq,
-                        const SeqInfo* seq, const unsigned long long* toff, uint64_t N, Z* zz, DecodeStatus* st) {
-  const size_t smem = sizeof(uint16_t) << maxlen;
-  k_huff_emit<Z><<<static_cast<unsigned>((nseq + kDecThreads - 1) / kDecThreads), kDecThreads, smem, ctx.stream>>>(
-      w, T, lut, maxlen, nseq, seq, toff, N, zz, st);
-  check_launch("k_huff_emit");
+static void decode_emit(Context& ctx, const uint32_t* w, uint64_t nw, uint64_t T, const uint16_t* lut, int maxlen,
+                        uint64_t nseq, const SeqInfo* seq, const unsigned long long* toff, uint64_t N, Z* zz,
+                        DecodeStatus* st) {
+  k_huff_emit_s<Z><<<static_cast<unsigned>((nseq + kDecThreads - 1) / kDecThreads), kDecThreads, huff_smem(maxlen),
+                     ctx.stream>>>(w, nw, T, lut, maxlen, nseq, seq, toff, N, zz, st);
+  check_launch("k_huff_emit_s");
 }
 
 template <typename Z>
@@ -1096,24 +1132,18 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         const uint64_t nseq = std::max<uint64_t>(1, (T + kSeqBits - 1) / kSeqBits);
         auto* seq = ctx.seq.get<SeqInfo>(nseq * sizeof(SeqInfo));
         const uint32_t* w = reinterpret_cast<const uint32_t*>(body);
-        const size_t smem = sizeof(uint16_t) << maxlen;
-        if (smem > 48 * 1024) {
-          CK(cudaFuncSetAttribute(k_huff_sync, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-          CK(cudaFuncSetAttribute(k_huff_emit<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-          CK(cudaFuncSetAttribute(k_huff_emit<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-        }
+        const uint64_t nw = (body_len + 64) / 4;
+        huff_smem_optin();
         prof.begin("huff_sync", static_cast<double>(body_len));
-        k_huff_sync<<<static_cast<unsigned>((nseq + kDecThreads - 1) / kDecThreads), kDecThreads, smem, s>>>(
-            w, T, lut, maxlen, nseq, seq);
-        check_launch("k_huff_sync");
+        k_huff_sync_s<<<static_cast<unsigned>((nseq + kDecThreads - 1) / kDecThreads), kDecThreads,
+                        huff_smem(maxlen), s>>>(w, nw, T, lut, maxlen, nseq, seq);
+        check_launch("k_huff_sync_s");
         const uint64_t nblk = (nseq + kDecThreads - 1) / kDecThreads;
         for (int it = 0; nblk > 1; ++it) {
           CK(cudaMemsetAsync(&sd->fix_changed, 0, 4, s));
-          k_huff_fix<<<static_cast<unsigned>((nblk - 1 + 127) / 128), 128, 0, s>>>(w, T, lut, maxlen, nseq, seq,
+          k_huff_fix_s<<<static_cast<unsigned>(nblk - 1), 32, fix_smem(maxlen), s>>>(w, nw, T, lut, maxlen, nseq, seq,
                                                                                   &sd->fix_changed);
-          check_launch("k_huff_fix");
+          check_launch("k_huff_fix_s");
           CK(cudaMemcpyAsync(&sh->fix_changed, &sd->fix_changed, 4, cudaMemcpyDeviceToHost, s));
           CK(cudaStreamSynchronize(s));
           if (!sh->fix_changed) break;
@@ -1136,10 +1166,10 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
           CK(cudaMemcpyAsync(&sd->dstat, &init, sizeof init, cudaMemcpyHostToDevice, s));
           prof.begin("huff_emit", static_cast<double>(body_len) + static_cast<double>(N) * (wide ? 8 : 4));
           if (wide)
-            decode_emit(ctx, w, T, lut, maxlen, nseq, seq, toff, N, ctx.zz.get<unsigned long long>(N * 8),
+            decode_emit(ctx, w, nw, T, lut, maxlen, nseq, seq, toff, N, ctx.zz.get<unsigned long long>(N * 8),
                         &sd->dstat);
           else
-            decode_emit(ctx, w, T, lut, maxlen, nseq, seq, toff, N, ctx.zz.get<uint32_t>(N * 4), &sd->dstat);
+            decode_emit(ctx, w, nw, T, lut, maxlen, nseq, seq, toff, N, ctx.zz.get<uint32_t>(N * 4), &sd->dstat);
           prof.end();
           CK(cudaMemcpyAsync(&sh->dstat, &sd->dstat, sizeof(DecodeStatus), cudaMemcpyDeviceToHost, s));
           CK(cudaStreamSynchronize(s));

@@ -113,64 +113,72 @@ __device__ __forceinline__ void build_rows(const GridDev& g, const RowTiling& rt
   m.nsub = j;
 }
 
-// Column descriptor of a tag-L node on the last axis.
-struct LastAxis {
-  bool fresh;
-  uint32_t kl, kr;    // finest columns of the bracketing neighbours (fresh)
-  uint32_t ckl, ckr;  // their compact columns
-  uint32_t ck;        // compact column (not fresh)
-  double wl, wr;
+// Column descriptors of the last axis (host-built, see device_hierarchy):
+//   colc[k] = {cpos[k-1], cpos[k+1]} when k is fresh at L (its bracketing
+//             neighbours are always k-1 and k+1 at the finest level), else
+//             {cpos[k], kNotFresh}
+//   colw[k] = {w_left, w_right} when fresh at L.
+constexpr uint32_t kNotFresh = 0xFFFFFFFFu;
+
+// Corner-row data of one row, held in registers by the warp that owns it.
+template <int NS>
+struct RowRegs {
+  uint64_t uoff[NS], coff[NS];
+  double w[NS];
+  uint64_t own, cown;
+  int nsub, all_fine;
+  __device__ __forceinline__ void load(const RowMeta& m) {
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      uoff[j] = m.uoff[j];
+      coff[j] = m.coff[j];
+      w[j] = m.w[j];
+    }
+    own = m.own;
+    cown = m.cown;
+    nsub = m.nsub;
+    all_fine = m.all_fine;
+  }
 };
 
-__device__ __forceinline__ LastAxis last_axis(const GridDev& g, int D, uint32_t k) {
-  const AxisTab& ax = g.ax[D - 1];
-  LastAxis la;
-  la.fresh = __ldg(ax.lvl + k) == g.L;
-  if (la.fresh) {
-    la.kl = __ldg(ax.left + k);
-    la.kr = __ldg(ax.right + k);
-    la.ckl = __ldg(ax.cl + k);
-    la.ckr = __ldg(ax.cr + k);
-    la.wl = __ldg(ax.wl + k);
-    la.wr = __ldg(ax.wr + k);
-    la.ck = 0;
-  } else {
-    la.kl = la.kr = la.ckl = la.ckr = 0;
-    la.wl = la.wr = 0.0;
-    la.ck = __ldg(ax.cpos + k);
-  }
-  return la;
-}
-
-// Σ_corners w·src over the finest grid (row offsets uoff) or the compact box
-// (row offsets coff), in the reference's corner order.
-template <class Ld>
-__device__ __forceinline__ double row_interp(const RowMeta& m, const uint64_t* off, const LastAxis& la, uint32_t kcol,
-                                             uint32_t kl, uint32_t kr, Ld ld) {
+// Σ_corners w·src in the reference's corner order for a compile-time number
+// of outer corner rows M (≤ NS).  Non-fresh last axis: column kc of every
+// corner row.  Fresh: columns kl then kr (last axis is the highest corner bit).
+template <int M, int NS, class Ld>
+__device__ __forceinline__ double interp_rows(const RowRegs<NS>& r, const uint64_t (&off)[NS], bool fresh,
+                                              uint64_t kc, uint64_t kl, uint64_t kr, double wl, double wr, Ld ld) {
   double acc = 0.0;
-  const int ns = m.nsub;
-  if (!la.fresh) {
-    for (int j = 0; j < ns; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], ld(off[j] + kcol)));
+  if (!fresh) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(r.w[j], ld(off[j] + kc)));
   } else {
-    for (int j = 0; j < ns; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], la.wl), ld(off[j] + kl)));
-    for (int j = 0; j < ns; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], la.wr), ld(off[j] + kr)));
+    double vl[M], vr[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      vl[j] = ld(off[j] + kl);
+      vr[j] = ld(off[j] + kr);
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(r.w[j], wl), vl[j]));
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(r.w[j], wr), vr[j]));
   }
   return acc;
 }
 
-// Maps a tile-local element index to (row within tile, column).
-__device__ __forceinline__ void tile_rc(uint32_t idx, uint32_t Kt, float invK, uint32_t& rr, uint32_t& kk) {
-  rr = __float2uint_rz(__fmul_rn(static_cast<float>(idx), invK));
-  int k = static_cast<int>(idx) - static_cast<int>(rr * Kt);
-  if (k < 0) {
-    --rr;
-    k += Kt;
-  } else if (k >= static_cast<int>(Kt)) {
-    ++rr;
-    k -= Kt;
-  }
-  kk = static_cast<uint32_t>(k);
+template <int NS, class Ld>
+__device__ __forceinline__ double interp_any(const RowRegs<NS>& r, const uint64_t (&off)[NS], bool fresh, uint64_t kc,
+                                             uint64_t kl, uint64_t kr, double wl, double wr, Ld ld) {
+  // r.nsub is warp-uniform: no divergence
+  if (NS >= 8 && r.nsub == 8) return interp_rows<(NS >= 8 ? 8 : 1), NS>(r, off, fresh, kc, kl, kr, wl, wr, ld);
+  if (NS >= 4 && r.nsub == 4) return interp_rows<(NS >= 4 ? 4 : 1), NS>(r, off, fresh, kc, kl, kr, wl, wr, ld);
+  if (NS >= 2 && r.nsub == 2) return interp_rows<(NS >= 2 ? 2 : 1), NS>(r, off, fresh, kc, kl, kr, wl, wr, ld);
+  return interp_rows<1, NS>(r, off, fresh, kc, kl, kr, wl, wr, ld);
 }
+
+// Work split of a tile: units of one row × 64 columns (2 adjacent columns
+// per lane: column parity, hence freshness, is uniform across the warp).
+constexpr int kUnitCols = 64;
 
 // ---------------------------------------------------------------------------
 // Compress: coarse box residuals + codes (compact), then the fused row pass.
@@ -217,7 +225,8 @@ __global__ void __launch_bounds__(256) k_coarse_quant(GridDev g, Widths W, const
 
 // The fused pass over the finest grid, row by row: forward + quantise +
 // zigzag store + varint histogram + a-posteriori check epilogue.  Coarse-box
-// nodes take their code and error from (zc, ec).
+// nodes take their code and error from (zc, ec).  Tiles are visited in a
+// static grid-stride order (deterministic per-CTA partials for LW).
 template <int D, typename T, typename Z, class Chk, bool LW>
 __global__ void __launch_bounds__(kRowThreads) k_fine_rows(GridDev g, RowTiling rt, Widths W, const T* __restrict__ u,
                                                           Z* __restrict__ zz, unsigned long long* __restrict__ hist,
@@ -225,100 +234,110 @@ __global__ void __launch_bounds__(kRowThreads) k_fine_rows(GridDev g, RowTiling 
                                                           const Z* __restrict__ zc, Chk chk,
                                                           unsigned long long* __restrict__ red_out, Widths lw,
                                                           double* __restrict__ partials) {
+  constexpr int NS = 1 << (D - 1);
   __shared__ RowMeta meta[kRowMaxR];
   __shared__ uint32_t sh[256];
   __shared__ double sred[kRowThreads / 32];
   for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
   auto ldu = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
   auto lde = [ec](uint64_t off) { return __ldg(ec + off); };
+  const AxisTab& ax = g.ax[D - 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t hsym = 0, hcnt = 0;
   unsigned long long ovf = 0;
   unsigned wide = 0;
   double red = 0.0;
+  const double dL = W.w[g.L];
   const uint64_t ntiles = ((rt.nrows + rt.R - 1) / rt.R) * rt.ncol_tiles;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {  // static, deterministic schedule
-  const uint64_t row_tile = tile / rt.ncol_tiles;
-  const uint32_t col_tile = static_cast<uint32_t>(tile - row_tile * rt.ncol_tiles);
-  const uint64_t r0 = row_tile * rt.R;
-  const uint32_t R = static_cast<uint32_t>(umin64(rt.R, rt.nrows - r0));
-  const uint32_t k0 = col_tile * rt.K;
-  const uint32_t Kt = min(rt.K, rt.n_last - k0);
-  __syncthreads();  // previous tile's rows no longer in use
-  build_rows<D>(g, rt, r0, R, meta);
-  __syncthreads();
-  const uint32_t E = R * Kt;
-  const float invK = Kt == rt.K ? rt.invK : 1.0f / static_cast<float>(Kt);
-  for (uint32_t idx = threadIdx.x; idx < E; idx += kRowThreads) {
-    uint32_t rr, kk;
-    tile_rc(idx, Kt, invK, rr, kk);
-    const uint32_t k = k0 + kk;
-    const RowMeta& m = meta[rr];
-    const uint64_t n = m.own + k;
-    const double src = static_cast<double>(__ldg(u + n));
-    uint64_t z = 0;
-    double e = 0.0, r = 0.0;
-    int tag;
-    if (g.L == 0) {  // every node is level 0: c = u
-      tag = 0;
-      const double scaled = __ddiv_rn(src, W.w[0]);
-      if (!(fabs(scaled) < 9223372036854775808.0)) {
-        ++ovf;
-      } else {
-        const long long q = __double2ll_rn(scaled);
-        r = __dsub_rn(src, __dmul_rn(__ll2double_rn(q), W.w[0]));
-        z = zigzag(q);
-      }
-      e = r;
-    } else {
-      const bool last_fine = __ldg(g.ax[D - 1].lvl + k) == g.L;
-      if (m.all_fine || last_fine) {
-        tag = g.L;
-        const LastAxis la = last_axis(g, D, k);
-        const double acc = row_interp(m, m.uoff, la, k, la.kl, la.kr, ldu);
-        const double c = __dsub_rn(src, acc);
-        const double delta = W.w[g.L];
-        const double scaled = __ddiv_rn(c, delta);
-        if (!(fabs(scaled) < 9223372036854775808.0)) {
-          ++ovf;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t row_tile = tile / rt.ncol_tiles;
+    const uint32_t col_tile = static_cast<uint32_t>(tile - row_tile * rt.ncol_tiles);
+    const uint64_t r0 = row_tile * rt.R;
+    const uint32_t R = static_cast<uint32_t>(umin64(rt.R, rt.nrows - r0));
+    const uint32_t k0 = col_tile * rt.K;
+    const uint32_t Kt = min(rt.K, rt.n_last - k0);
+    __syncthreads();  // previous tile's rows no longer in use
+    build_rows<D>(g, rt, r0, R, meta);
+    __syncthreads();
+    const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
+    for (uint32_t unit = warp; unit < R * nchunks; unit += kRowThreads / 32) {
+      const uint32_t rr = unit / nchunks, ch = unit - rr * nchunks;
+      RowRegs<NS> m;
+      m.load(meta[rr]);
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const uint32_t kk = ch * kUnitCols + 2 * lane + cc;
+        if (kk >= Kt) continue;
+        const uint32_t k = k0 + kk;
+        const uint64_t n = m.own + k;
+        const double src = static_cast<double>(__ldg(u + n));
+        uint64_t z = 0;
+        double e = 0.0, r = 0.0;
+        int tag = 0;
+        if (g.L == 0) {  // every node is level 0: c = u
+          const double scaled = __ddiv_rn(src, W.w[0]);
+          if (!(fabs(scaled) < 9223372036854775808.0)) {
+            ++ovf;
+          } else {
+            const long long q = __double2ll_rn(scaled);
+            r = __dsub_rn(src, __dmul_rn(__ll2double_rn(q), W.w[0]));
+            z = zigzag(q);
+          }
+          e = r;
         } else {
-          const long long q = __double2ll_rn(scaled);
-          r = __dsub_rn(c, __dmul_rn(__ll2double_rn(q), delta));
-          z = zigzag(q);
+          const uint2 cc2 = __ldg(reinterpret_cast<const uint2*>(ax.colc) + k);
+          const bool fresh = cc2.y != kNotFresh;
+          if (m.all_fine || fresh) {
+            tag = g.L;
+            double wl = 0.0, wr = 0.0;
+            if (fresh) {
+              const double2 ww = __ldg(reinterpret_cast<const double2*>(ax.colw) + k);
+              wl = ww.x;
+              wr = ww.y;
+            }
+            const double acc = interp_any<NS>(m, m.uoff, fresh, k, k - 1, k + 1, wl, wr, ldu);
+            const double c = __dsub_rn(src, acc);
+            const double scaled = __ddiv_rn(c, dL);
+            if (!(fabs(scaled) < 9223372036854775808.0)) {
+              ++ovf;
+            } else {
+              const long long q = __double2ll_rn(scaled);
+              r = __dsub_rn(c, __dmul_rn(__ll2double_rn(q), dL));
+              z = zigzag(q);
+            }
+            if (!LW) e = __dadd_rn(r, interp_any<NS>(m, m.coff, fresh, cc2.x, cc2.x, cc2.y, wl, wr, lde));
+          } else {  // coarse-box node: finished by k_coarse_quant / the coarse inverse
+            const uint64_t cj = m.cown + cc2.x;
+            z = static_cast<uint64_t>(zc[cj]);
+            if (!LW) {
+              e = ec[cj];
+            } else {  // the level-weighted estimator needs this node's tag and r
+              uint32_t i[4] = {0, 0, 0, 0};
+              decompose<D>(g, n, i);
+              tag = node_tag<D>(g, i);
+              r = ec[cj];
+            }
+          }
         }
-        if (!LW) e = __dadd_rn(r, row_interp(m, m.coff, la, la.ck, la.ckl, la.ckr, lde));
-      } else {  // coarse-box node: finished by k_coarse_quant / the coarse inverse
-        const uint64_t cj = m.cown + __ldg(g.ax[D - 1].cpos + k);
-        z = static_cast<uint64_t>(zc[cj]);
-        if (!LW) e = ec[cj];
-        if (LW) {  // the level-weighted estimator needs this node's tag and r
-          uint32_t i[4] = {0, 0, 0, 0};
-          decompose<D>(g, n, i);
-          tag = node_tag<D>(g, i);
-          r = ec[cj];
-        } else {
-          tag = 0;
-        }
+        if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
+        zz[n] = static_cast<Z>(z);
+        hist_varint(sh, z, hsym, hcnt);
+        if (LW) red = __dadd_rn(red, __dmul_rn(lw.w[tag], __dmul_rn(r, r)));
+        else chk(n, e, src, red);
       }
     }
-    if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
-    zz[n] = static_cast<Z>(z);
-    hist_varint(sh, z, hsym, hcnt);
-    if (LW) red = __dadd_rn(red, __dmul_rn(lw.w[tag], __dmul_rn(r, r)));
-    else chk(n, e, src, red);
   }
-  }  // tiles
   hist_flush(sh, hsym, hcnt);
   if (ovf) atomicAdd(&flags->overflow, ovf);
   if (wide) atomicOr(&flags->wide, 1u);
   if (LW) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) red = __dadd_rn(red, __shfl_down_sync(0xffffffffu, red, o));
-    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = red;
+    if (lane == 0) sred[warp] = red;
   } else if (red_out) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) red = fmax(red, __shfl_xor_sync(0xffffffffu, red, o));
-    if ((threadIdx.x & 31) == 0 && red > 0.0)
-      atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
+    if (lane == 0 && red > 0.0) atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
   }
   __syncthreads();
   if (LW && threadIdx.x == 0) {
@@ -368,6 +387,7 @@ template <int D, typename Z, class Out>
 __global__ void __launch_bounds__(kRowThreads) k_recon_rows(GridDev g, RowTiling rt, Widths W,
                                                            const Z* __restrict__ zz, const double* __restrict__ vc,
                                                            Out out) {
+  constexpr int NS = 1 << (D - 1);
   __shared__ RowMeta meta[kRowMaxR];
   const uint64_t row_tile = blockIdx.x / rt.ncol_tiles;
   const uint32_t col_tile = blockIdx.x - static_cast<uint32_t>(row_tile * rt.ncol_tiles);
@@ -378,25 +398,41 @@ __global__ void __launch_bounds__(kRowThreads) k_recon_rows(GridDev g, RowTiling
   build_rows<D>(g, rt, r0, R, meta);
   __syncthreads();
   auto ldv = [vc](uint64_t off) { return __ldg(vc + off); };
-  const uint32_t E = R * Kt;
-  const float invK = Kt == rt.K ? rt.invK : 1.0f / static_cast<float>(Kt);
-  for (uint32_t idx = threadIdx.x; idx < E; idx += kRowThreads) {
-    uint32_t rr, kk;
-    tile_rc(idx, Kt, invK, rr, kk);
-    const uint32_t k = k0 + kk;
-    const RowMeta& m = meta[rr];
-    const uint64_t n = m.own + k;
-    double v;
-    if (g.L == 0) {
-      v = __dmul_rn(__ll2double_rn(unzigzag(static_cast<uint64_t>(zz[n]))), W.w[0]);
-    } else if (m.all_fine || __ldg(g.ax[D - 1].lvl + k) == g.L) {
-      const LastAxis la = last_axis(g, D, k);
-      const double base = __dmul_rn(__ll2double_rn(unzigzag(static_cast<uint64_t>(zz[n]))), W.w[g.L]);
-      v = __dadd_rn(base, row_interp(m, m.coff, la, la.ck, la.ckl, la.ckr, ldv));
-    } else {
-      v = vc[m.cown + __ldg(g.ax[D - 1].cpos + k)];
+  const AxisTab& ax = g.ax[D - 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double dL = W.w[g.L];
+  const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
+  for (uint32_t unit = warp; unit < R * nchunks; unit += kRowThreads / 32) {
+    const uint32_t rr = unit / nchunks, ch = unit - rr * nchunks;
+    RowRegs<NS> m;
+    m.load(meta[rr]);
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const uint32_t kk = ch * kUnitCols + 2 * lane + cc;
+      if (kk >= Kt) continue;
+      const uint32_t k = k0 + kk;
+      const uint64_t n = m.own + k;
+      double v;
+      if (g.L == 0) {
+        v = __dmul_rn(__ll2double_rn(unzigzag(static_cast<uint64_t>(zz[n]))), W.w[0]);
+      } else {
+        const uint2 cc2 = __ldg(reinterpret_cast<const uint2*>(ax.colc) + k);
+        const bool fresh = cc2.y != kNotFresh;
+        if (m.all_fine || fresh) {
+          double wl = 0.0, wr = 0.0;
+          if (fresh) {
+            const double2 ww = __ldg(reinterpret_cast<const double2*>(ax.colw) + k);
+            wl = ww.x;
+            wr = ww.y;
+          }
+          const double base = __dmul_rn(__ll2double_rn(unzigzag(static_cast<uint64_t>(zz[n]))), dL);
+          v = __dadd_rn(base, interp_any<NS>(m, m.coff, fresh, cc2.x, cc2.x, cc2.y, wl, wr, ldv));
+        } else {
+          v = vc[m.cown + cc2.x];
+        }
+      }
+      out(n, v);
     }
-    out(n, v);
   }
 }
 
