@@ -5,6 +5,8 @@ Bar (north_star / SURVEY §8): containers byte-identical to the reference's
 identical ratio), decompressed arrays bit-identical to the reference's
 decompressor, and every reconstruction within the requested bound.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -150,3 +152,37 @@ def test_corrupt_streams_match_reference_errors(mg, oracle):
         assert gerr == werr, (trial, gerr, werr)
         if werr is None:
             assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configurations at full size: the container the
+# GPU produces is byte-identical to the CPU reference's on the same input
+# bytes, and the GPU decompressor reproduces the reference decompressor's
+# output bit for bit.  (cfg 2: ~30 s of CPU oracle time; cfg 3: ~15 s.)
+FULL = [
+    ("cfg2_513cubed_f32_inf_rel1e-4", (513, 513, 513), np.float32, 1e-4, 0, 0.0, 1),
+    ("cfg3_8193sq_f64_s1_rel1e-3", (8193, 8193), np.float64, 1e-3, 1, 1.0, 1),
+]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", FULL, ids=lambda c: c[0])
+def test_full_size_parity(mg, oracle, case):
+    name, shape, dt, tol, norm, s, mode = case
+    u = oracle.multisine(shape).astype(dt)
+    spec = mg.ErrorSpec(tol, mg.Norm(norm), s, mg.Mode(mode))
+    got = mg.compress(u, mg.make_grid(shape), spec, mg.Codec.huffman)
+    from oracle import binding
+
+    if binding.available("reference"):  # the reference library itself (OpenMP), else the restatement
+        oracle = binding.get("reference")
+        oracle.set_threads(os.cpu_count() or 1)
+    want = oracle.compress(u, tol, norm, s, mode, 2)
+    assert len(got) == len(want)
+    assert got == want
+    back = mg.decompress(want)
+    ref_back = oracle.decompress(want)
+    assert np.array_equal(back.view(np.uint8), ref_back.view(np.uint8))
+    if norm == 0:
+        tau = tol * float(u.max() - u.min())
+        assert float(np.max(np.abs(back.astype(np.float64) - u))) <= tau
