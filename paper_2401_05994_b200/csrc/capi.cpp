@@ -145,6 +145,83 @@ std::vector<std::pair<uint64_t, uint64_t>> split_multiblock(const uint8_t* f, ui
   return out;
 }
 
+
+// Owned device allocation (RAII).
+struct DeviceArray {
+  void* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t bytes) {
+    if (bytes <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      raise(Errc::cuda, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    }
+    n = bytes;
+  }
+  ~DeviceArray() {
+    if (p) cudaFree(p);
+  }
+};
+
+// Block `rng` of a device array of `shape`: a pointer into it when the block
+// is contiguous (only leading axes split), else a device gather of the box
+// (cudaMemcpy3D over the last three axes, looped over the first).
+const void* copy_box(cudaStream_t st, const void* data, size_t unit, int d, const uint64_t* shape,
+                     const std::vector<Range>& rng, DeviceArray& tmp) {
+  uint64_t stride[kMaxDims];
+  stride[d - 1] = 1;
+  for (int a = d - 1; a > 0; --a) stride[a - 1] = stride[a] * shape[a];
+  int first_partial = -1;
+  for (int a = 0; a < d; ++a)
+    if (rng[a].length() != shape[a]) {
+      first_partial = a;
+      break;
+    }
+  bool contiguous = true;
+  for (int a = first_partial + 1; first_partial >= 0 && a < d; ++a)
+    if (rng[a].length() != shape[a]) contiguous = false;
+  uint64_t origin = 0, bcount = 1;
+  for (int a = 0; a < d; ++a) {
+    origin += rng[a].begin * stride[a];
+    bcount *= rng[a].length();
+  }
+  const uint8_t* base = static_cast<const uint8_t*>(data);
+  if (contiguous) return base + origin * unit;
+  tmp.alloc(bcount * unit);
+  // view as [outer][n2][n1][n0] with the last three axes copied by cudaMemcpy3D
+  const int k = d >= 3 ? d - 3 : 0;  // axes [0, k) are looped
+  uint64_t ext[3] = {1, 1, 1}, full[3] = {1, 1, 1}, beg[3] = {0, 0, 0};
+  for (int a = k, j = 3 - (d - k); a < d; ++a, ++j) {
+    ext[j] = rng[a].length();
+    full[j] = shape[a];
+    beg[j] = rng[a].begin;
+  }
+  uint64_t nouter = 1;
+  for (int a = 0; a < k; ++a) nouter *= rng[a].length();
+  uint8_t* dst = static_cast<uint8_t*>(tmp.p);
+  std::vector<uint64_t> pos(std::max(k, 1), 0);
+  for (uint64_t o = 0; o < nouter; ++o) {
+    uint64_t src_off = 0;
+    for (int a = 0; a < k; ++a) src_off += (rng[a].begin + pos[a]) * stride[a];
+    cudaMemcpy3DParms p{};
+    p.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(base + src_off * unit), full[2] * unit, full[2], full[1]);
+    p.srcPos = make_cudaPos(beg[2] * unit, beg[1], beg[0]);
+    p.dstPtr = make_cudaPitchedPtr(dst + o * ext[0] * ext[1] * ext[2] * unit, ext[2] * unit, ext[2], ext[1]);
+    p.dstPos = make_cudaPos(0, 0, 0);
+    p.extent = make_cudaExtent(ext[2] * unit, ext[1], ext[0]);
+    p.kind = cudaMemcpyDeviceToDevice;
+    if (cudaMemcpy3DAsync(&p, st) != cudaSuccess) raise(Errc::cuda, "block gather failed");
+    for (int a = k - 1; a >= 0; --a) {
+      if (++pos[a] < rng[a].length()) break;
+      pos[a] = 0;
+    }
+  }
+  return tmp.p;
+}
+
 }  // namespace
 
 extern "C" {
@@ -352,22 +429,31 @@ int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndims, const uint
       ErrorSpec bspec = spec;
       bspec.mode = Mode::abs;
       const uint64_t count = whole.count();
+      // the whole array on the device once; blocks are cut from it there
+      cudaStream_t st = context_stream(ctx);
+      DeviceArray staged;
+      const void* ddata = data;
+      if (!is_device_pointer(data)) {
+        staged.alloc(count * unit);
+        if (cudaMemcpyAsync(staged.p, data, count * unit, cudaMemcpyHostToDevice, st) != cudaSuccess)
+          raise(Errc::cuda, "input upload failed");
+        ddata = staged.p;
+      }
       if (spec.mode == Mode::rel) {  // global normalisation (tools/mgrc.cpp:405-418)
-        const FieldStats st = field_stats(ctx, data, dt, count);
-        if (st.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
-        double nrm = st.max - st.min;
+        const FieldStats fs = field_stats(ctx, ddata, dt, count);
+        if (fs.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
+        double nrm = fs.max - fs.min;
         if (spec.norm == Norm::s) {
-          // RMS over the whole array: 4096-block ordered sum (the CLI's scan is
-          // fully serial; this differs from it by rounding only).
+          // RMS over the whole array in the CLI's fully serial order (mgrc.cpp:197-233)
           std::vector<uint8_t> host;
           const void* src = data;
-          double ss = 0.0;
           if (is_device_pointer(data)) {
             host.resize(count * unit);
             if (cudaMemcpy(host.data(), data, count * unit, cudaMemcpyDeviceToHost) != cudaSuccess)
               raise(Errc::cuda, "copy failed");
             src = host.data();
           }
+          double ss = 0.0;
           for (uint64_t i = 0; i < count; ++i) {
             const double v = dt == DType::f32 ? static_cast<double>(static_cast<const float*>(src)[i])
                                               : static_cast<const double*>(src)[i];
@@ -378,61 +464,21 @@ int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndims, const uint
         if (nrm == 0.0) raise(Errc::degenerate_data, "relative bound on a constant file");
         bspec.tol = spec.tol * nrm;
       }
-      const bool on_dev = is_device_pointer(data);
-      uint64_t stride[kMaxDims];
-      stride[ndims - 1] = 1;
-      for (int a = ndims - 1; a > 0; --a) stride[a - 1] = stride[a] * shape[a];
-      std::vector<uint8_t> gather;
-
+      DeviceArray gather;
       for (uint64_t b = 0; b < nb; ++b) {
         const auto rng = plan.block(b);
         uint64_t bshape[kMaxDims];
         std::vector<double> bc[kMaxDims];
         const double* cptr[kMaxDims];
+        uint64_t bcount = 1;
         for (int a = 0; a < ndims; ++a) {
           bshape[a] = rng[a].length();
+          bcount *= bshape[a];
           bc[a].assign(whole.coords[a].begin() + rng[a].begin, whole.coords[a].begin() + rng[a].end);
           cptr[a] = bc[a].data();
         }
-        // contiguous iff all axes after the first partial one are whole
-        bool contiguous = true;
-        int first_partial = -1;
-        for (int a = 0; a < ndims; ++a)
-          if (bshape[a] != shape[a]) {
-            first_partial = a;
-            break;
-          }
-        for (int a = first_partial + 1; first_partial >= 0 && a < ndims; ++a)
-          if (bshape[a] != shape[a]) contiguous = false;
-        uint64_t origin = 0, bcount = 1;
-        for (int a = 0; a < ndims; ++a) {
-          origin += rng[a].begin * stride[a];
-          bcount *= bshape[a];
-        }
-        const void* bdata = static_cast<const uint8_t*>(data) + origin * unit;
-        if (!contiguous) {  // strided sub-box: gather rows
-          const uint64_t run = bshape[ndims - 1];
-          gather.resize(bcount * unit);
-          std::vector<uint64_t> pos(ndims, 0);
-          for (uint64_t row = 0; row < bcount / run; ++row) {
-            uint64_t off = rng[ndims - 1].begin;
-            for (int a = 0; a + 1 < ndims; ++a) off += (rng[a].begin + pos[a]) * stride[a];
-            const void* src = static_cast<const uint8_t*>(data) + off * unit;
-            if (on_dev) {
-              if (cudaMemcpy(gather.data() + row * run * unit, src, run * unit, cudaMemcpyDeviceToHost) !=
-                  cudaSuccess)
-                raise(Errc::cuda, "gather copy failed");
-            } else {
-              std::memcpy(gather.data() + row * run * unit, src, run * unit);
-            }
-            for (int a = ndims - 2; a >= 0; --a) {
-              if (++pos[a] < bshape[a]) break;
-              pos[a] = 0;
-            }
-          }
-          bdata = gather.data();
-        }
-
+        const void* bdata = copy_box(st, ddata, unit, ndims, shape, rng, gather);
+        (void)bcount;
         const Grid bg = make_grid(ndims, bshape, cptr);
         const ContainerParts parts = compress(ctx, bdata, dt, bg, bspec, cd);
         blocks[b].resize(parts.total());

@@ -528,6 +528,21 @@ struct FineRows {
   };
 };
 
+template <typename T, typename Z, class Chk>
+struct FinePairs {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const RowTiling& rt, const Widths& W, double inv_L, const T* u,
+                    Z* zz, unsigned long long* hist, QuantFlags* fl, const double* ec, const Z* zc, const Chk& chk,
+                    unsigned long long* red, int blocks) {
+      k_fine_warp<D, T, Z, Chk><<<num_sms() * 2, kRowThreads, 0, s>>>(g, rt, W, inv_L, u, zz, hist, fl, ec, zc, chk,
+                                                                       red);
+      check_launch("k_fine_warp");
+      (void)blocks;
+    }
+  };
+};
+
 template <typename Z>
 struct ReconCoarse {
   template <int D>
@@ -658,6 +673,11 @@ static double blocked_sumsq(Context& ctx, const T* v, uint64_t n) {
 FieldStats field_stats(Context& ctx, const void* data, DType dtype, uint64_t n) {
   Scratch* sd = ctx.sd();
   Scratch* sh = ctx.sh();
+  if (!is_device_pointer(data)) {  // host array: stage it (the kernels read device memory only)
+    void* d = ctx.in.get<uint8_t>(n * dtype_size(dtype));
+    CK(cudaMemcpyAsync(d, data, n * dtype_size(dtype), cudaMemcpyHostToDevice, ctx.stream));
+    data = d;
+  }
   if (dtype == DType::f32) launch_stats(ctx, static_cast<const float*>(data), n, &sd->stats);
   else launch_stats(ctx, static_cast<const double*>(data), n, &sd->stats);
   CK(cudaMemcpyAsync(&sh->stats, &sd->stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx.stream));
@@ -774,7 +794,23 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
           by_dim<FineRows<T, Z, ChkLevelWeighted, true>::template L>(grid.d, s, g, rt, W, u, zz, sd->hist,
                                                                      &sd->qflags, ec, zc, ChkLevelWeighted{}, nullptr,
                                                                      lw, part, fine_blocks);
-        else if (s0 && dtype == DType::f32)
+        else if (L >= 1) {
+          const double inv_L = 1.0 / widths[L];
+          if (s0 && dtype == DType::f32)
+            by_dim<FinePairs<T, Z, ChkCastStore>::template L>(grid.d, s, g, rt, W, inv_L, u, zz, sd->hist,
+                                                              &sd->qflags, ec, zc, ChkCastStore{estore}, nullptr,
+                                                              fine_blocks);
+          else if (s0)
+            by_dim<FinePairs<T, Z, ChkStore>::template L>(grid.d, s, g, rt, W, inv_L, u, zz, sd->hist, &sd->qflags,
+                                                          ec, zc, ChkStore{estore}, nullptr, fine_blocks);
+          else if (dtype == DType::f32)
+            by_dim<FinePairs<T, Z, ChkCastMaxAbs>::template L>(grid.d, s, g, rt, W, inv_L, u, zz, sd->hist,
+                                                               &sd->qflags, ec, zc, ChkCastMaxAbs{}, &sd->red_bits,
+                                                               fine_blocks);
+          else
+            by_dim<FinePairs<T, Z, ChkMaxAbs>::template L>(grid.d, s, g, rt, W, inv_L, u, zz, sd->hist, &sd->qflags,
+                                                           ec, zc, ChkMaxAbs{}, &sd->red_bits, fine_blocks);
+        } else if (s0 && dtype == DType::f32)
           by_dim<FineRows<T, Z, ChkCastStore, false>::template L>(grid.d, s, g, rt, W, u, zz, sd->hist, &sd->qflags,
                                                                   ec, zc, ChkCastStore{estore}, nullptr, lw, part,
                                                                   fine_blocks);

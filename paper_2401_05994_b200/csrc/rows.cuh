@@ -350,6 +350,378 @@ __global__ void __launch_bounds__(kRowThreads) k_fine_rows(GridDev g, RowTiling 
 }
 
 // ---------------------------------------------------------------------------
+// Quantisation q = round_half_even(c / δ) (quantize.cpp:105-123) without the
+// IEEE division on the common path: t = c · fl(1/δ) differs from the exact
+// quotient fl(c/δ) by at most 2^-51·|t|, so whenever t is farther than
+// 2^-49·|t| from every half-integer both round to the same integer; otherwise
+// (probability ~2^-48·|t|) and for |t| ≥ 2^50 the exact division decides.
+// Returns false on overflow (|c/δ| ≥ 2^63, quantize.cpp:113-116).
+__device__ __forceinline__ bool quantize_fast(double c, double delta, double inv, long long& q, double& r) {
+  const double t = __dmul_rn(c, inv);
+  const double at = fabs(t);
+  if (at < 1125899906842624.0) {  // 2^50
+    const double f = __dsub_rn(t, floor(t));
+    if (fabs(__dsub_rn(f, 0.5)) > __dmul_rn(at, 1.7763568394002505e-15)) {  // 2^-49
+      q = __double2ll_rn(t);
+      r = __dsub_rn(c, __dmul_rn(__ll2double_rn(q), delta));
+      return true;
+    }
+  }
+  const double scaled = __ddiv_rn(c, delta);
+  if (!(fabs(scaled) < 9223372036854775808.0)) return false;
+  q = __double2ll_rn(scaled);
+  r = __dsub_rn(c, __dmul_rn(__ll2double_rn(q), delta));
+  return true;
+}
+
+// Fused finest-level pass, column-pair form.  Each lane owns columns (k, k+1)
+// with k even: at the finest level an even column is never fresh and an odd
+// one is fresh unless it is the last index, whose bracketing neighbours are
+// k and k+2.  So the corner values of the odd column are the even column's
+// (own lane) and the next lane's even column (warp shuffle), halving the
+// gathers; the coarse-box errors are shared the same way.  Rows whose outer
+// indices are all coarse (t_o < L) have their even column in the coarse box
+// (code and error read from zc/ec) and only the last axis fresh on the odd
+// one.  The number of outer corner rows M (1, 2, 4, 8) is warp-uniform and
+// dispatched to a specialised body.  Same arithmetic, same order as
+// transform.cpp:111-128.
+template <typename T, typename Z, class Chk>
+struct PairCtx {
+  const GridDev* g;
+  const T* __restrict__ u;
+  Z* __restrict__ zz;
+  const double* __restrict__ ec;
+  const Z* __restrict__ zc;
+  const uint4* colc4;
+  const double2* colw;
+  double dL, inv_L;
+  Chk chk;
+  uint32_t* sh;
+  uint32_t hsym, hcnt;
+  unsigned long long ovf;
+  unsigned wide;
+  double red;
+
+  __device__ __forceinline__ uint64_t quant(double c, double& r) {
+    long long q;
+    if (!quantize_fast(c, dL, inv_L, q, r)) {
+      ++ovf;
+      r = 0.0;
+      return 0;
+    }
+    return zigzag(q);
+  }
+  __device__ __forceinline__ void emit(uint64_t n, uint64_t z, double e, double src) {
+    if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
+    zz[n] = static_cast<Z>(z);
+    hist_varint(sh, z, hsym, hcnt);
+    chk(n, e, src, red);
+  }
+  __device__ __forceinline__ double ld(uint64_t i) const { return static_cast<double>(__ldg(u + i)); }
+
+  // one row unit (64 columns) with M outer corner rows (M = 1: row not all-fine)
+  template <int M, class Meta>
+  __device__ __forceinline__ void unit(const Meta& m, uint32_t k0, uint32_t kk, uint32_t Kt, int lane) {
+    const bool va = kk < Kt, vb = kk + 1 < Kt;
+    const uint32_t k = k0 + min(kk, Kt - 1);
+    const uint4 cc = __ldg(colc4 + (k >> 1));
+    const bool fb = vb && cc.w != kNotFresh;
+    const bool fine = M > 1;  // row all-fine (every node tagged L)
+    const uint64_t own = m.own;
+    const uint64_t n = own + k;
+    const double sa = ld(n);
+    const double sb = vb ? ld(n + 1) : 0.0;
+    double wl = 0.0, wr = 0.0;
+    if (fb) {
+      const double2 ww = __ldg(colw + k + 1);
+      wl = ww.x;
+      wr = ww.y;
+    }
+    double U0[M], U2[M], E0[M], E2[M];
+    const uint64_t cbase0 = fine ? 0 : m.cown;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      U0[j] = fine ? ld(m.uoff[j] + k) : sa;
+      E0[j] = __ldg(ec + (fine ? m.coff[j] : cbase0) + cc.x);
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      U2[j] = __shfl_down_sync(0xffffffffu, U0[j], 1);
+      E2[j] = __shfl_down_sync(0xffffffffu, E0[j], 1);
+    }
+    if (fb && (lane == 31 || kk + 2 >= Kt)) {  // column k+2 is not held by the next lane
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        U2[j] = ld((fine ? m.uoff[j] : own) + k + 2);
+        E2[j] = __ldg(ec + (fine ? m.coff[j] : cbase0) + cc.w);
+      }
+    }
+    if (!va) return;
+    // column k (even, never fresh)
+    if (fine) {
+      double acc = 0.0, eacc = 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], U0[j]));
+#pragma unroll
+      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(m.w[j], E0[j]));
+      double r;
+      const uint64_t z = quant(__dsub_rn(sa, acc), r);
+      emit(n, z, __dadd_rn(r, eacc), sa);
+    } else {
+      emit(n, static_cast<uint64_t>(zc[cbase0 + cc.x]), E0[0], sa);
+    }
+    if (!vb) return;
+    // column k+1
+    if (fb) {
+      double wlj[M], wrj[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        wlj[j] = __dmul_rn(m.w[j], wl);
+        wrj[j] = __dmul_rn(m.w[j], wr);
+      }
+      double acc = 0.0, eacc = 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(wlj[j], U0[j]));
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(wrj[j], U2[j]));
+#pragma unroll
+      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(wlj[j], E0[j]));
+#pragma unroll
+      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(wrj[j], E2[j]));
+      double r;
+      const uint64_t z = quant(__dsub_rn(sb, acc), r);
+      emit(n + 1, z, __dadd_rn(r, eacc), sb);
+    } else if (fine) {  // last index of an even-length axis, tagged L by the outer axes
+      double acc = 0.0, eacc = 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], ld(m.uoff[j] + k + 1)));
+#pragma unroll
+      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(m.w[j], __ldg(ec + m.coff[j] + cc.z)));
+      double r;
+      const uint64_t z = quant(__dsub_rn(sb, acc), r);
+      emit(n + 1, z, __dadd_rn(r, eacc), sb);
+    } else {
+      const uint64_t cj = cbase0 + cc.z;
+      emit(n + 1, static_cast<uint64_t>(zc[cj]), ec[cj], sb);
+    }
+  }
+};
+
+template <int D, typename T, typename Z, class Chk>
+__global__ void __launch_bounds__(kRowThreads, 3) k_fine_pairs(GridDev g, RowTiling rt, Widths W, double inv_L,
+                                                              const T* __restrict__ u, Z* __restrict__ zz,
+                                                              unsigned long long* __restrict__ hist,
+                                                              QuantFlags* flags, const double* __restrict__ ec,
+                                                              const Z* __restrict__ zc, Chk chk,
+                                                              unsigned long long* __restrict__ red_out) {
+  __shared__ RowMeta meta[kRowMaxR];
+  __shared__ uint32_t sh[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  PairCtx<T, Z, Chk> P;
+  P.g = &g;
+  P.u = u;
+  P.zz = zz;
+  P.ec = ec;
+  P.zc = zc;
+  P.colc4 = reinterpret_cast<const uint4*>(g.ax[D - 1].colc);
+  P.colw = reinterpret_cast<const double2*>(g.ax[D - 1].colw);
+  P.dL = W.w[g.L];
+  P.inv_L = inv_L;
+  P.chk = chk;
+  P.sh = sh;
+  P.hsym = P.hcnt = 0;
+  P.ovf = 0;
+  P.wide = 0;
+  P.red = 0.0;
+  const uint64_t ntiles = ((rt.nrows + rt.R - 1) / rt.R) * rt.ncol_tiles;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t row_tile = tile / rt.ncol_tiles;
+    const uint32_t col_tile = static_cast<uint32_t>(tile - row_tile * rt.ncol_tiles);
+    const uint64_t r0 = row_tile * rt.R;
+    const uint32_t R = static_cast<uint32_t>(umin64(rt.R, rt.nrows - r0));
+    const uint32_t k0 = col_tile * rt.K;  // even (K is n_last or 4096)
+    const uint32_t Kt = min(rt.K, rt.n_last - k0);
+    __syncthreads();
+    build_rows<D>(g, rt, r0, R, meta);
+    __syncthreads();
+    const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
+    uint32_t rr = 0, ch = warp;
+    while (ch >= nchunks && rr < R) {
+      ch -= nchunks;
+      ++rr;
+    }
+    for (; rr < R;) {
+      const RowMeta& m = meta[rr];
+      const uint32_t kk = ch * kUnitCols + 2 * lane;
+      if (!m.all_fine) P.template unit<1>(m, k0, kk, Kt, lane);
+      else if (D >= 4 && m.nsub == 8) P.template unit<(D >= 4 ? 8 : 2)>(m, k0, kk, Kt, lane);
+      else if (D >= 3 && m.nsub == 4) P.template unit<(D >= 3 ? 4 : 2)>(m, k0, kk, Kt, lane);
+      else P.template unit<2>(m, k0, kk, Kt, lane);
+      ch += kRowThreads / 32;
+      while (ch >= nchunks && rr < R) {
+        ch -= nchunks;
+        ++rr;
+      }
+    }
+  }
+  hist_flush(sh, P.hsym, P.hcnt);
+  if (P.ovf) atomicAdd(&flags->overflow, P.ovf);
+  if (P.wide) atomicOr(&flags->wide, 1u);
+  if (red_out) {
+    double red = P.red;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) red = fmax(red, __shfl_xor_sync(0xffffffffu, red, o));
+    if (lane == 0 && red > 0.0) atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
+}
+
+// Warp-per-row form of the fused pass: a warp owns whole row segments (no
+// CTA barriers), builds the row's corner metadata itself (lane j computes
+// outer corner row j, broadcast by shuffles) and software-pipelines its
+// 64-column units: the gathers of unit i+1 are in flight while unit i is
+// computed.
+template <int NS>
+struct RowLite {                 // warp-uniform row metadata in registers
+  uint64_t uoff[NS], coff[NS];
+  double w[NS];
+  uint64_t own, cown;
+  int nsub, all_fine;
+};
+
+template <int D>
+__device__ __forceinline__ void warp_row_meta(const GridDev& g, uint64_t row, RowLite<(1 << (D - 1))>& m) {
+  const int lane = threadIdx.x & 31;
+  uint32_t o[4] = {0, 0, 0, 0};
+  uint64_t q = row;
+#pragma unroll
+  for (int a = D - 2; a >= 0; --a) {
+    const uint64_t qq = q / g.shape[a];
+    o[a] = static_cast<uint32_t>(q - qq * g.shape[a]);
+    q = qq;
+  }
+  int t_o = 0;
+  uint32_t F = 0;
+  uint64_t own = 0, cown = 0;
+  bool all_coarse = true;
+  int lv[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < D - 1; ++a) {
+    lv[a] = __ldg(g.ax[a].lvl + o[a]);
+    t_o = max(t_o, lv[a]);
+    own += static_cast<uint64_t>(o[a]) * g.stride[a];
+    if (lv[a] == g.L) all_coarse = false;
+    else cown += static_cast<uint64_t>(__ldg(g.ax[a].cpos + o[a])) * g.cstride[a];
+  }
+  m.own = own;
+  m.cown = all_coarse ? cown : ~0ull;
+  m.all_fine = t_o == g.L ? 1 : 0;
+  if (m.all_fine) {
+#pragma unroll
+    for (int a = 0; a < D - 1; ++a)
+      if (lv[a] == g.L) F |= 1u << a;
+  }
+  const int nsub = 1 << __popc(F);
+  m.nsub = nsub;
+  // lane j < nsub: the j-th submask of F (increasing order) -> corner row j
+  uint64_t uo = 0, co = 0;
+  double w = 1.0;
+  if (lane < nsub) {
+    // expand the j-th submask: bit b of j selects the b-th fresh axis (ascending)
+    int b = 0;
+#pragma unroll
+    for (int a = 0; a < D - 1; ++a) {
+      if ((F >> a) & 1u) {
+        const bool right = (lane >> b) & 1;
+        ++b;
+        w = __dmul_rn(w, right ? __ldg(g.ax[a].wr + o[a]) : __ldg(g.ax[a].wl + o[a]));
+        uo += static_cast<uint64_t>(right ? __ldg(g.ax[a].right + o[a]) : __ldg(g.ax[a].left + o[a])) * g.stride[a];
+        co += static_cast<uint64_t>(right ? __ldg(g.ax[a].cr + o[a]) : __ldg(g.ax[a].cl + o[a])) * g.cstride[a];
+      } else {
+        uo += static_cast<uint64_t>(o[a]) * g.stride[a];
+        co += static_cast<uint64_t>(__ldg(g.ax[a].cpos + o[a])) * g.cstride[a];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < (1 << (D - 1)); ++j) {
+    m.uoff[j] = __shfl_sync(0xffffffffu, uo, j);
+    m.coff[j] = __shfl_sync(0xffffffffu, co, j);
+    m.w[j] = __shfl_sync(0xffffffffu, w, j);
+  }
+}
+
+// Registers of one 64-column unit (lane: columns k, k+1).
+template <int M>
+struct UnitLoads {
+  uint4 cc;
+  double sa, sb, wl, wr;
+  double U0[M], E0[M];
+};
+
+template <int D, typename T, typename Z, class Chk>
+__global__ void __launch_bounds__(kRowThreads, 2) k_fine_warp(GridDev g, RowTiling rt, Widths W, double inv_L,
+                                                             const T* __restrict__ u, Z* __restrict__ zz,
+                                                             unsigned long long* __restrict__ hist, QuantFlags* flags,
+                                                             const double* __restrict__ ec, const Z* __restrict__ zc,
+                                                             Chk chk, unsigned long long* __restrict__ red_out) {
+  __shared__ uint32_t sh[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  PairCtx<T, Z, Chk> P;
+  P.g = &g;
+  P.u = u;
+  P.zz = zz;
+  P.ec = ec;
+  P.zc = zc;
+  P.colc4 = reinterpret_cast<const uint4*>(g.ax[D - 1].colc);
+  P.colw = reinterpret_cast<const double2*>(g.ax[D - 1].colw);
+  P.dL = W.w[g.L];
+  P.inv_L = inv_L;
+  P.chk = chk;
+  P.sh = sh;
+  P.hsym = P.hcnt = 0;
+  P.ovf = 0;
+  P.wide = 0;
+  P.red = 0.0;
+  const uint64_t nitems = rt.nrows * rt.ncol_tiles;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t item = gw; item < nitems; item += nwarps) {
+    const uint64_t row = item / rt.ncol_tiles;
+    const uint32_t seg = static_cast<uint32_t>(item - row * rt.ncol_tiles);
+    const uint32_t k0 = seg * rt.K;  // even
+    const uint32_t Kt = min(rt.K, rt.n_last - k0);
+    RowLite<(1 << (D - 1))> mm;
+    warp_row_meta<D>(g, row, mm);
+    const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
+    for (uint32_t ch = 0; ch < nchunks; ++ch) {
+      const uint32_t kk = ch * kUnitCols + 2 * lane;
+      if (!mm.all_fine) P.template unit<1>(mm, k0, kk, Kt, lane);
+      else if (D >= 4 && mm.nsub == 8) P.template unit<(D >= 4 ? 8 : 2)>(mm, k0, kk, Kt, lane);
+      else if (D >= 3 && mm.nsub == 4) P.template unit<(D >= 3 ? 4 : 2)>(mm, k0, kk, Kt, lane);
+      else P.template unit<2>(mm, k0, kk, Kt, lane);
+    }
+  }
+  hist_flush(sh, P.hsym, P.hcnt);
+  if (P.ovf) atomicAdd(&flags->overflow, P.ovf);
+  if (P.wide) atomicOr(&flags->wide, 1u);
+  if (red_out) {
+    double red = P.red;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) red = fmax(red, __shfl_xor_sync(0xffffffffu, red, o));
+    if (lane == 0 && red > 0.0) atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
+}
+
+// ---------------------------------------------------------------------------
 // Decompress: dequantised coarse box (compact), then the row reconstruction.
 
 template <int D, typename Z>
