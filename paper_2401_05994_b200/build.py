@@ -17,7 +17,6 @@ ROOT = PKG.parent
 LIB = PKG / "libmgrc_gpu.so"
 
 SOURCES = ["pipeline.cu", "host.cpp", "capi.cpp"]
-HEADERS = ["kernels.cuh", "pipeline.hpp", "host.hpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,7 +39,8 @@ def needs_build() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "mgrc_gpu.h", Path(__file__)]
+    deps = ([CSRC / s for s in SOURCES] + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.hpp")) +
+            [ROOT / "include" / "mgrc_gpu.h", Path(__file__)])
     return any(p.stat().st_mtime > t for p in deps)
 
 

@@ -18,6 +18,8 @@ namespace mgrc_gpu {
 namespace dev {
 
 constexpr int kWarmBits = 1024;  // warm-up decoded before each subsequence's nominal start
+constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never published)
+constexpr int kSyncReal = kDecThreads - kSyncWarm;
 constexpr int kStageWords = kDecThreads * kSeqBits / 32;
 constexpr int kTailWords = 32;   // look-ahead past the last subsequence (open codewords / varints)
 constexpr int kStageTotal = kWarmBits / 32 + kStageWords + kTailWords + 4;
@@ -137,13 +139,18 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __r
   __shared__ int nbad;
   const int lutn = 1 << maxlen;
   for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
-  const uint64_t cta_bit = static_cast<uint64_t>(blockIdx.x) * kDecThreads * kSeqBits;
-  const uint64_t base = blockIdx.x ? cta_bit - kWarmBits : 0;  // first staged bit (word aligned)
+  // thread t <-> subsequence j = c·kSyncReal - kSyncWarm + t: the first
+  // kSyncWarm threads re-decode the predecessor CTA's last subsequences
+  // (never published) so that the CTA's first published start is true unless a
+  // desynchronisation outlasts kSyncWarm subsequences (then k_huff_fix_s).
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kSyncReal - kSyncWarm;
+  const uint64_t base = j0 > 0 ? static_cast<uint64_t>(j0) * kSeqBits - kWarmBits : 0;  // word aligned
   stage_words(w, nw, base >> 5, sm, kStageTotal);
   __syncthreads();
   const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
-  const uint64_t j = blockIdx.x * static_cast<uint64_t>(kDecThreads) + threadIdx.x;
-  const bool valid = j < nseq;
+  const int64_t js = j0 + static_cast<int64_t>(threadIdx.x);
+  const bool valid = js >= 0 && static_cast<uint64_t>(js) < nseq;
+  const uint64_t j = valid ? static_cast<uint64_t>(js) : 0;
   uint32_t F = 0, E = 0, nterm = 0, last = 0, end = 0;
   if (valid) {
     const uint32_t S = static_cast<uint32_t>(j * kSeqBits - base);
@@ -159,7 +166,8 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __r
   for (;;) {
     if (threadIdx.x == 0) nbad = 0;
     __syncthreads();
-    if (valid && threadIdx.x > 0 && sexit[threadIdx.x - 1] != sstart[threadIdx.x]) bad[atomicAdd(&nbad, 1)] = threadIdx.x;
+    if (valid && threadIdx.x > 0 && js > 0 && sexit[threadIdx.x - 1] != sstart[threadIdx.x])
+      bad[atomicAdd(&nbad, 1)] = threadIdx.x;
     __syncthreads();
     const int nb = nbad;
     if (nb == 0) break;
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __r
     }
     __syncthreads();
     if (t >= 0) {  // compacted re-decode of subsequence t from its predecessor's exit
-      const uint64_t jj = blockIdx.x * static_cast<uint64_t>(kDecThreads) + t;
+      const uint64_t jj = static_cast<uint64_t>(j0 + t);
       const uint32_t e2 = min(static_cast<uint32_t>(jj * kSeqBits - base) + static_cast<uint32_t>(kSeqBits), tl);
       BitReader br;
       br.init(sm, from);
@@ -186,11 +194,11 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __r
       s2.nterm = nt2;
       s2.last_cont = (last2 & 0xFF) >= 0x80;
       s2.pad = 0;
-      seq[jj] = s2;
+      if (t >= kSyncWarm) seq[jj] = s2;
     }
     __syncthreads();
   }
-  if (valid && sstart[threadIdx.x] == F && sexit[threadIdx.x] == E) {  // never re-decoded
+  if (valid && threadIdx.x >= kSyncWarm && sstart[threadIdx.x] == F && sexit[threadIdx.x] == E) {  // never re-decoded
     SeqInfo s;
     s.start = base + F;
     s.exit = base + E;
@@ -218,9 +226,9 @@ __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ 
   uint16_t* lut = reinterpret_cast<uint16_t*>(dyn + stage_idx(kFixWords) + 2);
   __shared__ int s_go;
   __shared__ unsigned long long s_from;
-  const uint64_t b = blockIdx.x + 1;
-  uint64_t j = b * kDecThreads;
-  const uint64_t jend = umin64(j + kDecThreads, nseq);
+  const uint64_t b = blockIdx.x + 1;  // edge b: first published subsequence of sync CTA b
+  uint64_t j = b * kSyncReal;
+  const uint64_t jend = umin64(j + kSyncReal, nseq);
   if (j >= nseq) return;
   bool lut_ready = false;
   while (j < jend) {

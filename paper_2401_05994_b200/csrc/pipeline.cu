@@ -560,8 +560,13 @@ struct ReconRows {
   struct L {
     static void run(cudaStream_t s, const GridDev& g, const RowTiling& rt, const Widths& W, const Z* zz,
                     const double* vc, const Out& out) {
-      k_recon_rows<D, Z, Out><<<static_cast<unsigned>(row_tiles(rt)), kRowThreads, 0, s>>>(g, rt, W, zz, vc, out);
-      check_launch("k_recon_rows");
+      if (g.L >= 1) {
+        k_recon_warp<D, Z, Out><<<num_sms() * 3, kRowThreads, 0, s>>>(g, rt, W, zz, vc, out);
+        check_launch("k_recon_warp");
+      } else {
+        k_recon_rows<D, Z, Out><<<static_cast<unsigned>(row_tiles(rt)), kRowThreads, 0, s>>>(g, rt, W, zz, vc, out);
+        check_launch("k_recon_rows");
+      }
     }
   };
 };
@@ -1171,10 +1176,10 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         const uint64_t nw = (body_len + 64) / 4;
         huff_smem_optin();
         prof.begin("huff_sync", static_cast<double>(body_len));
-        k_huff_sync_s<<<static_cast<unsigned>((nseq + kDecThreads - 1) / kDecThreads), kDecThreads,
-                        huff_smem(maxlen), s>>>(w, nw, T, lut, maxlen, nseq, seq);
+        const uint64_t nblk = (nseq + kSyncReal - 1) / kSyncReal;
+        k_huff_sync_s<<<static_cast<unsigned>(nblk), kDecThreads, huff_smem(maxlen), s>>>(w, nw, T, lut, maxlen,
+                                                                                         nseq, seq);
         check_launch("k_huff_sync_s");
-        const uint64_t nblk = (nseq + kDecThreads - 1) / kDecThreads;
         for (int it = 0; nblk > 1; ++it) {
           CK(cudaMemsetAsync(&sd->fix_changed, 0, 4, s));
           k_huff_fix_s<<<static_cast<unsigned>(nblk - 1), 32, fix_smem(maxlen), s>>>(w, nw, T, lut, maxlen, nseq, seq,

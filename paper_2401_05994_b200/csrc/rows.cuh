@@ -808,5 +808,132 @@ __global__ void __launch_bounds__(kRowThreads) k_recon_rows(GridDev g, RowTiling
   }
 }
 
+// Decompress finest level, warp-per-row column-pair form (see k_fine_warp):
+// v = q·δ_L + Σ w·v_coarse over the corners, coarse-box nodes copied from vc.
+template <typename Z, class Out>
+struct ReconCtx {
+  const Z* __restrict__ zz;
+  const double* __restrict__ vc;
+  const uint4* colc4;
+  const double2* colw;
+  double dL;
+  Out out;
+
+  template <int M>
+  struct Ld {  // one unit's loads, issued ahead of its arithmetic
+    uint4 cc;
+    uint64_t za, zb;
+    double2 ww;
+    double V0[M];
+    double V2x[M];  // column k+2 corners when the next lane does not hold them
+  };
+
+  template <int M, class Meta>
+  __device__ __forceinline__ void load(const Meta& m, uint32_t k0, uint32_t kk, uint32_t Kt, int lane,
+                                       Ld<M>& L) const {
+    const bool vb = kk + 1 < Kt;
+    const uint32_t k = k0 + min(kk, Kt - 1);
+    const bool fine = M > 1;
+    const uint64_t n = m.own + k;
+    const uint64_t cbase0 = fine ? 0 : m.cown;
+    L.cc = __ldg(colc4 + (k >> 1));
+    const bool fb = vb && L.cc.w != kNotFresh;
+    L.za = fine ? static_cast<uint64_t>(__ldg(zz + n)) : 0;
+    L.zb = (fb || (vb && fine)) ? static_cast<uint64_t>(__ldg(zz + n + 1)) : 0;
+    L.ww = fb ? __ldg(colw + k + 1) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < M; ++j) L.V0[j] = __ldg(vc + (fine ? m.coff[j] : cbase0) + L.cc.x);
+    if (fb && (lane == 31 || kk + 2 >= Kt)) {
+#pragma unroll
+      for (int j = 0; j < M; ++j) L.V2x[j] = __ldg(vc + (fine ? m.coff[j] : cbase0) + L.cc.w);
+    }
+  }
+
+  template <int M, class Meta>
+  __device__ __forceinline__ void compute(const Meta& m, uint32_t k0, uint32_t kk, uint32_t Kt, int lane,
+                                          const Ld<M>& L) const {
+    const bool va = kk < Kt, vb = kk + 1 < Kt;
+    const uint32_t k = k0 + min(kk, Kt - 1);
+    const bool fb = vb && L.cc.w != kNotFresh;
+    const bool fine = M > 1;
+    const uint64_t n = m.own + k;
+    const uint64_t cbase0 = fine ? 0 : m.cown;
+    double V2[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) V2[j] = __shfl_down_sync(0xffffffffu, L.V0[j], 1);
+    if (fb && (lane == 31 || kk + 2 >= Kt)) {
+#pragma unroll
+      for (int j = 0; j < M; ++j) V2[j] = L.V2x[j];
+    }
+    if (!va) return;
+    if (fine) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], L.V0[j]));
+      out(n, __dadd_rn(__dmul_rn(__ll2double_rn(unzigzag(L.za)), dL), acc));
+    } else {
+      out(n, L.V0[0]);
+    }
+    if (!vb) return;
+    if (fb) {
+      const double wl = L.ww.x, wr = L.ww.y;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wl), L.V0[j]));
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wr), V2[j]));
+      out(n + 1, __dadd_rn(__dmul_rn(__ll2double_rn(unzigzag(L.zb)), dL), acc));
+    } else if (fine) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], __ldg(vc + m.coff[j] + L.cc.z)));
+      out(n + 1, __dadd_rn(__dmul_rn(__ll2double_rn(unzigzag(L.zb)), dL), acc));
+    } else {
+      out(n + 1, vc[cbase0 + L.cc.z]);
+    }
+  }
+
+  // all units of one row segment, loads of unit i+1 in flight during unit i
+  template <int M, class Meta>
+  __device__ __forceinline__ void row(const Meta& m, uint32_t k0, uint32_t Kt, int lane) const {
+    const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
+    for (uint32_t ch = 0; ch < nchunks; ++ch) {
+      const uint32_t kk = ch * kUnitCols + 2 * lane;
+      Ld<M> cur;
+      load<M>(m, k0, kk, Kt, lane, cur);
+      compute<M>(m, k0, kk, Kt, lane, cur);
+    }
+  }
+};
+
+template <int D, typename Z, class Out>
+__global__ void __launch_bounds__(kRowThreads, 3) k_recon_warp(GridDev g, RowTiling rt, Widths W,
+                                                              const Z* __restrict__ zz, const double* __restrict__ vc,
+                                                              Out out) {
+  const int lane = threadIdx.x & 31;
+  ReconCtx<Z, Out> P;
+  P.zz = zz;
+  P.vc = vc;
+  P.colc4 = reinterpret_cast<const uint4*>(g.ax[D - 1].colc);
+  P.colw = reinterpret_cast<const double2*>(g.ax[D - 1].colw);
+  P.dL = W.w[g.L];
+  P.out = out;
+  const uint64_t nitems = rt.nrows * rt.ncol_tiles;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t item = gw; item < nitems; item += nwarps) {
+    const uint64_t row = item / rt.ncol_tiles;
+    const uint32_t seg = static_cast<uint32_t>(item - row * rt.ncol_tiles);
+    const uint32_t k0 = seg * rt.K;
+    const uint32_t Kt = min(rt.K, rt.n_last - k0);
+    RowLite<(1 << (D - 1))> mm;
+    warp_row_meta<D>(g, row, mm);
+    if (!mm.all_fine) P.template row<1>(mm, k0, Kt, lane);
+    else if (D >= 4 && mm.nsub == 8) P.template row<(D >= 4 ? 8 : 2)>(mm, k0, Kt, lane);
+    else if (D >= 3 && mm.nsub == 4) P.template row<(D >= 3 ? 4 : 2)>(mm, k0, Kt, lane);
+    else P.template row<2>(mm, k0, Kt, lane);
+  }
+}
+
 }  // namespace dev
 }  // namespace mgrc_gpu
