@@ -698,6 +698,18 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_fine_warp(GridDev g, RowTili
     const uint32_t Kt = min(rt.K, rt.n_last - k0);
     RowLite<(1 << (D - 1))> mm;
     warp_row_meta<D>(g, row, mm);
+    {  // pull this warp's next row segment of u into L2 while this one is computed
+      const uint64_t nitem = item + nwarps;
+      if (nitem < nitems) {
+        const uint64_t nrow = nitem / rt.ncol_tiles;
+        const uint32_t nk0 = static_cast<uint32_t>(nitem - nrow * rt.ncol_tiles) * rt.K;
+        const uint32_t nK = min(rt.K, rt.n_last - nk0);
+        const char* base = reinterpret_cast<const char*>(u + nrow * rt.n_last + nk0);
+        const uint32_t bytes = nK * static_cast<uint32_t>(sizeof(T));
+        for (uint32_t off = lane * 128u; off < bytes; off += 32u * 128u)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+      }
+    }
     const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
     for (uint32_t ch = 0; ch < nchunks; ++ch) {
       const uint32_t kk = ch * kUnitCols + 2 * lane;
@@ -928,6 +940,18 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_recon_warp(GridDev g, RowTil
     const uint32_t Kt = min(rt.K, rt.n_last - k0);
     RowLite<(1 << (D - 1))> mm;
     warp_row_meta<D>(g, row, mm);
+    {  // pull this warp's next row segment of the codes into L2
+      const uint64_t nitem = item + nwarps;
+      if (nitem < nitems) {
+        const uint64_t nrow = nitem / rt.ncol_tiles;
+        const uint32_t nk0 = static_cast<uint32_t>(nitem - nrow * rt.ncol_tiles) * rt.K;
+        const uint32_t nK = min(rt.K, rt.n_last - nk0);
+        const char* base = reinterpret_cast<const char*>(zz + nrow * rt.n_last + nk0);
+        const uint32_t bytes = nK * static_cast<uint32_t>(sizeof(Z));
+        for (uint32_t off = lane * 128u; off < bytes; off += 32u * 128u)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+      }
+    }
     if (!mm.all_fine) P.template row<1>(mm, k0, Kt, lane);
     else if (D >= 4 && mm.nsub == 8) P.template row<(D >= 4 ? 8 : 2)>(mm, k0, Kt, lane);
     else if (D >= 3 && mm.nsub == 4) P.template row<(D >= 3 ? 4 : 2)>(mm, k0, Kt, lane);
