@@ -543,6 +543,17 @@ struct FinePairs {
   };
 };
 
+struct InvWarp {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, double* v) {
+      const RowTiling rt = row_tiling(g);
+      k_inv_warp<D><<<num_sms() * 3, kRowThreads, 0, s>>>(g, rt, v);
+      check_launch("k_inv_warp");
+    }
+  };
+};
+
 template <typename Z>
 struct ReconCoarse {
   template <int D>
@@ -788,8 +799,7 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
             const SrcResidual csrc{ec};
             for (int l = 1; l < dh.gc.L; ++l)
               by_dim<InvBox<SrcResidual>::template L>(grid.d, s, dh.gc, dh.cboxes[l], l, csrc, ec);
-            by_dim<InvFinest<SrcResidual, EpiStore64, true>::template L>(grid.d, s, dh.gc, csrc, ec,
-                                                                         EpiStore64{ec}, nullptr);
+            if (dh.gc.L >= 1) by_dim<InvWarp::L>(grid.d, s, dh.gc, ec);
           }
           prof.end();
         }
@@ -1035,7 +1045,7 @@ static void run_recon(Context& ctx, DevHier& dh, const Z* zz, const Widths& W, D
     const SrcResidual csrc{vc};
     for (int l = 1; l < dh.gc.L; ++l)
       by_dim<InvBox<SrcResidual>::template L>(g.d, s, dh.gc, dh.cboxes[l], l, csrc, vc);
-    by_dim<InvFinest<SrcResidual, EpiStore64, true>::template L>(g.d, s, dh.gc, csrc, vc, EpiStore64{vc}, nullptr);
+    if (dh.gc.L >= 1) by_dim<InvWarp::L>(g.d, s, dh.gc, vc);
   }
   const RowTiling rt = row_tiling(g);
   if (dtype == DType::f64)

@@ -959,5 +959,129 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_recon_warp(GridDev g, RowTil
   }
 }
 
+// ---------------------------------------------------------------------------
+// In-place finest level of an inverse (v(tag-L node) += I(v)(node)) on a grid
+// whose coarse values live in the same array — used on the compact coarse
+// box, whose level L−1 is 7/8 of it in 3-D (transform.cpp:155-159).  Same
+// column-pair structure as k_fine_warp: fresh indices at the finest level are
+// the odd positions (minus the last), bracketed by k−1 and k+1.
+template <int NS>
+struct RowU {
+  uint64_t uoff[NS];
+  double w[NS];
+  uint64_t own;
+  int nsub, all_fine;
+};
+
+template <int D>
+__device__ __forceinline__ void warp_row_meta_u(const GridDev& g, uint64_t row, RowU<(1 << (D - 1))>& m) {
+  const int lane = threadIdx.x & 31;
+  uint32_t o[4] = {0, 0, 0, 0};
+  uint64_t q = row;
+#pragma unroll
+  for (int a = D - 2; a >= 0; --a) {
+    const uint64_t qq = q / g.shape[a];
+    o[a] = static_cast<uint32_t>(q - qq * g.shape[a]);
+    q = qq;
+  }
+  uint32_t F = 0;
+  uint64_t own = 0;
+#pragma unroll
+  for (int a = 0; a < D - 1; ++a) {
+    if (__ldg(g.ax[a].lvl + o[a]) == g.L) F |= 1u << a;
+    own += static_cast<uint64_t>(o[a]) * g.stride[a];
+  }
+  m.own = own;
+  m.all_fine = F != 0;
+  m.nsub = 1 << __popc(F);
+  uint64_t uo = 0;
+  double w = 1.0;
+  if (lane < m.nsub) {
+    int b = 0;
+#pragma unroll
+    for (int a = 0; a < D - 1; ++a) {
+      if ((F >> a) & 1u) {
+        const bool right = (lane >> b) & 1;
+        ++b;
+        w = __dmul_rn(w, right ? __ldg(g.ax[a].wr + o[a]) : __ldg(g.ax[a].wl + o[a]));
+        uo += static_cast<uint64_t>(right ? __ldg(g.ax[a].right + o[a]) : __ldg(g.ax[a].left + o[a])) * g.stride[a];
+      } else {
+        uo += static_cast<uint64_t>(o[a]) * g.stride[a];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < (1 << (D - 1)); ++j) {
+    m.uoff[j] = __shfl_sync(0xffffffffu, uo, j);
+    m.w[j] = __shfl_sync(0xffffffffu, w, j);
+  }
+}
+
+template <int M, int NS>
+__device__ __forceinline__ void inv_unit(const GridDev& g, const RowU<NS>& m, double* v, uint32_t k0, uint32_t kk,
+                                         uint32_t Kt, int lane, int D) {
+  const bool va = kk < Kt, vb = kk + 1 < Kt;
+  const uint32_t k = k0 + min(kk, Kt - 1);
+  const AxisTab& ax = g.ax[D - 1];
+  const bool fb = vb && __ldg(ax.lvl + k + 1) == g.L;
+  const bool fine = M > 1;
+  const uint64_t n = m.own + k;
+  double U0[M], U2[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) U0[j] = v[(fine ? m.uoff[j] : m.own) + k];
+#pragma unroll
+  for (int j = 0; j < M; ++j) U2[j] = __shfl_down_sync(0xffffffffu, U0[j], 1);
+  if (fb && (lane == 31 || kk + 2 >= Kt)) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) U2[j] = v[(fine ? m.uoff[j] : m.own) + k + 2];
+  }
+  if (!va) return;
+  if (fine) {  // even column: tag L via the outer axes
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], U0[j]));
+    v[n] = __dadd_rn(v[n], acc);
+  }
+  if (!vb) return;
+  if (fb) {
+    const double wl = __ldg(ax.wl + k + 1), wr = __ldg(ax.wr + k + 1);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wl), U0[j]));
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wr), U2[j]));
+    v[n + 1] = __dadd_rn(v[n + 1], acc);
+  } else if (fine) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], v[m.uoff[j] + k + 1]));
+    v[n + 1] = __dadd_rn(v[n + 1], acc);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kRowThreads, 3) k_inv_warp(GridDev g, RowTiling rt, double* v) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nitems = rt.nrows * rt.ncol_tiles;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t item = gw; item < nitems; item += nwarps) {
+    const uint64_t row = item / rt.ncol_tiles;
+    const uint32_t seg = static_cast<uint32_t>(item - row * rt.ncol_tiles);
+    const uint32_t k0 = seg * rt.K;
+    const uint32_t Kt = min(rt.K, rt.n_last - k0);
+    RowU<(1 << (D - 1))> mm;
+    warp_row_meta_u<D>(g, row, mm);
+    const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
+    for (uint32_t ch = 0; ch < nchunks; ++ch) {
+      const uint32_t kk = ch * kUnitCols + 2 * lane;
+      if (!mm.all_fine) inv_unit<1>(g, mm, v, k0, kk, Kt, lane, D);
+      else if (D >= 4 && mm.nsub == 8) inv_unit<(D >= 4 ? 8 : 2)>(g, mm, v, k0, kk, Kt, lane, D);
+      else if (D >= 3 && mm.nsub == 4) inv_unit<(D >= 3 ? 4 : 2)>(g, mm, v, k0, kk, Kt, lane, D);
+      else inv_unit<2>(g, mm, v, k0, kk, Kt, lane, D);
+    }
+  }
+}
+
 }  // namespace dev
 }  // namespace mgrc_gpu
