@@ -514,6 +514,21 @@ struct CoarseQuant {
   };
 };
 
+template <typename T, typename Z>
+struct CoarseQuantRows {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const GridDev& gc, const BoxDev& box2, const Widths& W,
+                    double inv, const T* u, double* ec, Z* zc, QuantFlags* fl) {
+      const RowTiling rt = row_tiling(gc);
+      k_cq_warp<D, T, Z><<<num_sms() * 3, kRowThreads, 0, s>>>(g, gc, rt, W, inv, u, ec, zc, fl);
+      check_launch("k_cq_warp");
+      k_cq_box<D, T, Z><<<grid_blocks(box2.count, 256), 256, 0, s>>>(g, box2, W, u, ec, zc, fl);
+      check_launch("k_cq_box");
+    }
+  };
+};
+
 template <typename T, typename Z, class Chk, bool LW>
 struct FineRows {
   template <int D>
@@ -794,7 +809,11 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
         // (a) r and codes of the coarse box; (b) its inverse (container.cpp:93-113)
         if (L >= 1) {
           prof.begin("coarse_check", static_cast<double>(g.Nc) * (sizeof(T) + 8 + zb));
-          by_dim<CoarseQuant<T, Z>::template L>(grid.d, s, g, W, u, ec, zc, &sd->qflags);
+          if (L >= 2)
+            by_dim<CoarseQuantRows<T, Z>::template L>(grid.d, s, g, dh.gc, dh.boxes[L - 2], W, 1.0 / widths[L - 1], u,
+                                                      ec, zc, &sd->qflags);
+          else
+            by_dim<CoarseQuant<T, Z>::template L>(grid.d, s, g, W, u, ec, zc, &sd->qflags);
           if (!level_weighted) {
             const SrcResidual csrc{ec};
             for (int l = 1; l < dh.gc.L; ++l)

@@ -1083,5 +1083,202 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_inv_warp(GridDev g, RowTilin
   }
 }
 
+// ---------------------------------------------------------------------------
+// Compress, coarse box: r and codes of its finest level (tag L−1, 7/8 of the
+// box in 3-D) in column-pair form over the compact grid gc, reading u at the
+// corresponding finest-grid positions (cset); the remaining nodes (tag ≤ L−2)
+// by the generic gather over the level-(L−2) box (k_cq_box).
+template <int NS>
+struct RowCQ {
+  uint64_t uoff[NS];  // finest-grid offsets of the corner rows
+  double w[NS];
+  uint64_t own_c, own_f;
+  int nsub, all_fine;
+};
+
+template <int D>
+__device__ __forceinline__ void warp_row_meta_cq(const GridDev& g, const GridDev& gc, uint64_t row,
+                                                 RowCQ<(1 << (D - 1))>& m) {
+  const int lane = threadIdx.x & 31;
+  uint32_t o[4] = {0, 0, 0, 0};
+  uint64_t q = row;
+#pragma unroll
+  for (int a = D - 2; a >= 0; --a) {
+    const uint64_t qq = q / gc.shape[a];
+    o[a] = static_cast<uint32_t>(q - qq * gc.shape[a]);
+    q = qq;
+  }
+  uint32_t F = 0;
+  uint64_t own_c = 0, own_f = 0;
+#pragma unroll
+  for (int a = 0; a < D - 1; ++a) {
+    if (__ldg(gc.ax[a].lvl + o[a]) == gc.L) F |= 1u << a;
+    own_c += static_cast<uint64_t>(o[a]) * gc.stride[a];
+    own_f += static_cast<uint64_t>(__ldg(g.ax[a].cset + o[a])) * g.stride[a];
+  }
+  m.own_c = own_c;
+  m.own_f = own_f;
+  m.all_fine = F != 0;
+  m.nsub = 1 << __popc(F);
+  uint64_t uo = 0;
+  double w = 1.0;
+  if (lane < m.nsub) {
+    int b = 0;
+#pragma unroll
+    for (int a = 0; a < D - 1; ++a) {
+      uint32_t oc = o[a];
+      if ((F >> a) & 1u) {
+        const bool right = (lane >> b) & 1;
+        ++b;
+        w = __dmul_rn(w, right ? __ldg(gc.ax[a].wr + o[a]) : __ldg(gc.ax[a].wl + o[a]));
+        oc = right ? __ldg(gc.ax[a].right + o[a]) : __ldg(gc.ax[a].left + o[a]);
+      }
+      uo += static_cast<uint64_t>(__ldg(g.ax[a].cset + oc)) * g.stride[a];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < (1 << (D - 1)); ++j) {
+    m.uoff[j] = __shfl_sync(0xffffffffu, uo, j);
+    m.w[j] = __shfl_sync(0xffffffffu, w, j);
+  }
+}
+
+template <int M, int NS, typename T, typename Z>
+__device__ __forceinline__ void cq_unit(const GridDev& g, const GridDev& gc, const RowCQ<NS>& m, const T* __restrict__ u,
+                                        double* __restrict__ ec, Z* __restrict__ zc, double delta, double inv,
+                                        uint32_t k0, uint32_t kk, uint32_t Kt, int lane, int D,
+                                        unsigned long long& ovf, unsigned& wide) {
+  const bool va = kk < Kt, vb = kk + 1 < Kt;
+  const uint32_t k = k0 + min(kk, Kt - 1);
+  const AxisTab& axc = gc.ax[D - 1];
+  const uint32_t* cs = g.ax[D - 1].cset;
+  const bool fb = vb && __ldg(axc.lvl + k + 1) == gc.L;
+  const bool fine = M > 1;
+  const uint32_t ck = __ldg(cs + k);
+  double U0[M], U2[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) U0[j] = static_cast<double>(__ldg(u + (fine ? m.uoff[j] : m.own_f) + ck));
+#pragma unroll
+  for (int j = 0; j < M; ++j) U2[j] = __shfl_down_sync(0xffffffffu, U0[j], 1);
+  if (fb && (lane == 31 || kk + 2 >= Kt)) {
+    const uint32_t ck2 = __ldg(cs + k + 2);
+#pragma unroll
+    for (int j = 0; j < M; ++j) U2[j] = static_cast<double>(__ldg(u + (fine ? m.uoff[j] : m.own_f) + ck2));
+  }
+  if (!va) return;
+  auto quant = [&](double c, uint64_t nc) {
+    long long qv;
+    double r;
+    uint64_t z = 0;
+    if (quantize_fast(c, delta, inv, qv, r)) {
+      z = zigzag(qv);
+      if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
+    } else {
+      ++ovf;
+      r = 0.0;
+    }
+    ec[nc] = r;
+    zc[nc] = static_cast<Z>(z);
+  };
+  if (fine) {  // even column, tag L−1 through the outer axes
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], U0[j]));
+    quant(__dsub_rn(static_cast<double>(__ldg(u + m.own_f + ck)), acc), m.own_c + k);
+  }
+  if (!vb) return;
+  const uint32_t ck1 = __ldg(cs + k + 1);
+  if (fb) {
+    const double wl = __ldg(axc.wl + k + 1), wr = __ldg(axc.wr + k + 1);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wl), U0[j]));
+#pragma unroll
+    for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wr), U2[j]));
+    quant(__dsub_rn(static_cast<double>(__ldg(u + m.own_f + ck1)), acc), m.own_c + k + 1);
+  } else if (fine) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+      acc = __dadd_rn(acc, __dmul_rn(m.w[j], static_cast<double>(__ldg(u + m.uoff[j] + ck1))));
+    quant(__dsub_rn(static_cast<double>(__ldg(u + m.own_f + ck1)), acc), m.own_c + k + 1);
+  }
+}
+
+template <int D, typename T, typename Z>
+__global__ void __launch_bounds__(kRowThreads, 3) k_cq_warp(GridDev g, GridDev gc, RowTiling rt, Widths W, double inv,
+                                                           const T* __restrict__ u, double* __restrict__ ec,
+                                                           Z* __restrict__ zc, QuantFlags* flags) {
+  const int lane = threadIdx.x & 31;
+  const double delta = W.w[gc.L];
+  unsigned long long ovf = 0;
+  unsigned wide = 0;
+  const uint64_t nitems = rt.nrows * rt.ncol_tiles;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t item = gw; item < nitems; item += nwarps) {
+    const uint64_t row = item / rt.ncol_tiles;
+    const uint32_t seg = static_cast<uint32_t>(item - row * rt.ncol_tiles);
+    const uint32_t k0 = seg * rt.K;
+    const uint32_t Kt = min(rt.K, rt.n_last - k0);
+    RowCQ<(1 << (D - 1))> mm;
+    warp_row_meta_cq<D>(g, gc, row, mm);
+    const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
+    for (uint32_t ch = 0; ch < nchunks; ++ch) {
+      const uint32_t kk = ch * kUnitCols + 2 * lane;
+      if (!mm.all_fine) cq_unit<1>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide);
+      else if (D >= 4 && mm.nsub == 8)
+        cq_unit<(D >= 4 ? 8 : 2)>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide);
+      else if (D >= 3 && mm.nsub == 4)
+        cq_unit<(D >= 3 ? 4 : 2)>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide);
+      else cq_unit<2>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide);
+    }
+  }
+  if (ovf) atomicAdd(&flags->overflow, ovf);
+  if (wide) atomicOr(&flags->wide, 1u);
+}
+
+// Nodes of tag ≤ L−2: generic gather over the level-(L−2) box (finest
+// coordinates), results stored at their compact positions.
+template <int D, typename T, typename Z>
+__global__ void __launch_bounds__(256) k_cq_box(GridDev g, BoxDev box, Widths W, const T* __restrict__ u,
+                                                double* __restrict__ ec, Z* __restrict__ zc, QuantFlags* flags) {
+  auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
+  unsigned long long ovf = 0;
+  unsigned wide = 0;
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < box.count; p += step) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    uint64_t q = p, n = 0, nc = 0;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      const uint64_t qq = q / box.n[a];
+      i[a] = __ldg(box.set[a] + (q - qq * box.n[a]));
+      n += static_cast<uint64_t>(i[a]) * g.stride[a];
+      nc += static_cast<uint64_t>(__ldg(g.ax[a].cpos + i[a])) * g.cstride[a];
+      q = qq;
+    }
+    const int tag = node_tag<D>(g, i);
+    double c = static_cast<double>(u[n]);
+    if (tag > 0) c = __dsub_rn(c, interp<D>(g, i, tag, ld));
+    const double delta = W.w[tag];
+    const double scaled = __ddiv_rn(c, delta);
+    double r = 0.0;
+    uint64_t z = 0;
+    if (fabs(scaled) < 9223372036854775808.0) {
+      const long long qv = __double2ll_rn(scaled);
+      r = __dsub_rn(c, __dmul_rn(__ll2double_rn(qv), delta));
+      z = zigzag(qv);
+      if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
+    } else {
+      ++ovf;
+    }
+    ec[nc] = r;
+    zc[nc] = static_cast<Z>(z);
+  }
+  if (ovf) atomicAdd(&flags->overflow, ovf);
+  if (wide) atomicOr(&flags->wide, 1u);
+}
+
 }  // namespace dev
 }  // namespace mgrc_gpu
