@@ -815,150 +815,6 @@ __device__ __forceinline__ uint32_t varint_bits(uint64_t z, const uint8_t* len) 
   }
 }
 
-template <typename Z>
-__global__ void __launch_bounds__(kPackThreads) k_tile_bits(const Z* __restrict__ zz, uint64_t n,
-                                                            const uint8_t* __restrict__ len_g,
-                                                            unsigned long long* __restrict__ tile_bits) {
-  __shared__ uint8_t len[256];
-  __shared__ unsigned long long wsum[kPackThreads / 32];
-  len[threadIdx.x] = len_g[threadIdx.x];
-  __syncthreads();
-  const uint64_t base = blockIdx.x * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
-  unsigned long long s = 0;
-#pragma unroll
-  for (int k = 0; k < kPackPerThread; ++k)
-    if (base + k < n) s += varint_bits(static_cast<uint64_t>(zz[base + k]), len);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int w = 0; w < kPackThreads / 32; ++w) t += wsum[w];
-    tile_bits[blockIdx.x] = t;
-  }
-}
-
-// Exclusive scan of u64 in one CTA (used on per-tile / per-block counts,
-// which are ≤ ~10^6 entries).  out[n] receives the total.
-__global__ void __launch_bounds__(1024) k_scan_u64_single(const unsigned long long* __restrict__ in,
-                                                          unsigned long long* __restrict__ out, uint64_t n) {
-  __shared__ unsigned long long wsum[32];
-  __shared__ unsigned long long carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint64_t base = 0; base < n; base += blockDim.x) {
-    const uint64_t i = base + threadIdx.x;
-    const unsigned long long x = i < n ? in[i] : 0;
-    unsigned long long incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      unsigned long long w = lane < (blockDim.x >> 5) ? wsum[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      wsum[lane] = w;
-    }
-    __syncthreads();
-    const unsigned long long before = carry + (warp ? wsum[warp - 1] : 0) + incl - x;
-    if (i < n) out[i] = before;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = before + x;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[n] = carry;
-}
-
-// Packs one tile of values: per-value bit counts → block exclusive scan →
-// codes OR-ed into a shared word buffer aligned to the output's 32-bit word
-// grid → interior words stored, the two edge words (shared with the
-// neighbouring tiles) OR-ed atomically.  Output words hold the stream
-// MSB-first in memory byte order (byte-swapped big-endian words).
-template <typename Z>
-__global__ void __launch_bounds__(kPackThreads) k_pack(const Z* __restrict__ zz, uint64_t n,
-                                                       const uint32_t* __restrict__ code_g,
-                                                       const uint8_t* __restrict__ len_g,
-                                                       const unsigned long long* __restrict__ tile_off,
-                                                       uint32_t* __restrict__ out) {
-  extern __shared__ uint32_t words[];
-  __shared__ uint32_t code[256];
-  __shared__ uint8_t len[256];
-  __shared__ unsigned long long wsum[kPackThreads / 32];
-  code[threadIdx.x] = code_g[threadIdx.x];
-  len[threadIdx.x] = len_g[threadIdx.x];
-  __syncthreads();
-  const uint64_t base = blockIdx.x * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
-  uint64_t z[kPackPerThread];
-  uint32_t bits[kPackPerThread];
-  unsigned long long mine = 0;
-#pragma unroll
-  for (int k = 0; k < kPackPerThread; ++k) {
-    z[k] = base + k < n ? static_cast<uint64_t>(zz[base + k]) : 0;
-    bits[k] = base + k < n ? varint_bits(z[k], len) : 0;
-    mine += bits[k];
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int w = 1; w < kPackThreads / 32; ++w) wsum[w] += wsum[w - 1];
-  __syncthreads();
-  const unsigned long long tile_start = tile_off[blockIdx.x];
-  const unsigned long long tile_total = wsum[kPackThreads / 32 - 1];
-  const uint32_t shift0 = static_cast<uint32_t>(tile_start & 31);
-  const uint64_t nwords = (shift0 + tile_total + 31) >> 5;
-  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0;
-  __syncthreads();
-  // local bit position (relative to the first output word of the tile)
-  uint64_t p = shift0 + (warp ? wsum[warp - 1] : 0) + incl - mine;
-#pragma unroll
-  for (int k = 0; k < kPackPerThread; ++k) {
-    if (base + k >= n) break;
-    uint64_t v = z[k];
-    for (;;) {
-      const uint32_t sym = v >= 0x80 ? static_cast<uint32_t>((v & 0x7F) | 0x80) : static_cast<uint32_t>(v);
-      const uint32_t l = len[sym], c = code[sym];
-      const uint32_t w = static_cast<uint32_t>(p >> 5), o = static_cast<uint32_t>(p & 31);
-      if (o + l <= 32) {
-        atomicOr(&words[w], c << (32 - o - l));
-      } else {
-        const uint32_t spill = o + l - 32;
-        atomicOr(&words[w], c >> spill);
-        atomicOr(&words[w + 1], c << (32 - spill));
-      }
-      p += l;
-      if (v < 0x80) break;
-      v >>= 7;
-    }
-  }
-  __syncthreads();
-  if (tile_total == 0) return;
-  const uint64_t gw0 = tile_start >> 5;
-  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) {
-    const uint32_t val = bswap32(words[w]);
-    if (w == 0 || w == nwords - 1) {
-      if (val) atomicOr(out + gw0 + w, val);
-    } else {
-      out[gw0 + w] = val;
-    }
-  }
-}
-
 // Single-pass Huffman / varint packer: per-value bit counts → block scan →
 // look-back for the tile's start bit → codes OR-ed into a shared-memory word
 // image → interior words stored directly; the first and last word of the
@@ -1015,26 +871,40 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ 
   const uint64_t nwords = (shift0 + tile_total + 31) >> 5;
   for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0;
   __syncthreads();
-  uint64_t p = shift0 + (warp ? wsum[warp - 1] : 0) + incl - mine;
+  // Each thread's codes form one contiguous bit span: assemble it in a 64-bit
+  // register accumulator and store whole words; only the span's first and
+  // last words can be shared with a neighbouring thread (atomicOr).
+  const uint64_t p0 = shift0 + (warp ? wsum[warp - 1] : 0) + incl - mine;
+  const uint64_t p1 = p0 + mine;  // span [p0, p1)
+  if (mine) {
+    const uint32_t w_first = static_cast<uint32_t>(p0 >> 5), w_last = static_cast<uint32_t>((p1 - 1) >> 5);
+    uint64_t acc = 0;                                  // bits left-aligned
+    uint32_t nacc = static_cast<uint32_t>(p0 & 31);    // the first word starts mid-word
+    uint32_t wi = w_first;
+    auto put_word = [&](uint32_t word) {
+      if (wi == w_first || wi == w_last) atomicOr(&words[wi], word);
+      else words[wi] = word;
+      ++wi;
+    };
 #pragma unroll
-  for (int k = 0; k < kPackPerThread; ++k) {
-    if (base + k >= n) break;
-    uint64_t v = z[k];
-    for (;;) {
-      const uint32_t sym = v >= 0x80 ? static_cast<uint32_t>((v & 0x7F) | 0x80) : static_cast<uint32_t>(v);
-      const uint32_t l = len[sym], c = code[sym];
-      const uint32_t w = static_cast<uint32_t>(p >> 5), o = static_cast<uint32_t>(p & 31);
-      if (o + l <= 32) {
-        atomicOr(&words[w], c << (32 - o - l));
-      } else {
-        const uint32_t spill = o + l - 32;
-        atomicOr(&words[w], c >> spill);
-        atomicOr(&words[w + 1], c << (32 - spill));
+    for (int k = 0; k < kPackPerThread; ++k) {
+      if (base + k >= n) break;
+      uint64_t v = z[k];
+      for (;;) {
+        const uint32_t sym = v >= 0x80 ? static_cast<uint32_t>((v & 0x7F) | 0x80) : static_cast<uint32_t>(v);
+        const uint32_t l = len[sym], c = code[sym];
+        acc |= static_cast<uint64_t>(c) << (64 - nacc - l);
+        nacc += l;
+        if (nacc >= 32) {
+          put_word(static_cast<uint32_t>(acc >> 32));
+          acc <<= 32;
+          nacc -= 32;
+        }
+        if (v < 0x80) break;
+        v >>= 7;
       }
-      p += l;
-      if (v < 0x80) break;
-      v >>= 7;
     }
+    if (nacc) put_word(static_cast<uint32_t>(acc >> 32));
   }
   __syncthreads();
   const uint64_t gw0 = tile_start_bit >> 5;

@@ -5,7 +5,7 @@
 //    K2  k_forward_quant      forward transform + quantise + varint histogram
 //    K3  k_inverse_box/finest a-posteriori error of the residuals (shrink loop)
 //    K4  (host)               Huffman lengths + canonical codes (256 symbols)
-//    K5  k_tile_bits/k_pack   bit-offset scan + MSB-first packing
+//    K5  k_pack_lb/k_pack_edges  single-pass look-back bit packing (MSB-first)
 //    K5b k_crc_blocks/fold    CRC-32 of the payload
 //  decompress (container.cpp:210-261)
 //    CRC → k_huff_sync/fix (self-synchronising decode) → k_huff_emit
