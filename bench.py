@@ -54,6 +54,11 @@ WORKLOADS = {
     "cfg4_1025cubed_f64_inf_rel1e-5": ((1025, 1025, 1025), "f64", 1e-5, 0, 0.0, 1),
 }
 DEFAULT_WORKLOAD = "cfg2_513cubed_f32_inf_rel1e-4"
+# configs[4]: 2049^3 f32, INF REL 1e-4, chunked into 8 slabs [257, 256x7] (chunk_mem = 257*2049^2*4) that
+# are split across the ranks (strong scaling: total work fixed) — the multi-GPU sweep of BASELINE.json.
+CHUNKED_WORKLOAD = "cfg5_2049cubed_f32_chunked_rel1e-4"
+WORKLOADS[CHUNKED_WORKLOAD] = ((2049, 2049, 2049), "f32", 1e-4, 0, 0.0, 1)
+CHUNK_MEM = 257 * 2049 * 2049 * 4
 
 
 def peaks():
@@ -88,6 +93,26 @@ def multisine_torch(shape, device):
     u = u + 0.25 * torch.sin(two_pi * (7.0 * t0 + 5.0 * t3))
     u = u + 1.5 * t0
     return u.expand(*shape).contiguous()
+
+
+# dominant phase -> its main kernel (for the ncu DRAM traffic lookup)
+PHASE_KERNEL = {"fine": "k_fine_warp", "huff_sync": "k_huff_sync_s", "huff_emit": "k_huff_emit_s",
+                "recon": "k_recon_warp", "pack": "k_pack_lb", "coarse_check": "k_cq_warp", "crc": "k_crc_blocks",
+                "stats": "k_stats"}
+
+
+def ncu_traffic(phase):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the phase's kernel, from the committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json, scripts/ncu_traffic.py); None if absent."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    k = PHASE_KERNEL.get(phase)
+    for name, v in d.get("kernels", {}).items():
+        if k and k in name:
+            return v["dram_bytes"]
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -239,6 +264,151 @@ def run_reference_arm(args, workload):
     return 0
 
 
+def multisine_rows(shape, r0, r1, device):
+    """Rows [r0, r1) (axis 0) of multisine(shape), evaluated exactly as multisine_torch."""
+    import torch
+
+    d = len(shape)
+    t = [torch.linspace(0.0, 1.0, n, dtype=torch.float64, device=device) for n in shape]
+    t[0] = t[0][r0:r1]
+
+    def ax(a):
+        if a >= d:
+            return torch.zeros((1,) * d, dtype=torch.float64, device=device)
+        return t[a].reshape([-1 if k == a else 1 for k in range(d)])
+
+    t0, t1, t2, t3 = ax(0), ax(1), ax(2), ax(3)
+    two_pi = 2.0 * np.pi
+    u = torch.sin(two_pi * (t0 + 0.7 * t1 + 0.4 * t2))
+    u = u + 0.5 * torch.sin(two_pi * (3.0 * t0 + 2.2 * t1))
+    u = u + 0.25 * torch.sin(two_pi * (7.0 * t0 + 5.0 * t3))
+    u = u + 1.5 * t0
+    return u.expand(r1 - r0, *shape[1:])
+
+
+def run_chunked(args, world, rank, local, coll_dev):
+    """configs[4]: the chunked driver (paper_2401_05994_b200/sharded.py, tools/mgrc.cpp:363-542) with the
+    slabs split across ranks; device-resident containers; NCCL all-gathers of [min,max] and of the sizes."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_05994_b200 as mg
+    from paper_2401_05994_b200 import sharded
+
+    mg.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    mg.set_stream(stream.cuda_stream)
+    shape, dts, tol, norm, s, mode = WORKLOADS[CHUNKED_WORKLOAD]
+    plan = mg.plan_chunks(shape, mg.DType.f32, CHUNK_MEM)
+    nb = plan.shape[0]
+    mine = sharded.blocks_of(rank, nb, world)
+    r0, r1 = int(plan[mine[0]][0][0]), int(plan[mine[-1]][0][1])
+    u = torch.empty((r1 - r0,) + tuple(shape[1:]), dtype=torch.float32, device="cuda")
+    for a in range(r0, r1, 64):  # generate in row chunks (bounded f64 temporaries)
+        b = min(r1, a + 64)
+        u[a - r0:b - r0] = multisine_rows(shape, a, b, "cuda").to(torch.float32)
+    slab_bytes = {b: int(np.prod([int(r[1] - r[0]) for r in plan[b]])) * 4 for b in mine}
+    dsts = {b: torch.empty(slab_bytes[b] * 2 + (1 << 20), dtype=torch.uint8, device="cuda") for b in mine}
+    outs = {b: torch.empty(slab_bytes[b] // 4, dtype=torch.float32, device="cuda") for b in mine}
+    coords = [np.arange(n, dtype=np.float64) for n in shape]
+    sizes_local = {}
+
+    def allgather_vec(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=coll_dev)
+        if world == 1:
+            return [vals]
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return [p.cpu().tolist() for p in parts]
+
+    def view(b):
+        a0, a1 = int(plan[b][0][0]), int(plan[b][0][1])
+        return u[a0 - r0:a1 - r0]
+
+    def compress_step():
+        mn, mx = np.inf, -np.inf
+        for b in mine:  # REL normalisation (mgrc.cpp:405-418): per-rank stats, one tiny all-gather
+            a, c, _ = mg.field_stats(view(b))
+            mn, mx = min(mn, a), max(mx, c)
+        st = allgather_vec([mn, mx])
+        tau = tol * (max(r[1] for r in st) - min(r[0] for r in st))
+        spec = mg.ErrorSpec(tau, mg.Norm.inf, 0.0, mg.Mode.abs)
+        for b in mine:
+            bshape = tuple(int(r[1] - r[0]) for r in plan[b])
+            grid = mg.make_grid(bshape, sharded.block_coords(plan[b].tolist(), coords))
+            sizes_local[b] = mg.compress_to(view(b), dsts[b], grid, spec, mg.Codec.huffman)
+        vec = [0.0] * nb
+        for b in mine:
+            vec[b] = float(sizes_local[b])
+        allv = allgather_vec(vec)
+        return [int(sum(r[b] for r in allv)) for b in range(nb)]
+
+    def decompress_step():
+        for b in mine:
+            mg.decompress_into(dsts[b][:sizes_local[b]], outs[b])
+
+    for _ in range(args.warmup):
+        sizes = compress_step()
+        decompress_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = mg.launch_count()
+    tc = td = 0.0
+    for _ in range(args.steps):
+        e[0].record(stream)
+        sizes = compress_step()
+        e[1].record(stream)
+        decompress_step()
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        tc += e[0].elapsed_time(e[1])
+        td += e[1].elapsed_time(e[2])
+    if world > 1:
+        dist.barrier()
+    launches = mg.launch_count() - l0
+    clk = clocks.stop()
+    t = torch.tensor([tc, td], dtype=torch.float64, device=coll_dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tc, td = (float(x) for x in t.tolist())
+    total_bytes = int(np.prod(shape)) * 4
+    stream_len = len(sharded.frame_header(sizes)) + sum(sizes)
+    ms_step = (tc + td) / args.steps
+    # bound check on this rank's slabs (max over ranks)
+    err = 0.0
+    for b in mine:  # in row chunks (bounded temporaries)
+        ob, ub = outs[b].view(view(b).shape), view(b)
+        for a in range(0, ub.shape[0], 16):
+            err = max(err, float((ob[a:a + 16].double() - ub[a:a + 16].double()).abs().max()))
+    errs = allgather_vec([err])
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": 2.0 * total_bytes / (ms_step * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (f32 data widened to f64 in registers)",
+            "data": "synthetic multisine field (test_support.hpp:43-62), generated on the GPUs",
+            "config": {"workload": CHUNKED_WORKLOAD, "shape": list(shape), "elem": "f32", "tol": tol, "norm": "inf",
+                       "mode": "rel", "codec": "huffman", "chunk_mem": CHUNK_MEM, "slabs": nb,
+                       "slab_rows": [int(r[0][1] - r[0][0]) for r in plan], "parallelism": f"slabs over {world} ranks",
+                       "l2": "inputs/outputs exceed the 126 MB L2; no flush"},
+            "compress_gbs": total_bytes * args.steps / (tc * 1e-3) / 1e9,
+            "decompress_gbs": total_bytes * args.steps / (td * 1e-3) / 1e9,
+            "ratio": total_bytes / stream_len, "stream_bytes": stream_len,
+            "max_err": max(r[0] for r in errs), "gpu_launches": int(launches), "clocks": clk,
+            "e2e": None, "cpu_baseline": None, "roofline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 
@@ -264,9 +434,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    shared_gpu = world > 1 and ndev < world  # test mode: several ranks on one device (gloo for the collective)
+    local = local % ndev
     torch.cuda.set_device(local)
+    coll_dev = "cpu" if shared_gpu else "cuda"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.workload == CHUNKED_WORKLOAD:
+        return run_chunked(args, world, rank, local, coll_dev)
 
     import paper_2401_05994_b200 as mg
 
@@ -292,7 +471,7 @@ def main():
     def gather_sizes(n):
         if world == 1:
             return [n]
-        t = torch.tensor([n], dtype=torch.int64, device="cuda")
+        t = torch.tensor([n], dtype=torch.int64, device=coll_dev)
         allt = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(allt, t)
         return [int(x.item()) for x in allt]
@@ -357,7 +536,7 @@ def main():
     tc = sum(ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps))
     td = sum(ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps))
     if world > 1:
-        t = torch.tensor([total_ms, tc, td], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms, tc, td], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, tc, td = (float(x) for x in t.tolist())
     ms_step = total_ms / args.steps
@@ -373,6 +552,7 @@ def main():
     dom_ms = phase_ms[dom] / phase_n[dom]
     dom_bytes = phase_bytes[dom] / phase_n[dom]
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(dom)
     step_alg = (2 * nbytes + 2 * clen)  # B_c + B_d
     phases = {k: {"ms": round(phase_ms[k] / args.steps, 4),
                   "gbs": round(phase_bytes[k] / args.steps / (phase_ms[k] / args.steps * 1e-3) / 1e9, 1)
@@ -402,7 +582,7 @@ def main():
         torch.cuda.synchronize()
         e_ms = h0.elapsed_time(h1)
         if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            t = torch.tensor([e_ms], dtype=torch.float64, device=coll_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": 2.0 * nbytes * world * args.steps / (e_ms * 1e-3) / 1e9, "unit": UNIT,
@@ -431,7 +611,7 @@ def main():
             "max_err": max_err, "tau": tau, "bound_met": max_err <= tau,
             "step_alg_roofline_frac": step_alg * world / (ms_step * 1e-3) / 1e9 / peak / world,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": dom_bytes,
+                         "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": dom_bytes,
                          "ms_per_launch": dom_ms, "peak_source": peak_src},
             "phases_ms_per_step": phases,
             "gpu_launches": int(launches),

@@ -20,6 +20,7 @@ namespace dev {
 constexpr int kWarmBits = 1024;  // warm-up decoded before each subsequence's nominal start
 constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never published)
 constexpr int kSyncReal = kDecThreads - kSyncWarm;
+constexpr int kSyncRounds = 1 << 20;  // in-CTA resynchronisation rounds (effectively until consistent)
 constexpr int kStageWords = kDecThreads * kSeqBits / 32;
 constexpr int kTailWords = 32;   // look-ahead past the last subsequence (open codewords / varints)
 constexpr int kStageTotal = kWarmBits / 32 + kStageWords + kTailWords + 4;
@@ -163,7 +164,9 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __r
   }
   sexit[threadIdx.x] = E;
   sstart[threadIdx.x] = F;
-  for (;;) {
+  // in-CTA re-decode rounds, capped: a chain still open after kSyncRounds is
+  // left inconsistent and resolved by the transfer-table windows (host loop)
+  for (int round = 0; round < kSyncRounds; ++round) {
     if (threadIdx.x == 0) nbad = 0;
     __syncthreads();
     if (valid && threadIdx.x > 0 && js > 0 && sexit[threadIdx.x - 1] != sstart[threadIdx.x])
@@ -376,6 +379,211 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_emit_s(const uint32_t* __r
   if ((k & (CH - 1)) != 0 && k > k_first) flush(k);
   if (err) atomicMax(&st->error, err);
   if (wide) atomicOr(&st->wide, 1u);
+}
+
+// ---------------------------------------------------------------------------
+// Long desynchronisation chains (periodic stretches of the stream can keep a
+// decoder out of phase for megabits, e.g. long runs of one multi-bit code):
+// instead of walking them serially, tabulate for every subsequence of a
+// window the decode from EVERY entry offset o < maxlen — exit offset into the
+// next subsequence, terminators, last-continues — and compose the tables with
+// a parallel scan from the window's known true entry.  The decode from o = 0
+// is recorded as boundary / terminator bitmaps; the other offsets are walked
+// until they land on a recorded boundary (then both coincide).
+constexpr int kTfOffs = 16;
+constexpr int kTfThreads = 64;
+constexpr int kTfStage = kTfThreads * kSeqBits / 32 + kTailWords + 4;
+constexpr int kTfMapStride = kSeqBits / 32 + 1;
+
+struct TfTab {
+  uint8_t ex[kTfOffs];    // exit - S_{j+1}
+  uint16_t nt[kTfOffs];   // varint terminators
+  uint32_t lc;            // bit o: last codeword continues a varint
+};
+
+__device__ __forceinline__ uint32_t tf_terms_before(const uint32_t* Mm, uint32_t rel) {
+  uint32_t c = 0;
+  const uint32_t wq = rel >> 5;
+  for (uint32_t w = 0; w < wq; ++w) c += __popc(Mm[w]);
+  return c + __popc(Mm[wq] & ((1u << (rel & 31)) - 1u));
+}
+
+constexpr uint64_t kTfWin = 512;  // subsequences per window
+constexpr int kTfCtasPerWin = static_cast<int>(kTfWin) / kTfThreads;
+
+// grid: (window, CTA within the window); window w covers [starts[w], starts[w] + kTfWin) ∩ [0, nseq)
+__global__ void __launch_bounds__(kTfThreads) k_tf_tables(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+                                                          const uint16_t* __restrict__ lut_g, int maxlen,
+                                                          const unsigned long long* __restrict__ starts,
+                                                          uint64_t nseq, TfTab* __restrict__ tabs_all) {
+  const uint64_t win = blockIdx.x / kTfCtasPerWin;
+  const uint64_t j_first = starts[win];
+  const uint64_t count = umin64(kTfWin, nseq - j_first);
+  TfTab* tabs = tabs_all + win * kTfWin;
+  extern __shared__ uint32_t dyn[];
+  uint32_t* sm = dyn;                                              // staged words
+  uint32_t* maps = sm + stage_idx(kTfStage) + 2;                   // B | M per thread
+  uint16_t* lut = reinterpret_cast<uint16_t*>(maps + 2 * kTfThreads * kTfMapStride);
+  const int lutn = 1 << maxlen;
+  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
+  const uint64_t j0 = j_first + static_cast<uint64_t>(blockIdx.x % kTfCtasPerWin) * kTfThreads;
+  if (j0 >= j_first + count) return;
+  const uint64_t base = j0 * kSeqBits;
+  stage_words(w, nw, base >> 5, sm, kTfStage);
+  __syncthreads();
+  const uint64_t j = j0 + threadIdx.x;
+  if (j >= j_first + count || j >= nseq) return;
+  const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
+  const uint32_t S = threadIdx.x * kSeqBits;
+  const uint32_t end = min(S + static_cast<uint32_t>(kSeqBits), tl);
+  const bool last_seq = j + 1 == nseq;
+  uint32_t* Bm = maps + threadIdx.x * kTfMapStride;
+  uint32_t* Mm = maps + (kTfThreads + threadIdx.x) * kTfMapStride;
+  for (int q = 0; q < kSeqBits / 32; ++q) Bm[q] = Mm[q] = 0u;
+  // o = 0: recorded decode
+  uint32_t p = S, last0 = 0;
+  {
+    BitReader br;
+    br.init(sm, p);
+    while (p < end) {
+      br.refill();
+      const uint32_t ent = lut[br.peek(maxlen)];
+      const uint32_t l = lut_len(ent);
+      if (p + l > tl) break;
+      const uint32_t rel = p - S;
+      Bm[rel >> 5] |= 1u << (rel & 31);
+      Mm[rel >> 5] |= lut_term(ent) << (rel & 31);
+      last0 = lut_term(ent) ^ 1u;
+      p += l;
+      br.consume(l);
+    }
+  }
+  const uint32_t e0 = p;
+  uint32_t n0 = 0;
+  for (int q = 0; q < kSeqBits / 32; ++q) n0 += __popc(Mm[q]);
+  TfTab t;
+  t.lc = 0;
+  for (int o = 0; o < kTfOffs; ++o) {
+    uint32_t eo = e0, no = n0, lco = last0;
+    if (o > 0 && o < maxlen) {
+      if (S + o >= end) {
+        eo = S + o;
+        no = 0;
+        lco = 0;
+      } else {
+        uint32_t q = S + o, walked = 0, lastw = 0;
+        bool merged = false, any = false;
+        BitReader bo;
+        bo.init(sm, q);
+        while (q < end) {
+          const uint32_t rel = q - S;
+          if ((Bm[rel >> 5] >> (rel & 31)) & 1u) {
+            merged = true;
+            break;
+          }
+          bo.refill();
+          const uint32_t ent = lut[bo.peek(maxlen)];
+          const uint32_t l = lut_len(ent);
+          if (q + l > tl) break;
+          walked += lut_term(ent);
+          lastw = lut_term(ent) ^ 1u;
+          any = true;
+          q += l;
+          bo.consume(l);
+        }
+        if (merged) {
+          no = walked + (n0 - tf_terms_before(Mm, q - S));
+        } else {
+          eo = q;
+          no = walked;
+          lco = any ? lastw : 0u;
+        }
+      }
+    }
+    t.ex[o] = last_seq ? 0 : static_cast<uint8_t>(min(eo - end, 255u));
+    t.nt[o] = static_cast<uint16_t>(no);
+    t.lc |= lco << o;
+  }
+  tabs[j - j_first] = t;
+}
+
+// One CTA: compose the window's tables from the true entry offset of its first
+// subsequence and rewrite every subsequence's (start, exit, nterm, last_cont).
+constexpr int kTfResolveThreads = 512;
+
+// grid: one CTA per window
+__global__ void __launch_bounds__(kTfResolveThreads) k_tf_resolve(const TfTab* __restrict__ tabs_all,
+                                                                  const unsigned long long* __restrict__ starts,
+                                                                  uint64_t nseq, uint64_t T, SeqInfo* seq) {
+  const uint64_t j_first = starts[blockIdx.x];
+  const uint64_t count = umin64(kTfWin, nseq - j_first);
+  const TfTab* tabs = tabs_all + static_cast<uint64_t>(blockIdx.x) * kTfWin;
+  __shared__ uint8_t maps[kTfResolveThreads][kTfOffs];
+  __shared__ uint8_t tmp[kTfResolveThreads][kTfOffs];
+  const int t = threadIdx.x;
+  const uint64_t per = (count + kTfResolveThreads - 1) / kTfResolveThreads;
+  const uint64_t a = umin64(count, t * per), b = umin64(count, a + per);
+  // 1. compose this thread's chunk: map o -> entry offset after the chunk
+  uint8_t f[kTfOffs];
+#pragma unroll
+  for (int o = 0; o < kTfOffs; ++o) f[o] = static_cast<uint8_t>(o);
+  for (uint64_t i = a; i < b; ++i) {
+    const TfTab& tb = tabs[i];
+#pragma unroll
+    for (int o = 0; o < kTfOffs; ++o) f[o] = tb.ex[f[o] & 15];
+  }
+#pragma unroll
+  for (int o = 0; o < kTfOffs; ++o) maps[t][o] = f[o];
+  __syncthreads();
+  // 2. inclusive scan of the chunk maps (Hillis–Steele; composition is associative)
+  for (int d = 1; d < kTfResolveThreads; d <<= 1) {
+    if (t >= d) {
+#pragma unroll
+      for (int o = 0; o < kTfOffs; ++o) tmp[t][o] = maps[t][maps[t - d][o] & 15];
+    } else {
+#pragma unroll
+      for (int o = 0; o < kTfOffs; ++o) tmp[t][o] = maps[t][o];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int o = 0; o < kTfOffs; ++o) maps[t][o] = tmp[t][o];
+    __syncthreads();
+  }
+  // 3. true entry offset of the window, then of this chunk; rewrite the entries
+  const SeqInfo first = seq[j_first];
+  const uint64_t S0 = j_first * kSeqBits;
+  const uint32_t e_in = static_cast<uint32_t>(
+      (j_first > 0 ? *reinterpret_cast<volatile unsigned long long*>(&seq[j_first - 1].exit) : 0ull) - S0);
+  (void)first;
+  uint32_t o = t == 0 ? e_in : maps[t - 1][e_in & 15];
+  uint32_t lc_prev = j_first > 0 ? seq[j_first - 1].last_cont : 0;
+  (void)lc_prev;
+  for (uint64_t i = a; i < b; ++i) {
+    const TfTab& tb = tabs[i];
+    const uint64_t j = j_first + i;
+    const uint64_t Sj = j * kSeqBits;
+    SeqInfo s;
+    s.start = Sj + o;
+    const uint32_t ex = tb.ex[o & 15];
+    s.exit = j + 1 == nseq ? T : (j + 1) * kSeqBits + ex;
+    s.nsym = 0;
+    s.nterm = tb.nt[o & 15];
+    s.last_cont = (tb.lc >> (o & 15)) & 1u;
+    s.pad = 0;
+    seq[j] = s;
+    o = ex;
+  }
+}
+
+// Positions j (1..nseq-1) with seq[j-1].exit != seq[j].start (first `cap`).
+__global__ void k_seq_mismatch(const SeqInfo* __restrict__ seq, uint64_t nseq, unsigned long long* list,
+                               unsigned int* nlist, unsigned int cap) {
+  const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x + 1;
+  if (j >= nseq) return;
+  if (seq[j - 1].exit != seq[j].start) {
+    const unsigned k = atomicAdd(nlist, 1u);
+    if (k < cap) list[k] = j;
+  }
 }
 
 }  // namespace dev

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -135,7 +137,7 @@ class Context {
   bool profiling = false;
   std::vector<PhaseTime> profile;
   // workspace
-  DevBuf in, zz, zc, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws;
+  DevBuf in, zz, zc, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws, tfst, tftab;
   DevBuf scratch_d;
   PinnedBuf scratch_h, partial_h;
   std::unique_ptr<DevHier> hier;
@@ -1030,6 +1032,9 @@ ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len) {
 static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords) * 4 + (sizeof(uint16_t) << maxlen); }
 
 static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
+static size_t tf_smem(int maxlen) {
+  return static_cast<size_t>(stage_idx(kTfStage) + 2 + 2 * kTfThreads * kTfMapStride) * 4 + (sizeof(uint16_t) << maxlen);
+}
 
 static void huff_smem_optin() {
   static thread_local bool done = false;
@@ -1038,6 +1043,8 @@ static void huff_smem_optin() {
   CK(cudaFuncSetAttribute(k_huff_sync_s, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(k_tf_tables, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(tf_smem(kMaxCodeLen))));
   CK(cudaFuncSetAttribute(k_huff_fix_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(fix_smem(kMaxCodeLen))));
   done = true;
@@ -1209,15 +1216,62 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         k_huff_sync_s<<<static_cast<unsigned>(nblk), kDecThreads, huff_smem(maxlen), s>>>(w, nw, T, lut, maxlen,
                                                                                          nseq, seq);
         check_launch("k_huff_sync_s");
-        for (int it = 0; nblk > 1; ++it) {
+        // CTA edges: short chains are re-walked serially (two rounds at most) ...
+        bool pending = false;
+        for (int it = 0; nblk > 1 && it < 2; ++it) {
           CK(cudaMemsetAsync(&sd->fix_changed, 0, 4, s));
           k_huff_fix_s<<<static_cast<unsigned>(nblk - 1), 32, fix_smem(maxlen), s>>>(w, nw, T, lut, maxlen, nseq, seq,
                                                                                   &sd->fix_changed);
           check_launch("k_huff_fix_s");
           CK(cudaMemcpyAsync(&sh->fix_changed, &sd->fix_changed, 4, cudaMemcpyDeviceToHost, s));
           CK(cudaStreamSynchronize(s));
-          if (!sh->fix_changed) break;
+          pending = sh->fix_changed != 0;
+          if (!pending) break;
         }
+        // ... long ones (periodic stretches that stay out of phase for megabits) are resolved a window
+        // at a time by transfer tables composed with a parallel scan.
+        int tf_windows = 0;
+        for (uint64_t guard = 0; pending; ++guard) {
+          if (guard > nseq / 512 + 16) raise(Errc::invalid_state, "internal: Huffman resynchronisation did not converge");
+          constexpr unsigned kCap = 4096;
+          auto* lst = ctx.lbws.get<unsigned long long>(kCap * 8 + 16);
+          auto* nl = reinterpret_cast<unsigned int*>(lst + kCap);
+          CK(cudaMemsetAsync(nl, 0, 4, s));
+          k_seq_mismatch<<<static_cast<unsigned>((nseq + 255) / 256), 256, 0, s>>>(seq, nseq, lst, nl, kCap);
+          check_launch("k_seq_mismatch");
+          unsigned int nmis = 0;
+          CK(cudaMemcpyAsync(&nmis, nl, 4, cudaMemcpyDeviceToHost, s));
+          CK(cudaStreamSynchronize(s));
+          if (nmis == 0) break;
+          std::vector<unsigned long long> js(std::min<unsigned>(nmis, kCap));
+          CK(cudaMemcpy(js.data(), lst, js.size() * 8, cudaMemcpyDeviceToHost));
+          std::sort(js.begin(), js.end());
+          if (const char* dbg = std::getenv("MGRC_DEBUG"); dbg && dbg[0] == '2' && guard < 40) {
+            std::fprintf(stderr, "[mgrc] iter %llu: %u mismatches, first:", static_cast<unsigned long long>(guard), nmis);
+            for (size_t q = 0; q < js.size() && q < 6; ++q) std::fprintf(stderr, " %llu", js[q]);
+            std::fprintf(stderr, "\n");
+          }
+          // non-overlapping windows from every mismatch, all resolved in one pair of launches; windows
+          // whose entry is not yet true get rewritten by a later round (the earliest one always is)
+          std::vector<unsigned long long> starts;
+          uint64_t covered = 0;
+          for (const unsigned long long j : js) {
+            if (j < covered) continue;
+            starts.push_back(j);
+            covered = j + kTfWin;
+          }
+          const uint64_t nwin = starts.size();
+          auto* st_d = ctx.tfst.get<unsigned long long>(nwin * 8);
+          CK(cudaMemcpyAsync(st_d, starts.data(), nwin * 8, cudaMemcpyHostToDevice, s));
+          auto* tabs = ctx.tftab.get<TfTab>(nwin * kTfWin * sizeof(TfTab));
+          k_tf_tables<<<static_cast<unsigned>(nwin * kTfCtasPerWin), kTfThreads, tf_smem(maxlen), s>>>(
+              w, nw, T, lut, maxlen, st_d, nseq, tabs);
+          check_launch("k_tf_tables");
+          k_tf_resolve<<<static_cast<unsigned>(nwin), kTfResolveThreads, 0, s>>>(tabs, st_d, nseq, T, seq);
+          check_launch("k_tf_resolve");
+          tf_windows += static_cast<int>(nwin);
+        }
+        if (std::getenv("MGRC_DEBUG")) std::fprintf(stderr, "[mgrc] huffman long-chain windows: %d\n", tf_windows);
         prof.end();
         auto* cnt = ctx.tiles.get<unsigned long long>(nseq * 8);
         auto* toff = ctx.scan.get<unsigned long long>((nseq + 1) * 8);
