@@ -472,16 +472,22 @@ struct PairCtx {
     }
     if (!vb) return;
     // column k+1
-    if (fb) {  // corner weights (w_j·w_l), (w_j·w_r) recomputed in place (register pressure)
+    if (fb) {
+      double wlj[M], wrj[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        wlj[j] = __dmul_rn(m.w[j], wl);
+        wrj[j] = __dmul_rn(m.w[j], wr);
+      }
       double acc = 0.0, eacc = 0.0;
 #pragma unroll
-      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wl), U0[j]));
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(wlj[j], U0[j]));
 #pragma unroll
-      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wr), U2[j]));
+      for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(wrj[j], U2[j]));
 #pragma unroll
-      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(__dmul_rn(m.w[j], wl), E0[j]));
+      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(wlj[j], E0[j]));
 #pragma unroll
-      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(__dmul_rn(m.w[j], wr), E2[j]));
+      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(wrj[j], E2[j]));
       double r;
       const uint64_t z = quant(__dsub_rn(sb, acc), r);
       emit(n + 1, z, __dadd_rn(r, eacc), sb);
