@@ -246,7 +246,7 @@ int mgrc_gpu_set_stream(void* stream) {
       context_set_stream(c, static_cast<cudaStream_t>(stream));
     } else {
       cudaStream_t s;
-      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) raise(Errc::cuda, "stream create");
+      if (cudaStreamCreateWithFlags(&s, cudaStreamDefault) != cudaSuccess) raise(Errc::cuda, "stream create");
       context_set_stream(c, s);
     }
   });

@@ -20,7 +20,7 @@ namespace dev {
 constexpr int kWarmBits = 1024;  // warm-up decoded before each subsequence's nominal start
 constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never published)
 constexpr int kSyncReal = kDecThreads - kSyncWarm;
-constexpr int kSyncRounds = 1 << 20;  // in-CTA resynchronisation rounds (effectively until consistent)
+constexpr int kSyncRounds = 1 << 20;  // in-CTA resynchronisation rounds (uncapped: capping + transfer tables measured slower)
 constexpr int kStageWords = kDecThreads * kSeqBits / 32;
 constexpr int kTailWords = 32;   // look-ahead past the last subsequence (open codewords / varints)
 constexpr int kStageTotal = kWarmBits / 32 + kStageWords + kTailWords + 4;
@@ -131,7 +131,8 @@ __device__ __forceinline__ uint32_t count_to(BitReader& br, const uint16_t* lut,
 // codeword boundary.
 __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                              const uint16_t* __restrict__ lut_g, int maxlen,
-                                                             uint64_t nseq, SeqInfo* __restrict__ seq) {
+                                                             uint64_t nseq, SeqInfo* __restrict__ seq,
+                                                             unsigned int* capped) {
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;
   uint16_t* lut = reinterpret_cast<uint16_t*>(dyn + kStageSmemWords);
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __r
   sstart[threadIdx.x] = F;
   // in-CTA re-decode rounds, capped: a chain still open after kSyncRounds is
   // left inconsistent and resolved by the transfer-table windows (host loop)
-  for (int round = 0; round < kSyncRounds; ++round) {
+  for (int round = 0;; ++round) {
     if (threadIdx.x == 0) nbad = 0;
     __syncthreads();
     if (valid && threadIdx.x > 0 && js > 0 && sexit[threadIdx.x - 1] != sstart[threadIdx.x])
@@ -174,6 +175,10 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __r
     __syncthreads();
     const int nb = nbad;
     if (nb == 0) break;
+    if (round == kSyncRounds) {  // leave the rest to the transfer-table windows
+      if (threadIdx.x == 0) atomicOr(capped, 1u);
+      break;
+    }
     int t = -1;
     uint32_t from = 0;
     if (threadIdx.x < nb) {
@@ -422,8 +427,8 @@ __global__ void __launch_bounds__(kTfThreads) k_tf_tables(const uint32_t* __rest
   TfTab* tabs = tabs_all + win * kTfWin;
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;                                              // staged words
-  uint32_t* maps = sm + stage_idx(kTfStage) + 2;                   // B | M per thread
-  uint16_t* lut = reinterpret_cast<uint16_t*>(maps + 2 * kTfThreads * kTfMapStride);
+  uint32_t* maps = sm + stage_idx(kTfStage) + 2;                   // B0 | M0 | B1 | M1 per thread
+  uint16_t* lut = reinterpret_cast<uint16_t*>(maps + 4 * kTfThreads * kTfMapStride);
   const int lutn = 1 << maxlen;
   for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
   const uint64_t j0 = j_first + static_cast<uint64_t>(blockIdx.x % kTfCtasPerWin) * kTfThreads;
@@ -437,12 +442,18 @@ __global__ void __launch_bounds__(kTfThreads) k_tf_tables(const uint32_t* __rest
   const uint32_t S = threadIdx.x * kSeqBits;
   const uint32_t end = min(S + static_cast<uint32_t>(kSeqBits), tl);
   const bool last_seq = j + 1 == nseq;
-  uint32_t* Bm = maps + threadIdx.x * kTfMapStride;
-  uint32_t* Mm = maps + (kTfThreads + threadIdx.x) * kTfMapStride;
-  for (int q = 0; q < kSeqBits / 32; ++q) Bm[q] = Mm[q] = 0u;
-  // o = 0: recorded decode
-  uint32_t p = S, last0 = 0;
-  {
+  // two recorded tracks: the decode from offset 0, and the first offset that does
+  // not merge into it (periodic stretches usually have exactly two phases)
+  uint32_t* B[2] = {maps + threadIdx.x * kTfMapStride, maps + (2 * kTfThreads + threadIdx.x) * kTfMapStride};
+  uint32_t* M[2] = {maps + (kTfThreads + threadIdx.x) * kTfMapStride,
+                    maps + (3 * kTfThreads + threadIdx.x) * kTfMapStride};
+  uint32_t tex[2] = {0, 0}, tn[2] = {0, 0}, tlc[2] = {0, 0};
+  int ntracks = 0;
+  auto record = [&](uint32_t from, int k) {  // full decode from `from`, recorded as track k
+    uint32_t* Bm = B[k];
+    uint32_t* Mm = M[k];
+    for (int q = 0; q < kSeqBits / 32; ++q) Bm[q] = Mm[q] = 0u;
+    uint32_t p = from, last = 0, n = 0;
     BitReader br;
     br.init(sm, p);
     while (p < end) {
@@ -453,18 +464,21 @@ __global__ void __launch_bounds__(kTfThreads) k_tf_tables(const uint32_t* __rest
       const uint32_t rel = p - S;
       Bm[rel >> 5] |= 1u << (rel & 31);
       Mm[rel >> 5] |= lut_term(ent) << (rel & 31);
-      last0 = lut_term(ent) ^ 1u;
+      n += lut_term(ent);
+      last = lut_term(ent) ^ 1u;
       p += l;
       br.consume(l);
     }
-  }
-  const uint32_t e0 = p;
-  uint32_t n0 = 0;
-  for (int q = 0; q < kSeqBits / 32; ++q) n0 += __popc(Mm[q]);
+    tex[k] = p;
+    tn[k] = n;
+    tlc[k] = p > from ? last : 0u;
+  };
+  record(S, 0);
+  ntracks = 1;
   TfTab t;
   t.lc = 0;
   for (int o = 0; o < kTfOffs; ++o) {
-    uint32_t eo = e0, no = n0, lco = last0;
+    uint32_t eo = tex[0], no = tn[0], lco = tlc[0];
     if (o > 0 && o < maxlen) {
       if (S + o >= end) {
         eo = S + o;
@@ -472,13 +486,18 @@ __global__ void __launch_bounds__(kTfThreads) k_tf_tables(const uint32_t* __rest
         lco = 0;
       } else {
         uint32_t q = S + o, walked = 0, lastw = 0;
-        bool merged = false, any = false;
+        int hit = -1;
+        bool any = false;
         BitReader bo;
         bo.init(sm, q);
         while (q < end) {
           const uint32_t rel = q - S;
-          if ((Bm[rel >> 5] >> (rel & 31)) & 1u) {
-            merged = true;
+          if ((B[0][rel >> 5] >> (rel & 31)) & 1u) {
+            hit = 0;
+            break;
+          }
+          if (ntracks > 1 && ((B[1][rel >> 5] >> (rel & 31)) & 1u)) {
+            hit = 1;
             break;
           }
           bo.refill();
@@ -491,12 +510,18 @@ __global__ void __launch_bounds__(kTfThreads) k_tf_tables(const uint32_t* __rest
           q += l;
           bo.consume(l);
         }
-        if (merged) {
-          no = walked + (n0 - tf_terms_before(Mm, q - S));
+        if (hit >= 0) {
+          eo = tex[hit];
+          no = walked + (tn[hit] - tf_terms_before(M[hit], q - S));
+          lco = tlc[hit];
         } else {
           eo = q;
           no = walked;
           lco = any ? lastw : 0u;
+          if (ntracks == 1) {  // keep this phase as the second recorded track
+            record(S + o, 1);
+            ntracks = 2;
+          }
         }
       }
     }

@@ -160,7 +160,9 @@ Context& context_for_current_device() {
   if (!c) {
     c = std::make_unique<Context>();
     c->device = dev;
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // a blocking stream: ordered after work the caller queued on the legacy default stream
+    // (e.g. the producer of a device input), so no caller-side synchronisation is needed
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamDefault));
     c->own_stream = true;
   }
   return *c;
@@ -1033,7 +1035,7 @@ static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords
 
 static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
 static size_t tf_smem(int maxlen) {
-  return static_cast<size_t>(stage_idx(kTfStage) + 2 + 2 * kTfThreads * kTfMapStride) * 4 + (sizeof(uint16_t) << maxlen);
+  return static_cast<size_t>(stage_idx(kTfStage) + 2 + 4 * kTfThreads * kTfMapStride) * 4 + (sizeof(uint16_t) << maxlen);
 }
 
 static void huff_smem_optin() {
@@ -1213,8 +1215,9 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         huff_smem_optin();
         prof.begin("huff_sync", static_cast<double>(body_len));
         const uint64_t nblk = (nseq + kSyncReal - 1) / kSyncReal;
+        CK(cudaMemsetAsync(&sd->raw_wide, 0, 4, s));  // reused as the "rounds capped" flag
         k_huff_sync_s<<<static_cast<unsigned>(nblk), kDecThreads, huff_smem(maxlen), s>>>(w, nw, T, lut, maxlen,
-                                                                                         nseq, seq);
+                                                                                         nseq, seq, &sd->raw_wide);
         check_launch("k_huff_sync_s");
         // CTA edges: short chains are re-walked serially (two rounds at most) ...
         bool pending = false;
@@ -1231,6 +1234,9 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         // ... long ones (periodic stretches that stay out of phase for megabits) are resolved a window
         // at a time by transfer tables composed with a parallel scan.
         int tf_windows = 0;
+        CK(cudaMemcpyAsync(&sh->raw_wide, &sd->raw_wide, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        pending = pending || sh->raw_wide != 0;  // some CTA left an in-CTA chain open
         for (uint64_t guard = 0; pending; ++guard) {
           if (guard > nseq / 512 + 16) raise(Errc::invalid_state, "internal: Huffman resynchronisation did not converge");
           constexpr unsigned kCap = 4096;
