@@ -828,31 +828,38 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ 
                                                           unsigned long long* __restrict__ tile_start,
                                                           uint32_t* __restrict__ edge_first,
                                                           uint32_t* __restrict__ edge_last,
-                                                          uint32_t* __restrict__ out) {
-  extern __shared__ uint32_t words[];
+                                                          uint32_t* __restrict__ out, uint32_t cap_words) {
+  extern __shared__ uint32_t words[];  // cap_words + 1: the tile's stream, packed from tile-relative bit 0
   __shared__ uint32_t code[256];
   __shared__ uint8_t len[256];
-  __shared__ unsigned long long wsum[kPackThreads / 32];
+  __shared__ uint32_t wsum[kPackThreads / 32];
   __shared__ unsigned long long s_prefix;
   __shared__ uint32_t s_tile;
   code[threadIdx.x] = code_g[threadIdx.x];
   len[threadIdx.x] = len_g[threadIdx.x];
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  for (uint32_t w = threadIdx.x; w <= cap_words; w += blockDim.x) words[w] = 0;
   __syncthreads();
   const uint64_t t = s_tile;
   const uint64_t base = t * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
   uint64_t z[kPackPerThread];
-  unsigned long long mine = 0;
+  if (sizeof(Z) == 4 && base + kPackPerThread <= n) {  // 2 x 16-byte loads
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(zz + base));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(zz + base) + 1);
+    z[0] = a.x, z[1] = a.y, z[2] = a.z, z[3] = a.w, z[4] = b.x, z[5] = b.y, z[6] = b.z, z[7] = b.w;
+  } else {
 #pragma unroll
-  for (int k = 0; k < kPackPerThread; ++k) {
-    z[k] = base + k < n ? static_cast<uint64_t>(zz[base + k]) : 0;
-    if (base + k < n) mine += varint_bits(z[k], len);
+    for (int k = 0; k < kPackPerThread; ++k) z[k] = base + k < n ? static_cast<uint64_t>(zz[base + k]) : 0;
   }
+  uint32_t mine = 0;  // ≤ 8 values × 150 bits
+#pragma unroll
+  for (int k = 0; k < kPackPerThread; ++k)
+    if (base + k < n) mine += varint_bits(z[k], len);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long incl = mine;
+  uint32_t incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
   if (lane == 31) wsum[warp] = incl;
@@ -860,26 +867,19 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ 
   if (threadIdx.x == 0)
     for (int w = 1; w < kPackThreads / 32; ++w) wsum[w] += wsum[w - 1];
   __syncthreads();
-  const unsigned long long tile_total = wsum[kPackThreads / 32 - 1];
+  const uint32_t tile_total = wsum[kPackThreads / 32 - 1];
+  // warp 0 looks back for the tile's global start bit while the other warps
+  // already pack at tile-relative positions
   if (warp == 0) {
-    const unsigned long long p = lookback(status, t, tile_total);
-    if (lane == 0) s_prefix = p;
+    const unsigned long long pfx = lookback(status, t, tile_total);
+    if (lane == 0) s_prefix = pfx;
   }
-  __syncthreads();
-  const unsigned long long tile_start_bit = s_prefix;
-  const uint32_t shift0 = static_cast<uint32_t>(tile_start_bit & 31);
-  const uint64_t nwords = (shift0 + tile_total + 31) >> 5;
-  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0;
-  __syncthreads();
-  // Each thread's codes form one contiguous bit span: assemble it in a 64-bit
-  // register accumulator and store whole words; only the span's first and
-  // last words can be shared with a neighbouring thread (atomicOr).
-  const uint64_t p0 = shift0 + (warp ? wsum[warp - 1] : 0) + incl - mine;
-  const uint64_t p1 = p0 + mine;  // span [p0, p1)
+  const uint32_t p0 = (warp ? wsum[warp - 1] : 0) + incl - mine;
   if (mine) {
-    const uint32_t w_first = static_cast<uint32_t>(p0 >> 5), w_last = static_cast<uint32_t>((p1 - 1) >> 5);
-    uint64_t acc = 0;                                  // bits left-aligned
-    uint32_t nacc = static_cast<uint32_t>(p0 & 31);    // the first word starts mid-word
+    const uint32_t p1 = p0 + mine;
+    const uint32_t w_first = p0 >> 5, w_last = (p1 - 1) >> 5;
+    uint64_t acc = 0;            // bits left-aligned
+    uint32_t nacc = p0 & 31;     // the first word starts mid-word
     uint32_t wi = w_first;
     auto put_word = [&](uint32_t word) {
       if (wi == w_first || wi == w_last) atomicOr(&words[wi], word);
@@ -907,9 +907,15 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ 
     if (nacc) put_word(static_cast<uint32_t>(acc >> 32));
   }
   __syncthreads();
+  // store, shifted right by the global bit alignment of the tile
+  const unsigned long long tile_start_bit = s_prefix;
+  const uint32_t shift0 = static_cast<uint32_t>(tile_start_bit & 31);
+  const uint32_t nwords = (shift0 + tile_total + 31) >> 5;
   const uint64_t gw0 = tile_start_bit >> 5;
-  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) {
-    const uint32_t val = bswap32(words[w]);
+  for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) {
+    const uint32_t hi = w ? words[w - 1] : 0u, lo = words[w];
+    const uint32_t word = shift0 ? ((lo >> shift0) | (hi << (32 - shift0))) : lo;
+    const uint32_t val = bswap32(word);
     if (w == 0) edge_first[t] = val;
     else if (w == nwords - 1) edge_last[t] = val;
     else out[gw0 + w] = val;

@@ -965,13 +965,24 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
       const uint64_t nwords = (total_bits + 31) / 32 + 2;
       auto* words = ctx.bits.get<uint32_t>(nwords * 4 + 16);
       prof.begin("pack", static_cast<double>(N) * (wide ? 8 : 4) + static_cast<double>(nbytes));
-      const size_t smem = static_cast<size_t>(kPackMaxWords) * 4;
+      // shared-memory image of one tile: bounded by the longest varint × the longest code
+      const int maxl = codec == Codec::varint ? 8 : table.max_len;
+      const uint32_t cap_words = static_cast<uint32_t>(
+          (static_cast<uint64_t>(kPackTile) * (wide ? 10 : 5) * static_cast<uint64_t>(maxl) + 31) / 32 + 1);
+      const size_t smem = static_cast<size_t>(cap_words + 1) * 4;
+      if (smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_pack_lb<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(k_pack_lb<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                200 * 1024));
+      }
       if (wide)
-        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(
-            static_cast<unsigned long long*>(zzp), N, dcodes, dlens, status, ticket, tstart, efirst, elast, words);
+        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<unsigned long long*>(zzp), N,
+                                                                            dcodes, dlens, status, ticket, tstart,
+                                                                            efirst, elast, words, cap_words);
       else
-        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(
-            static_cast<uint32_t*>(zzp), N, dcodes, dlens, status, ticket, tstart, efirst, elast, words);
+        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<uint32_t*>(zzp), N, dcodes,
+                                                                            dlens, status, ticket, tstart, efirst,
+                                                                            elast, words, cap_words);
       check_launch("k_pack_lb");
       k_pack_edges<<<static_cast<unsigned>((ntiles + 255) / 256), 256, 0, s>>>(tstart, ntiles, efirst, elast,
                                                                               words);
