@@ -335,52 +335,70 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_emit_s(const uint32_t* __r
   const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
   uint32_t p = static_cast<uint32_t>(s.start - base);
   const uint32_t ex = static_cast<uint32_t>(s.exit - base);
-  uint64_t acc = 0;
-  int nb = 0;
+  const bool near_end = ex + 256 >= tl;  // only then can a codeword run past the stream end
   unsigned err = 0, wide = 0;
   BitReader br;
   br.init(sm, p);
-  for (;;) {
-    if (p >= ex && nb == 0) break;
-    if (k >= N) break;
+  if (skipping) {  // the value open at the start began in the previous subsequence: skip to its end
+    for (;;) {
+      br.refill();
+      const uint32_t ent = lut[br.peek(maxlen)];
+      const uint32_t l = lut_len(ent);
+      if (p + l > tl) {
+        err = 2;
+        break;
+      }
+      p += l;
+      br.consume(l);
+      if (lut_term(ent)) {
+        ++k;
+        break;
+      }
+    }
+  }
+  // values stored by this thread: indices k .. ; `room` of them before N
+  const uint64_t room64 = k < N ? N - k : 0;
+  const uint32_t room = static_cast<uint32_t>(umin64(room64, 0xFFFFFFFFu));
+  const uint32_t k_lo = static_cast<uint32_t>(k);  // low bits for the chunk slots
+  uint32_t kk = 0;
+  uint64_t acc = 0;
+  uint32_t sh = 0;  // 7 × bytes of the open value
+  while (!err) {
+    if (p >= ex && sh == 0) break;
+    if (kk >= room) break;
     br.refill();
     const uint32_t ent = lut[br.peek(maxlen)];
     const uint32_t l = lut_len(ent);
-    if (p + l > tl) {  // stream ends inside an open value
+    if (near_end && p + l > tl) {  // stream ends inside an open value
       err = 2;
       break;
     }
-    const uint32_t b = ent & 0xFF;
     p += l;
     br.consume(l);
-    if (skipping) {
-      if (b < 0x80) {
-        skipping = false;
-        ++k;
-      }
-      continue;
-    }
-    if (nb == 9 && (b & 0xFE)) {  // varint overflows 64 bits (codec.cpp:80-81)
+    if (sh == 63 && (ent & 0xFEu)) {  // varint overflows 64 bits (codec.cpp:80-81)
       err = 1;
       break;
     }
-    acc |= static_cast<uint64_t>(b & 0x7F) << (7 * nb);
-    ++nb;
-    if (b < 0x80) {
-      if (sizeof(Z) == 4 && acc > 0xFFFFFFFFull) wide = 1;
-      my[k & (CH - 1)] = static_cast<Z>(acc);
-      if (((k + 1) & (CH - 1)) == 0) flush(k + 1);
-      if (k == N - 1) {  // exhausted_clean (codec.cpp:370-375)
-        st->end_bit = base + p;
-        const uint32_t rest = tl - p;
-        br.refill();
-        st->clean = rest < 8 && (rest == 0 || (static_cast<uint32_t>(br.buf >> 32) >> (32 - rest)) == 0);
-      }
-      ++k;
-      acc = 0;
-      nb = 0;
+    acc |= static_cast<uint64_t>(ent & 0x7Fu) << sh;
+    if (!lut_term(ent)) {
+      sh += 7;
+      continue;
     }
+    if (sizeof(Z) == 4 && (acc >> 32)) wide = 1;
+    const uint32_t ki = k_lo + kk;
+    my[ki & (CH - 1)] = static_cast<Z>(acc);
+    if (((ki + 1) & (CH - 1)) == 0) flush(k + kk + 1);
+    if (kk + 1 == room && room64 <= 0xFFFFFFFFu) {  // the N-th value: exhausted_clean (codec.cpp:370-375)
+      st->end_bit = base + p;
+      const uint32_t rest = tl - p;
+      br.refill();
+      st->clean = rest < 8 && (rest == 0 || (static_cast<uint32_t>(br.buf >> 32) >> (32 - rest)) == 0);
+    }
+    ++kk;
+    acc = 0;
+    sh = 0;
   }
+  k += kk;
   if ((k & (CH - 1)) != 0 && k > k_first) flush(k);
   if (err) atomicMax(&st->error, err);
   if (wide) atomicOr(&st->wide, 1u);
