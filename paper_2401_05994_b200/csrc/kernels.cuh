@@ -276,7 +276,16 @@ __global__ void __launch_bounds__(128) k_block_sumsq(const T* __restrict__ v, ui
 struct QuantFlags {
   unsigned long long overflow;  // |c/δ| ≥ 2^63 (quantize.cpp:113-116)
   unsigned int wide;            // some zz does not fit the u32 store
+  unsigned int pad;
+  unsigned long long rmax_bits; // max |r| over the coarse-box nodes (bits of a non-negative double)
 };
+
+__device__ __forceinline__ void flag_rmax(QuantFlags* f, double rmax) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  if ((threadIdx.x & 31) == 0 && rmax > 0.0)
+    atomicMax(&f->rmax_bits, static_cast<unsigned long long>(__double_as_longlong(rmax)));
+}
 
 __device__ __forceinline__ void hist_flush(uint32_t* sh, uint32_t& sym, uint32_t& cnt) {
   if (cnt) atomicAdd(&sh[sym], cnt);
@@ -598,27 +607,40 @@ __global__ void __launch_bounds__(256) k_coarse_resid(GridDev g, Widths W, const
 }
 
 // Check epilogues of the fused pass: (n, e, source value widened, reduction).
-struct ChkMaxAbs {  // max|e| (error_control.cpp:105, exec.cpp:75-87)
+struct ChkMaxAbs {
+  static constexpr bool kNeedsE = true;  // max|e| (error_control.cpp:105, exec.cpp:75-87)
   __device__ __forceinline__ void operator()(uint64_t, double e, double, double& red) const {
     red = fmax(red, fabs(e));
   }
 };
-struct ChkCastMaxAbs {  // f32: max|src − (double)(float)(u − e)| (container.cpp:96-107)
+struct ChkCastMaxAbs {
+  static constexpr bool kNeedsE = true;  // f32: max|src − (double)(float)(u − e)| (container.cpp:96-107)
   __device__ __forceinline__ void operator()(uint64_t, double e, double s, double& red) const {
     red = fmax(red, fabs(__dsub_rn(s, static_cast<double>(__double2float_rn(__dsub_rn(s, e))))));
   }
 };
-struct ChkStore {  // S(0): e stored for the ordered 4096-block RMS
+struct ChkStore {
+  static constexpr bool kNeedsE = true;  // S(0): e stored for the ordered 4096-block RMS
   double* out;
   __device__ __forceinline__ void operator()(uint64_t n, double e, double, double&) const { out[n] = e; }
 };
-struct ChkCastStore {  // S(0), f32: the cast error stored
+struct ChkCastStore {
+  static constexpr bool kNeedsE = true;  // S(0), f32: the cast error stored
   double* out;
   __device__ __forceinline__ void operator()(uint64_t n, double e, double s, double&) const {
     out[n] = __dsub_rn(s, static_cast<double>(__double2float_rn(__dsub_rn(s, e))));
   }
 };
-struct ChkLevelWeighted {  // S(s≠0): Σ 2^{2s(tag−L)} r² (error_control.cpp:72-100), r passed as e
+// Bound pass: the a-posteriori error is not evaluated; the pass only tracks
+// max|r| over the finest nodes (passed as e), see compress_t's accept bound.
+struct ChkBound {
+  static constexpr bool kNeedsE = false;
+  __device__ __forceinline__ void operator()(uint64_t, double r, double, double& red) const {
+    red = fmax(red, fabs(r));
+  }
+};
+struct ChkLevelWeighted {
+  static constexpr bool kNeedsE = true;  // S(s≠0): Σ 2^{2s(tag−L)} r² (error_control.cpp:72-100), r passed as e
   __device__ __forceinline__ void operator()(uint64_t, double, double, double&) const {}
 };
 

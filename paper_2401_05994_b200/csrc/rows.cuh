@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(256) k_coarse_quant(GridDev g, Widths W, const
   auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
   unsigned long long ovf = 0;
   unsigned wide = 0;
+  double rmax = 0.0;
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < g.Nc; j += step) {
     uint32_t i[4] = {0, 0, 0, 0};
@@ -218,7 +219,9 @@ __global__ void __launch_bounds__(256) k_coarse_quant(GridDev g, Widths W, const
     }
     ec[j] = r;
     zc[j] = static_cast<Z>(z);
+    rmax = fmax(rmax, fabs(r));
   }
+  flag_rmax(flags, rmax);
   if (ovf) atomicAdd(&flags->overflow, ovf);
   if (wide) atomicOr(&flags->wide, 1u);
 }
@@ -422,6 +425,7 @@ struct PairCtx {
   // one row unit (64 columns) with M outer corner rows (M = 1: row not all-fine)
   template <int M, class Meta>
   __device__ __forceinline__ void unit(const Meta& m, uint32_t k0, uint32_t kk, uint32_t Kt, int lane) {
+    constexpr bool kE = Chk::kNeedsE;
     const bool va = kk < Kt, vb = kk + 1 < Kt;
     const uint32_t k = k0 + min(kk, Kt - 1);
     const uint4 cc = __ldg(colc4 + (k >> 1));
@@ -442,33 +446,39 @@ struct PairCtx {
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       U0[j] = fine ? ld(m.uoff[j] + k) : sa;
-      E0[j] = __ldg(ec + (fine ? m.coff[j] : cbase0) + cc.x);
+      if constexpr (kE) E0[j] = __ldg(ec + (fine ? m.coff[j] : cbase0) + cc.x);
     }
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       U2[j] = __shfl_down_sync(0xffffffffu, U0[j], 1);
-      E2[j] = __shfl_down_sync(0xffffffffu, E0[j], 1);
+      if constexpr (kE) E2[j] = __shfl_down_sync(0xffffffffu, E0[j], 1);
     }
     if (fb && (lane == 31 || kk + 2 >= Kt)) {  // column k+2 is not held by the next lane
 #pragma unroll
       for (int j = 0; j < M; ++j) {
         U2[j] = ld((fine ? m.uoff[j] : own) + k + 2);
-        E2[j] = __ldg(ec + (fine ? m.coff[j] : cbase0) + cc.w);
+        if constexpr (kE) E2[j] = __ldg(ec + (fine ? m.coff[j] : cbase0) + cc.w);
       }
     }
     if (!va) return;
     // column k (even, never fresh)
     if (fine) {
-      double acc = 0.0, eacc = 0.0;
+      double acc = 0.0;
 #pragma unroll
       for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], U0[j]));
-#pragma unroll
-      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(m.w[j], E0[j]));
       double r;
       const uint64_t z = quant(__dsub_rn(sa, acc), r);
-      emit(n, z, __dadd_rn(r, eacc), sa);
+      if constexpr (kE) {
+        double eacc = 0.0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(m.w[j], E0[j]));
+        emit(n, z, __dadd_rn(r, eacc), sa);
+      } else {
+        emit(n, z, r, sa);
+      }
     } else {
-      emit(n, static_cast<uint64_t>(zc[cbase0 + cc.x]), E0[0], sa);
+      if constexpr (kE) emit(n, static_cast<uint64_t>(zc[cbase0 + cc.x]), E0[0], sa);
+      else emit(n, static_cast<uint64_t>(zc[cbase0 + cc.x]), 0.0, sa);
     }
     if (!vb) return;
     // column k+1
@@ -479,30 +489,41 @@ struct PairCtx {
         wlj[j] = __dmul_rn(m.w[j], wl);
         wrj[j] = __dmul_rn(m.w[j], wr);
       }
-      double acc = 0.0, eacc = 0.0;
+      double acc = 0.0;
 #pragma unroll
       for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(wlj[j], U0[j]));
 #pragma unroll
       for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(wrj[j], U2[j]));
-#pragma unroll
-      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(wlj[j], E0[j]));
-#pragma unroll
-      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(wrj[j], E2[j]));
       double r;
       const uint64_t z = quant(__dsub_rn(sb, acc), r);
-      emit(n + 1, z, __dadd_rn(r, eacc), sb);
+      if constexpr (kE) {
+        double eacc = 0.0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(wlj[j], E0[j]));
+#pragma unroll
+        for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(wrj[j], E2[j]));
+        emit(n + 1, z, __dadd_rn(r, eacc), sb);
+      } else {
+        emit(n + 1, z, r, sb);
+      }
     } else if (fine) {  // last index of an even-length axis, tagged L by the outer axes
-      double acc = 0.0, eacc = 0.0;
+      double acc = 0.0;
 #pragma unroll
       for (int j = 0; j < M; ++j) acc = __dadd_rn(acc, __dmul_rn(m.w[j], ld(m.uoff[j] + k + 1)));
-#pragma unroll
-      for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(m.w[j], __ldg(ec + m.coff[j] + cc.z)));
       double r;
       const uint64_t z = quant(__dsub_rn(sb, acc), r);
-      emit(n + 1, z, __dadd_rn(r, eacc), sb);
+      if constexpr (kE) {
+        double eacc = 0.0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) eacc = __dadd_rn(eacc, __dmul_rn(m.w[j], __ldg(ec + m.coff[j] + cc.z)));
+        emit(n + 1, z, __dadd_rn(r, eacc), sb);
+      } else {
+        emit(n + 1, z, r, sb);
+      }
     } else {
       const uint64_t cj = cbase0 + cc.z;
-      emit(n + 1, static_cast<uint64_t>(zc[cj]), ec[cj], sb);
+      if constexpr (kE) emit(n + 1, static_cast<uint64_t>(zc[cj]), ec[cj], sb);
+      else emit(n + 1, static_cast<uint64_t>(zc[cj]), 0.0, sb);
     }
   }
 };
@@ -1147,7 +1168,7 @@ template <int M, int NS, typename T, typename Z>
 __device__ __forceinline__ void cq_unit(const GridDev& g, const GridDev& gc, const RowCQ<NS>& m, const T* __restrict__ u,
                                         double* __restrict__ ec, Z* __restrict__ zc, double delta, double inv,
                                         uint32_t k0, uint32_t kk, uint32_t Kt, int lane, int D,
-                                        unsigned long long& ovf, unsigned& wide) {
+                                        unsigned long long& ovf, unsigned& wide, double& rmax) {
   const bool va = kk < Kt, vb = kk + 1 < Kt;
   const uint32_t k = k0 + min(kk, Kt - 1);
   const AxisTab& axc = gc.ax[D - 1];
@@ -1179,6 +1200,7 @@ __device__ __forceinline__ void cq_unit(const GridDev& g, const GridDev& gc, con
     }
     ec[nc] = r;
     zc[nc] = static_cast<Z>(z);
+    rmax = fmax(rmax, fabs(r));
   };
   if (fine) {  // even column, tag L−1 through the outer axes
     double acc = 0.0;
@@ -1213,6 +1235,7 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_cq_warp(GridDev g, GridDev g
   const double delta = W.w[gc.L];
   unsigned long long ovf = 0;
   unsigned wide = 0;
+  double rmax = 0.0;
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
   const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -1226,14 +1249,15 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_cq_warp(GridDev g, GridDev g
     const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
     for (uint32_t ch = 0; ch < nchunks; ++ch) {
       const uint32_t kk = ch * kUnitCols + 2 * lane;
-      if (!mm.all_fine) cq_unit<1>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide);
+      if (!mm.all_fine) cq_unit<1>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide, rmax);
       else if (D >= 4 && mm.nsub == 8)
-        cq_unit<(D >= 4 ? 8 : 2)>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide);
+        cq_unit<(D >= 4 ? 8 : 2)>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide, rmax);
       else if (D >= 3 && mm.nsub == 4)
-        cq_unit<(D >= 3 ? 4 : 2)>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide);
-      else cq_unit<2>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide);
+        cq_unit<(D >= 3 ? 4 : 2)>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide, rmax);
+      else cq_unit<2>(g, gc, mm, u, ec, zc, delta, inv, k0, kk, Kt, lane, D, ovf, wide, rmax);
     }
   }
+  flag_rmax(flags, rmax);
   if (ovf) atomicAdd(&flags->overflow, ovf);
   if (wide) atomicOr(&flags->wide, 1u);
 }
@@ -1246,6 +1270,7 @@ __global__ void __launch_bounds__(256) k_cq_box(GridDev g, BoxDev box, Widths W,
   auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
   unsigned long long ovf = 0;
   unsigned wide = 0;
+  double rmax = 0.0;
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < box.count; p += step) {
     uint32_t i[4] = {0, 0, 0, 0};
@@ -1275,7 +1300,9 @@ __global__ void __launch_bounds__(256) k_cq_box(GridDev g, BoxDev box, Widths W,
     }
     ec[nc] = r;
     zc[nc] = static_cast<Z>(z);
+    rmax = fmax(rmax, fabs(r));
   }
+  flag_rmax(flags, rmax);
   if (ovf) atomicAdd(&flags->overflow, ovf);
   if (wide) atomicOr(&flags->wide, 1u);
 }
