@@ -278,6 +278,7 @@ struct QuantFlags {
   unsigned int wide;            // some zz does not fit the u32 store
   unsigned int pad;
   unsigned long long rmax_bits; // max |r| over the coarse-box nodes (bits of a non-negative double)
+  unsigned long long queue;     // row-segment work queue of the fused pass
 };
 
 __device__ __forceinline__ void flag_rmax(QuantFlags* f, double rmax) {

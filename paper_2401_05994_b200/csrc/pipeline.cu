@@ -555,7 +555,7 @@ struct FinePairs {
                     Z* zz, unsigned long long* hist, QuantFlags* fl, const double* ec, const Z* zc, const Chk& chk,
                     unsigned long long* red, int blocks) {
       k_fine_warp<D, T, Z, Chk><<<num_sms() * 2, kRowThreads, 0, s>>>(g, rt, W, inv_L, u, zz, hist, fl, ec, zc, chk,
-                                                                       red);
+                                                                       red, &fl->queue);
       check_launch("k_fine_warp");
       (void)blocks;
     }

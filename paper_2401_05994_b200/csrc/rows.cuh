@@ -688,7 +688,8 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_fine_warp(GridDev g, RowTili
                                                              const T* __restrict__ u, Z* __restrict__ zz,
                                                              unsigned long long* __restrict__ hist, QuantFlags* flags,
                                                              const double* __restrict__ ec, const Z* __restrict__ zc,
-                                                             Chk chk, unsigned long long* __restrict__ red_out) {
+                                                             Chk chk, unsigned long long* __restrict__ red_out,
+                                                             unsigned long long* queue) {
   __shared__ uint32_t sh[256];
   for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
   __syncthreads();
@@ -712,7 +713,12 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_fine_warp(GridDev g, RowTili
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
   const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t item = gw; item < nitems; item += nwarps) {
+  // dynamic row-segment queue (load balance; every reduction here is order-independent)
+  uint64_t item = 0;
+  if (lane == 0) item = atomicAdd(queue, 1ull);
+  item = __shfl_sync(0xffffffffu, item, 0);
+  (void)gw;
+  while (item < nitems) {
     const uint64_t row = item / rt.ncol_tiles;
     const uint32_t seg = static_cast<uint32_t>(item - row * rt.ncol_tiles);
     const uint32_t k0 = seg * rt.K;  // even
@@ -720,7 +726,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_fine_warp(GridDev g, RowTili
     RowLite<(1 << (D - 1))> mm;
     warp_row_meta<D>(g, row, mm);
     {  // pull this warp's next row segment of u into L2 while this one is computed
-      const uint64_t nitem = item + nwarps;
+      const uint64_t nitem = item + nwarps;  // roughly the segment this warp gets next
       if (nitem < nitems) {
         const uint64_t nrow = nitem / rt.ncol_tiles;
         const uint32_t nk0 = static_cast<uint32_t>(nitem - nrow * rt.ncol_tiles) * rt.K;
@@ -739,6 +745,8 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_fine_warp(GridDev g, RowTili
       else if (D >= 3 && mm.nsub == 4) P.template unit<(D >= 3 ? 4 : 2)>(mm, k0, kk, Kt, lane);
       else P.template unit<2>(mm, k0, kk, Kt, lane);
     }
+    if (lane == 0) item = atomicAdd(queue, 1ull);
+    item = __shfl_sync(0xffffffffu, item, 0);
   }
   hist_flush(sh, P.hsym, P.hcnt);
   if (P.ovf) atomicAdd(&flags->overflow, P.ovf);
