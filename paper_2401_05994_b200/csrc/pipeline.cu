@@ -127,6 +127,7 @@ struct Scratch {  // small device-side results read back at sync points
   unsigned int fix_changed;
   unsigned int raw_wide;
   unsigned long long hist[256];
+  unsigned long long queues[4];  // dynamic work queues of the row kernels (zeroed per launch)
 };
 
 class Context {
@@ -523,9 +524,10 @@ struct CoarseQuantRows {
   template <int D>
   struct L {
     static void run(cudaStream_t s, const GridDev& g, const GridDev& gc, const BoxDev& box2, const Widths& W,
-                    double inv, const T* u, double* ec, Z* zc, QuantFlags* fl) {
+                    double inv, const T* u, double* ec, Z* zc, QuantFlags* fl, unsigned long long* queue) {
       const RowTiling rt = row_tiling(gc);
-      k_cq_warp<D, T, Z><<<num_sms() * 3, kRowThreads, 0, s>>>(g, gc, rt, W, inv, u, ec, zc, fl);
+      CK(cudaMemsetAsync(queue, 0, 8, s));
+      k_cq_warp<D, T, Z><<<num_sms() * 3, kRowThreads, 0, s>>>(g, gc, rt, W, inv, u, ec, zc, fl, queue);
       check_launch("k_cq_warp");
       k_cq_box<D, T, Z><<<grid_blocks(box2.count, 256), 256, 0, s>>>(g, box2, W, u, ec, zc, fl);
       check_launch("k_cq_box");
@@ -565,9 +567,10 @@ struct FinePairs {
 struct InvWarp {
   template <int D>
   struct L {
-    static void run(cudaStream_t s, const GridDev& g, double* v) {
+    static void run(cudaStream_t s, const GridDev& g, double* v, unsigned long long* queue) {
       const RowTiling rt = row_tiling(g);
-      k_inv_warp<D><<<num_sms() * 3, kRowThreads, 0, s>>>(g, rt, v);
+      CK(cudaMemsetAsync(queue, 0, 8, s));
+      k_inv_warp<D><<<num_sms() * 3, kRowThreads, 0, s>>>(g, rt, v, queue);
       check_launch("k_inv_warp");
     }
   };
@@ -589,9 +592,10 @@ struct ReconRows {
   template <int D>
   struct L {
     static void run(cudaStream_t s, const GridDev& g, const RowTiling& rt, const Widths& W, const Z* zz,
-                    const double* vc, const Out& out) {
+                    const double* vc, const Out& out, unsigned long long* queue) {
       if (g.L >= 1) {
-        k_recon_warp<D, Z, Out><<<num_sms() * 3, kRowThreads, 0, s>>>(g, rt, W, zz, vc, out);
+        CK(cudaMemsetAsync(queue, 0, 8, s));
+        k_recon_warp<D, Z, Out><<<num_sms() * 3, kRowThreads, 0, s>>>(g, rt, W, zz, vc, out, queue);
         check_launch("k_recon_warp");
       } else {
         k_recon_rows<D, Z, Out><<<static_cast<unsigned>(row_tiles(rt)), kRowThreads, 0, s>>>(g, rt, W, zz, vc, out);
@@ -829,14 +833,14 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
           prof.begin("coarse_check", static_cast<double>(g.Nc) * (sizeof(T) + 8 + zb));
           if (L >= 2)
             by_dim<CoarseQuantRows<T, Z>::template L>(grid.d, s, g, dh.gc, dh.boxes[L - 2], W, 1.0 / widths[L - 1], u,
-                                                      ec, zc, &sd->qflags);
+                                                      ec, zc, &sd->qflags, &sd->queues[0]);
           else
             by_dim<CoarseQuant<T, Z>::template L>(grid.d, s, g, W, u, ec, zc, &sd->qflags);
           if (!level_weighted && !bound) {
             const SrcResidual csrc{ec};
             for (int l = 1; l < dh.gc.L; ++l)
               by_dim<InvBox<SrcResidual>::template L>(grid.d, s, dh.gc, dh.cboxes[l], l, csrc, ec);
-            if (dh.gc.L >= 1) by_dim<InvWarp::L>(grid.d, s, dh.gc, ec);
+            if (dh.gc.L >= 1) by_dim<InvWarp::L>(grid.d, s, dh.gc, ec, &sd->queues[1]);
           }
           prof.end();
         }
@@ -1115,13 +1119,15 @@ static void run_recon(Context& ctx, DevHier& dh, const Z* zz, const Widths& W, D
     const SrcResidual csrc{vc};
     for (int l = 1; l < dh.gc.L; ++l)
       by_dim<InvBox<SrcResidual>::template L>(g.d, s, dh.gc, dh.cboxes[l], l, csrc, vc);
-    if (dh.gc.L >= 1) by_dim<InvWarp::L>(g.d, s, dh.gc, vc);
+    if (dh.gc.L >= 1) by_dim<InvWarp::L>(g.d, s, dh.gc, vc, &ctx.sd()->queues[1]);
   }
   const RowTiling rt = row_tiling(g);
   if (dtype == DType::f64)
-    by_dim<ReconRows<Z, OutF64>::template L>(g.d, s, g, rt, W, zz, vc, OutF64{static_cast<double*>(out)});
+    by_dim<ReconRows<Z, OutF64>::template L>(g.d, s, g, rt, W, zz, vc, OutF64{static_cast<double*>(out)},
+                                             &ctx.sd()->queues[2]);
   else
-    by_dim<ReconRows<Z, OutF32>::template L>(g.d, s, g, rt, W, zz, vc, OutF32{static_cast<float*>(out)});
+    by_dim<ReconRows<Z, OutF32>::template L>(g.d, s, g, rt, W, zz, vc, OutF32{static_cast<float*>(out)},
+                                             &ctx.sd()->queues[2]);
 }
 
 DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void* out, uint64_t out_cap) {

@@ -675,6 +675,13 @@ __device__ __forceinline__ void warp_row_meta(const GridDev& g, uint64_t row, Ro
   }
 }
 
+// Warp-wide dynamic work item (lane 0 takes a ticket, broadcast to the warp).
+__device__ __forceinline__ uint64_t next_item(unsigned long long* queue) {
+  uint64_t it = 0;
+  if ((threadIdx.x & 31) == 0) it = atomicAdd(queue, 1ull);
+  return __shfl_sync(0xffffffffu, it, 0);
+}
+
 // Registers of one 64-column unit (lane: columns k, k+1).
 template <int M>
 struct UnitLoads {
@@ -950,7 +957,7 @@ struct ReconCtx {
 template <int D, typename Z, class Out>
 __global__ void __launch_bounds__(kRowThreads, 3) k_recon_warp(GridDev g, RowTiling rt, Widths W,
                                                               const Z* __restrict__ zz, const double* __restrict__ vc,
-                                                              Out out) {
+                                                              Out out, unsigned long long* queue) {
   const int lane = threadIdx.x & 31;
   ReconCtx<Z, Out> P;
   P.zz = zz;
@@ -962,7 +969,8 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_recon_warp(GridDev g, RowTil
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
   const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t item = gw; item < nitems; item += nwarps) {
+  (void)gw;
+  for (uint64_t item = next_item(queue); item < nitems; item = next_item(queue)) {
     const uint64_t row = item / rt.ncol_tiles;
     const uint32_t seg = static_cast<uint32_t>(item - row * rt.ncol_tiles);
     const uint32_t k0 = seg * rt.K;
@@ -1089,12 +1097,14 @@ __device__ __forceinline__ void inv_unit(const GridDev& g, const RowU<NS>& m, do
 }
 
 template <int D>
-__global__ void __launch_bounds__(kRowThreads, 3) k_inv_warp(GridDev g, RowTiling rt, double* v) {
+__global__ void __launch_bounds__(kRowThreads, 3) k_inv_warp(GridDev g, RowTiling rt, double* v,
+                                                            unsigned long long* queue) {
   const int lane = threadIdx.x & 31;
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
   const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t item = gw; item < nitems; item += nwarps) {
+  (void)gw;
+  for (uint64_t item = next_item(queue); item < nitems; item = next_item(queue)) {
     const uint64_t row = item / rt.ncol_tiles;
     const uint32_t seg = static_cast<uint32_t>(item - row * rt.ncol_tiles);
     const uint32_t k0 = seg * rt.K;
@@ -1238,7 +1248,8 @@ __device__ __forceinline__ void cq_unit(const GridDev& g, const GridDev& gc, con
 template <int D, typename T, typename Z>
 __global__ void __launch_bounds__(kRowThreads, 3) k_cq_warp(GridDev g, GridDev gc, RowTiling rt, Widths W, double inv,
                                                            const T* __restrict__ u, double* __restrict__ ec,
-                                                           Z* __restrict__ zc, QuantFlags* flags) {
+                                                           Z* __restrict__ zc, QuantFlags* flags,
+                                                           unsigned long long* queue) {
   const int lane = threadIdx.x & 31;
   const double delta = W.w[gc.L];
   unsigned long long ovf = 0;
@@ -1247,7 +1258,8 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_cq_warp(GridDev g, GridDev g
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
   const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t item = gw; item < nitems; item += nwarps) {
+  (void)gw;
+  for (uint64_t item = next_item(queue); item < nitems; item = next_item(queue)) {
     const uint64_t row = item / rt.ncol_tiles;
     const uint32_t seg = static_cast<uint32_t>(item - row * rt.ncol_tiles);
     const uint32_t k0 = seg * rt.K;
