@@ -142,6 +142,8 @@ class Context {
   DevBuf scratch_d;
   PinnedBuf scratch_h, partial_h;
   std::unique_ptr<DevHier> hier;
+  cudaStream_t aux = nullptr;            // concurrent side work (decompress CRC)
+  cudaEvent_t ev_in = nullptr, ev_crc = nullptr;
   CrcConsts crc_k{};
   bool crc_ready = false;
 
@@ -149,6 +151,9 @@ class Context {
   Scratch* sh() { return scratch_h.get<Scratch>(sizeof(Scratch)); }
 
   ~Context() {
+    if (aux) cudaStreamDestroy(aux);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_crc) cudaEventDestroy(ev_crc);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
@@ -651,8 +656,9 @@ struct CrcSlot {
   unsigned long long* len;
 };
 
-static CrcSlot device_crc_launch(Context& ctx, const uint8_t* p, uint64_t n) {
+static CrcSlot device_crc_launch(Context& ctx, const uint8_t* p, uint64_t n, cudaStream_t cs = nullptr) {
   ensure_crc(ctx);
+  if (!cs) cs = ctx.stream;
   const uint64_t per_block = static_cast<uint64_t>(kCrcThreads) * kCrcSeg;
   uint64_t nb = std::max<uint64_t>(1, (n + per_block - 1) / per_block);
   const size_t cap = ((nb + 1) * (4 + 8) + 1024 + 255) & ~size_t{255};
@@ -662,12 +668,12 @@ static CrcSlot device_crc_launch(Context& ctx, const uint8_t* p, uint64_t n) {
   uint8_t* B = A + cap;
   uint32_t* c1 = reinterpret_cast<uint32_t*>(B);
   unsigned long long* l1 = reinterpret_cast<unsigned long long*>(B + ((4 * (nb + 1) + 15) & ~size_t{15}));
-  k_crc_blocks<<<static_cast<unsigned>(nb), kCrcThreads, 0, ctx.stream>>>(p, n, ctx.crc_tab.get<uint32_t>(4096),
-                                                                          ctx.crc_k, c0, l0);
+  k_crc_blocks<<<static_cast<unsigned>(nb), kCrcThreads, 0, cs>>>(p, n, ctx.crc_tab.get<uint32_t>(4096), ctx.crc_k,
+                                                                  c0, l0);
   check_launch("k_crc_blocks");
   while (nb > 1) {
     const uint64_t nb2 = (nb + kCrcThreads - 1) / kCrcThreads;
-    k_crc_fold<<<static_cast<unsigned>(nb2), kCrcThreads, 0, ctx.stream>>>(c0, l0, nb, ctx.crc_k, c1, l1);
+    k_crc_fold<<<static_cast<unsigned>(nb2), kCrcThreads, 0, cs>>>(c0, l0, nb, ctx.crc_k, c1, l1);
     check_launch("k_crc_fold");
     std::swap(c0, c1);
     std::swap(l0, l1);
@@ -1170,19 +1176,38 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
   prof.end();
   Scratch* sd = ctx.sd();
   Scratch* sh = ctx.sh();
-  // CRC (container.cpp:217-218)
+  // CRC (container.cpp:217-218), computed on the auxiliary stream concurrently
+  // with the decode; it is checked before any later error is reported and
+  // before returning, so a checksum mismatch still takes precedence exactly as
+  // in the reference (which checks it first).
   uint32_t crc = crc32_host(head.data(), split);
+  CrcSlot slot{nullptr, nullptr};
   if (body_len) {
-    prof.begin("crc", static_cast<double>(body_len));
-    CrcSlot slot = device_crc_launch(ctx, body, body_len);
-    prof.end();
-    CK(cudaMemcpyAsync(&sh->fix_changed, slot.crc, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    crc = split ? crc32_combine(crc, sh->fix_changed, body_len) : sh->fix_changed;
-  } else {
-    CK(cudaStreamSynchronize(s));
+    if (!ctx.aux) {
+      CK(cudaStreamCreateWithFlags(&ctx.aux, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx.ev_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx.ev_crc, cudaEventDisableTiming));
+    }
+    ensure_crc(ctx);
+    CK(cudaEventRecord(ctx.ev_in, s));
+    CK(cudaStreamWaitEvent(ctx.aux, ctx.ev_in, 0));
+    slot = device_crc_launch(ctx, body, body_len, ctx.aux);
+    CK(cudaEventRecord(ctx.ev_crc, ctx.aux));
   }
-  if (crc != info.checksum) raise(Errc::checksum_mismatch, "payload checksum failed");
+  bool crc_checked = false;
+  auto check_crc = [&]() {
+    if (crc_checked) return;
+    crc_checked = true;
+    if (body_len) {
+      uint32_t dcrc = 0;
+      CK(cudaMemcpyAsync(&sh->fix_changed, slot.crc, 4, cudaMemcpyDeviceToHost, ctx.aux));
+      CK(cudaStreamSynchronize(ctx.aux));
+      dcrc = sh->fix_changed;
+      crc = split ? crc32_combine(crc, dcrc, body_len) : dcrc;
+    }
+    if (crc != info.checksum) raise(Errc::checksum_mismatch, "payload checksum failed");
+  };
+  try {
 
   if (info.constant_field) {
     if (plen != 8) raise(Errc::corrupt_stream, "constant payload must be 8 bytes");
@@ -1372,6 +1397,11 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
       run_recon(ctx, dh, ctx.zz.get<uint32_t>(N * 4), W, info.dtype, dout, N);
     prof.end();
   }
+  } catch (const Error&) {
+    check_crc();  // a checksum mismatch is reported before any decode error
+    throw;
+  }
+  check_crc();
   if (!out_dev) {
     prof.begin("d2h_output", static_cast<double>(out_bytes));
     CK(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, s));
