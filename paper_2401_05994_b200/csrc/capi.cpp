@@ -449,7 +449,8 @@ int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndims, const uint
           const void* src = data;
           if (is_device_pointer(data)) {
             host.resize(count * unit);
-            if (cudaMemcpy(host.data(), data, count * unit, cudaMemcpyDeviceToHost) != cudaSuccess)
+            if (cudaMemcpyAsync(host.data(), data, count * unit, cudaMemcpyDeviceToHost, context_stream(ctx)) != cudaSuccess ||
+                cudaStreamSynchronize(context_stream(ctx)) != cudaSuccess)
               raise(Errc::cuda, "copy failed");
             src = host.data();
           }

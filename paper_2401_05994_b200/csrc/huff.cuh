@@ -17,7 +17,10 @@
 namespace mgrc_gpu {
 namespace dev {
 
-constexpr int kWarmBits = 1024;  // warm-up decoded before each subsequence's nominal start
+#ifndef MGRC_WARM_BITS
+#define MGRC_WARM_BITS 1024
+#endif
+constexpr int kWarmBits = MGRC_WARM_BITS;  // warm-up decoded before each subsequence's nominal start
 constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never published)
 constexpr int kSyncReal = kDecThreads - kSyncWarm;
 constexpr int kSyncRounds = 1 << 20;  // in-CTA resynchronisation rounds (uncapped: capping + transfer tables measured slower)

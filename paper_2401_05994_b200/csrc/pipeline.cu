@@ -1323,7 +1323,8 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
           CK(cudaStreamSynchronize(s));
           if (nmis == 0) break;
           std::vector<unsigned long long> js(std::min<unsigned>(nmis, kCap));
-          CK(cudaMemcpy(js.data(), lst, js.size() * 8, cudaMemcpyDeviceToHost));
+          CK(cudaMemcpyAsync(js.data(), lst, js.size() * 8, cudaMemcpyDeviceToHost, s));
+          CK(cudaStreamSynchronize(s));
           std::sort(js.begin(), js.end());
           if (const char* dbg = std::getenv("MGRC_DEBUG"); dbg && dbg[0] == '2' && guard < 40) {
             std::fprintf(stderr, "[mgrc] iter %llu: %u mismatches, first:", static_cast<unsigned long long>(guard), nmis);
