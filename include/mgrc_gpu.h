@@ -119,6 +119,11 @@ MGRC_GPU_API int mgrc_gpu_decompress_chunked(const uint8_t* in, uint64_t len, vo
 MGRC_GPU_API int mgrc_gpu_field_stats(const void* data, int dtype, uint64_t n, double* min, double* max,
                                       int* nonfinite);
 
+/* Page-locked host buffers for fast host<->device staging (the CLI's raw-file
+ * reads land in one; any host pointer is accepted by the calls above). */
+MGRC_GPU_API int mgrc_gpu_host_alloc(uint64_t bytes, void** p);
+MGRC_GPU_API void mgrc_gpu_host_free(void* p);
+
 MGRC_GPU_API const char* mgrc_gpu_last_error(void);
 MGRC_GPU_API void mgrc_gpu_free(void* p);
 MGRC_GPU_API int mgrc_gpu_set_device(int device);

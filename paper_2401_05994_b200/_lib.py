@@ -34,6 +34,8 @@ SIGNATURES = {
     "mgrc_gpu_compress_to": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_double, C.c_int, C.c_double, C.c_int,
                                        C.c_int, P, C.c_uint64, U64P]),
     "mgrc_gpu_decompress": (C.c_int, [P, C.c_uint64, C.POINTER(P), IP, IP, P]),
+    "mgrc_gpu_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(P)]),
+    "mgrc_gpu_host_free": (None, [P]),
     "mgrc_gpu_decompress_into": (C.c_int, [P, C.c_uint64, P, C.c_uint64, IP, IP, P]),
     "mgrc_gpu_inspect": (C.c_int, [P, C.c_uint64, C.POINTER(ContainerInfoC)]),
     "mgrc_gpu_describe": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_char_p)]),

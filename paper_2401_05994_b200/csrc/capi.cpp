@@ -231,6 +231,22 @@ const char* mgrc_gpu_last_error(void) { return g_last_error.c_str(); }
 void mgrc_gpu_free(void* p) { std::free(p); }
 uint64_t mgrc_gpu_launch_count(void) { return launch_count(); }
 
+int mgrc_gpu_host_alloc(uint64_t bytes, void** p) {
+  return guarded([&] {
+    require(p != nullptr, "null output pointer");
+    ensure_device();
+    *p = nullptr;
+    if (cudaHostAlloc(p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      raise(Errc::cuda, "cudaHostAlloc of " + std::to_string(bytes) + " bytes failed");
+    }
+  });
+}
+
+void mgrc_gpu_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int mgrc_gpu_set_device(int device) {
   return guarded([&] {
     ensure_device();
