@@ -18,7 +18,7 @@ namespace mgrc_gpu {
 namespace dev {
 
 #ifndef MGRC_WARM_BITS
-#define MGRC_WARM_BITS 1024
+#define MGRC_WARM_BITS 512
 #endif
 constexpr int kWarmBits = MGRC_WARM_BITS;  // warm-up decoded before each subsequence's nominal start
 constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never published)
@@ -596,14 +596,10 @@ __global__ void __launch_bounds__(kTfResolveThreads) k_tf_resolve(const TfTab* _
     __syncthreads();
   }
   // 3. true entry offset of the window, then of this chunk; rewrite the entries
-  const SeqInfo first = seq[j_first];
   const uint64_t S0 = j_first * kSeqBits;
   const uint32_t e_in = static_cast<uint32_t>(
       (j_first > 0 ? *reinterpret_cast<volatile unsigned long long*>(&seq[j_first - 1].exit) : 0ull) - S0);
-  (void)first;
   uint32_t o = t == 0 ? e_in : maps[t - 1][e_in & 15];
-  uint32_t lc_prev = j_first > 0 ? seq[j_first - 1].last_cont : 0;
-  (void)lc_prev;
   for (uint64_t i = a; i < b; ++i) {
     const TfTab& tb = tabs[i];
     const uint64_t j = j_first + i;

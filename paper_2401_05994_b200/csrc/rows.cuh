@@ -1102,7 +1102,6 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_inv_warp(GridDev g, RowTilin
   const int lane = threadIdx.x & 31;
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
   const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   (void)gw;
   for (uint64_t item = next_item(queue); item < nitems; item = next_item(queue)) {
     const uint64_t row = item / rt.ncol_tiles;
@@ -1257,7 +1256,6 @@ __global__ void __launch_bounds__(kRowThreads, 3) k_cq_warp(GridDev g, GridDev g
   double rmax = 0.0;
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
   const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   (void)gw;
   for (uint64_t item = next_item(queue); item < nitems; item = next_item(queue)) {
     const uint64_t row = item / rt.ncol_tiles;
