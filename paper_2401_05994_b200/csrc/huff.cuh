@@ -22,13 +22,19 @@ namespace dev {
 #endif
 constexpr int kWarmBits = MGRC_WARM_BITS;  // warm-up decoded before each subsequence's nominal start
 constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never published)
-constexpr int kSyncReal = kDecThreads - kSyncWarm;
+#ifndef MGRC_SYNC_THREADS
+#define MGRC_SYNC_THREADS 128
+#endif
+constexpr int kSyncThreads = MGRC_SYNC_THREADS;  // subsequences (threads) per sync CTA
+constexpr int kSyncReal = kSyncThreads - kSyncWarm;
 constexpr int kSyncRounds = 1 << 20;  // in-CTA resynchronisation rounds (uncapped: capping + transfer tables measured slower)
 constexpr int kStageWords = kDecThreads * kSeqBits / 32;
 constexpr int kTailWords = 32;   // look-ahead past the last subsequence (open codewords / varints)
 constexpr int kStageTotal = kWarmBits / 32 + kStageWords + kTailWords + 4;
 __host__ __device__ constexpr int stage_idx(int w) { return w + (w >> 5); }  // one pad word per 32
 constexpr int kStageSmemWords = stage_idx(kStageTotal) + 2;
+constexpr int kSyncStageTotal = kWarmBits / 32 + kSyncThreads * kSeqBits / 32 + kTailWords + 4;
+constexpr int kSyncSmemWords = stage_idx(kSyncStageTotal) + 2;
 
 __device__ __forceinline__ uint32_t lut_len(uint32_t ent) { return (ent >> 8) & 15u; }
 __device__ __forceinline__ uint32_t lut_term(uint32_t ent) { return (ent >> 12) & 1u; }
@@ -132,15 +138,15 @@ __device__ __forceinline__ uint32_t count_to(BitReader& br, const uint16_t* lut,
 // E_{j-1} until consistent.  Subsequence 0 starts at bit 0, so consistency at
 // every boundary (CTA edges: k_huff_fix_s) proves every F_j is a true
 // codeword boundary.
-__global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+__global__ void __launch_bounds__(kSyncThreads) k_huff_sync_s(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                              const uint16_t* __restrict__ lut_g, int maxlen,
                                                              uint64_t nseq, SeqInfo* __restrict__ seq,
                                                              unsigned int* capped) {
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;
-  uint16_t* lut = reinterpret_cast<uint16_t*>(dyn + kStageSmemWords);
-  __shared__ uint32_t sexit[kDecThreads], sstart[kDecThreads];
-  __shared__ int bad[kDecThreads];
+  uint16_t* lut = reinterpret_cast<uint16_t*>(dyn + kSyncSmemWords);
+  __shared__ uint32_t sexit[kSyncThreads], sstart[kSyncThreads];
+  __shared__ int bad[kSyncThreads];
   __shared__ int nbad;
   const int lutn = 1 << maxlen;
   for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_sync_s(const uint32_t* __r
   // desynchronisation outlasts kSyncWarm subsequences (then k_huff_fix_s).
   const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kSyncReal - kSyncWarm;
   const uint64_t base = j0 > 0 ? static_cast<uint64_t>(j0) * kSeqBits - kWarmBits : 0;  // word aligned
-  stage_words(w, nw, base >> 5, sm, kStageTotal);
+  stage_words(w, nw, base >> 5, sm, kSyncStageTotal);
   __syncthreads();
   const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
   const int64_t js = j0 + static_cast<int64_t>(threadIdx.x);

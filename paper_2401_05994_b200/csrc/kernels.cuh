@@ -1016,7 +1016,7 @@ __device__ __forceinline__ uint32_t crc_shift(uint32_t crc, uint64_t nbytes, con
 }
 
 constexpr int kCrcThreads = 256;
-constexpr int kCrcSeg = 256;  // bytes per thread: 16 independent 16-byte loads in flight, then 64 table steps
+constexpr int kCrcSeg = 1024;  // bytes per thread
 
 __global__ void __launch_bounds__(kCrcThreads) k_crc_blocks(const uint8_t* __restrict__ p, uint64_t n,
                                                             const uint32_t* __restrict__ tab_g, CrcConsts K,
@@ -1032,19 +1032,15 @@ __global__ void __launch_bounds__(kCrcThreads) k_crc_blocks(const uint8_t* __res
   uint32_t c = 0xFFFFFFFFu;
   uint64_t i = lo;
   if (hi - lo == kCrcSeg && (reinterpret_cast<uintptr_t>(p + lo) & 15) == 0) {
-    uint4 w[kCrcSeg / 16];
-#pragma unroll
-    for (int k = 0; k < kCrcSeg / 16; ++k) w[k] = __ldg(reinterpret_cast<const uint4*>(p + lo) + k);
-#pragma unroll
-    for (int k = 0; k < kCrcSeg / 16; ++k) {
-      const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+    for (; i < hi; i += 16) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p + i));
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         c ^= ws[j];
         c = tab[3][c & 255] ^ tab[2][(c >> 8) & 255] ^ tab[1][(c >> 16) & 255] ^ tab[0][c >> 24];
       }
     }
-    i = hi;
   }
   for (; i < hi; ++i) c = tab[0][(c ^ p[i]) & 255] ^ (c >> 8);
   scrc[threadIdx.x] = ~c;

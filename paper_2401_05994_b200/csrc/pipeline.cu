@@ -1084,6 +1084,7 @@ ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len) {
 }
 
 static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords) * 4 + (sizeof(uint16_t) << maxlen); }
+static size_t sync_smem(int maxlen) { return static_cast<size_t>(kSyncSmemWords) * 4 + (sizeof(uint16_t) << maxlen); }
 
 static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
 static size_t tf_smem(int maxlen) {
@@ -1094,7 +1095,8 @@ static void huff_smem_optin() {
   static thread_local bool done = false;
   if (done) return;
   const int mx = static_cast<int>(huff_smem(kMaxCodeLen));
-  CK(cudaFuncSetAttribute(k_huff_sync_s, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(k_huff_sync_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(sync_smem(kMaxCodeLen))));
   CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(k_tf_tables, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1289,7 +1291,7 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         prof.begin("huff_sync", static_cast<double>(body_len));
         const uint64_t nblk = (nseq + kSyncReal - 1) / kSyncReal;
         CK(cudaMemsetAsync(&sd->raw_wide, 0, 4, s));  // reused as the "rounds capped" flag
-        k_huff_sync_s<<<static_cast<unsigned>(nblk), kDecThreads, huff_smem(maxlen), s>>>(w, nw, T, lut, maxlen,
+        k_huff_sync_s<<<static_cast<unsigned>(nblk), kSyncThreads, sync_smem(maxlen), s>>>(w, nw, T, lut, maxlen,
                                                                                          nseq, seq, &sd->raw_wide);
         check_launch("k_huff_sync_s");
         // CTA edges: short chains are re-walked serially (two rounds at most) ...

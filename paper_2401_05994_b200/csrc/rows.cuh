@@ -23,6 +23,13 @@
 
 #include "kernels.cuh"
 
+#ifndef MGRC_FINE_MINB
+#define MGRC_FINE_MINB 2  // resident CTAs per SM the fused pass is compiled for
+#endif
+#ifndef MGRC_RECON_MINB
+#define MGRC_RECON_MINB 3
+#endif
+
 namespace mgrc_gpu {
 namespace dev {
 
@@ -691,7 +698,7 @@ struct UnitLoads {
 };
 
 template <int D, typename T, typename Z, class Chk>
-__global__ void __launch_bounds__(kRowThreads, 2) k_fine_warp(GridDev g, RowTiling rt, Widths W, double inv_L,
+__global__ void __launch_bounds__(kRowThreads, MGRC_FINE_MINB) k_fine_warp(GridDev g, RowTiling rt, Widths W, double inv_L,
                                                              const T* __restrict__ u, Z* __restrict__ zz,
                                                              unsigned long long* __restrict__ hist, QuantFlags* flags,
                                                              const double* __restrict__ ec, const Z* __restrict__ zc,
@@ -955,7 +962,7 @@ struct ReconCtx {
 };
 
 template <int D, typename Z, class Out>
-__global__ void __launch_bounds__(kRowThreads, 3) k_recon_warp(GridDev g, RowTiling rt, Widths W,
+__global__ void __launch_bounds__(kRowThreads, MGRC_RECON_MINB) k_recon_warp(GridDev g, RowTiling rt, Widths W,
                                                               const Z* __restrict__ zz, const double* __restrict__ vc,
                                                               Out out, unsigned long long* queue) {
   const int lane = threadIdx.x & 31;
