@@ -1295,8 +1295,12 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
                                                                                          nseq, seq, &sd->raw_wide);
         check_launch("k_huff_sync_s");
         // CTA edges: short chains are re-walked serially (two rounds at most) ...
-        bool pending = false;
-        for (int it = 0; nblk > 1 && it < 2; ++it) {
+        static const int fix_rounds = [] {
+          const char* e = std::getenv("MGRC_FIX_ROUNDS");
+          return e ? std::atoi(e) : 2;
+        }();
+        bool pending = fix_rounds == 0 && nblk > 1;  // no serial edge walks: every bad edge goes to the tables
+        for (int it = 0; nblk > 1 && it < fix_rounds; ++it) {
           CK(cudaMemsetAsync(&sd->fix_changed, 0, 4, s));
           k_huff_fix_s<<<static_cast<unsigned>(nblk - 1), 32, fix_smem(maxlen), s>>>(w, nw, T, lut, maxlen, nseq, seq,
                                                                                   &sd->fix_changed);

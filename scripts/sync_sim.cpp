@@ -154,6 +154,7 @@ int main(int argc, char** argv) {
     const uint64_t nblk = (nseq + REAL - 1) / REAL;
     uint64_t rounds_hist[8] = {0}, total_redo = 0, total_redo_warps = 0, init_sym = 0, bad_edges = 0;
     uint64_t max_rounds = 0, cta_open = 0, sum_rounds = 0;
+    std::vector<int> edge_walk;
     for (uint64_t b = 0; b < nblk; ++b) {
       const int64_t j0 = int64_t(b) * REAL - WARM;
       uint64_t F[NT], E[NT];
@@ -213,14 +214,32 @@ int main(int argc, char** argv) {
       sum_rounds += r;
       rounds_hist[std::min<uint64_t>(r, 7)]++;
       max_rounds = std::max(max_rounds, r);
-      // edge correctness: first published start must be a true boundary
-      if (b > 0 && valid[WARM] && !isb(F[WARM])) ++bad_edges;
+      // edge correctness: first published start must be a true boundary; the
+      // fix walk re-decodes from the true entry until an exit matches
+      if (b > 0 && valid[WARM] && !isb(F[WARM])) {
+        ++bad_edges;
+        uint64_t p = uint64_t(j0 + WARM) * S;
+        while (!isb(p)) ++p;  // true entry (first boundary >= S)
+        int walked = 0;
+        for (int t = WARM; t < NT && valid[t]; ++t) {
+          const uint64_t end = std::min(uint64_t(j0 + t) * S + S, T);
+          while (p < end) { const uint32_t l = len_at(p); if (p + l > T) break; p += l; }
+          ++walked;
+          if (p == E[t]) break;
+        }
+        edge_walk.push_back(walked);
+      }
     }
     std::printf("W=%d: CTAs %llu, init symbols/seq %.1f, redo seqs %llu (%.4f/seq), redo warp-rounds/CTA %.3f, "
                 "max rounds %llu, bad edges %llu, mean rounds %.2f\n  rounds hist:", W, (unsigned long long)nblk, double(init_sym) / nseq,
                 (unsigned long long)total_redo, double(total_redo) / nseq, double(total_redo_warps) / nblk,
                 (unsigned long long)max_rounds, (unsigned long long)bad_edges, double(sum_rounds) / nblk);
     for (int k = 0; k < 8; ++k) std::printf(" %d:%llu", k, (unsigned long long)rounds_hist[k]);
+    std::printf("\n");
+    std::sort(edge_walk.begin(), edge_walk.end());
+    std::printf("  edge walks (subsequences):");
+    for (size_t k = 0; k < edge_walk.size(); k += std::max<size_t>(1, edge_walk.size() / 12)) std::printf(" %d", edge_walk[k]);
+    if (!edge_walk.empty()) std::printf(" max %d", edge_walk.back());
     std::printf("\n");
   }
 }
