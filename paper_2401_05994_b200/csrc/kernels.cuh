@@ -824,8 +824,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const unsigned long lo
 // canonical Huffman code (codec.cpp:399-418, MSB-first, zero padded); codec 1
 // is the same packer with the identity 8-bit code.
 
-constexpr int kPackThreads = 256;
-constexpr int kPackPerThread = 8;
+#ifndef MGRC_PACK_THREADS
+#define MGRC_PACK_THREADS 256
+#endif
+#ifndef MGRC_PACK_PER
+#define MGRC_PACK_PER 16
+#endif
+constexpr int kPackThreads = MGRC_PACK_THREADS;
+constexpr int kPackPerThread = MGRC_PACK_PER;  // a multiple of 4
 constexpr int kPackTile = kPackThreads * kPackPerThread;  // values per tile
 constexpr int kPackMaxWords = kPackTile * 150 / 32 + 2;   // ≤ 10 bytes × 15 bits per value
 
@@ -858,23 +864,27 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ 
   __shared__ uint32_t wsum[kPackThreads / 32];
   __shared__ unsigned long long s_prefix;
   __shared__ uint32_t s_tile;
-  code[threadIdx.x] = code_g[threadIdx.x];
-  len[threadIdx.x] = len_g[threadIdx.x];
+  for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+    code[c] = code_g[c];
+    len[c] = len_g[c];
+  }
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   for (uint32_t w = threadIdx.x; w <= cap_words; w += blockDim.x) words[w] = 0;
   __syncthreads();
   const uint64_t t = s_tile;
   const uint64_t base = t * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
   uint64_t z[kPackPerThread];
-  if (sizeof(Z) == 4 && base + kPackPerThread <= n) {  // 2 x 16-byte loads
-    const uint4 a = __ldg(reinterpret_cast<const uint4*>(zz + base));
-    const uint4 b = __ldg(reinterpret_cast<const uint4*>(zz + base) + 1);
-    z[0] = a.x, z[1] = a.y, z[2] = a.z, z[3] = a.w, z[4] = b.x, z[5] = b.y, z[6] = b.z, z[7] = b.w;
+  if (sizeof(Z) == 4 && base + kPackPerThread <= n) {  // 16-byte loads
+#pragma unroll
+    for (int q = 0; q < kPackPerThread / 4; ++q) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(zz + base) + q);
+      z[4 * q] = a.x, z[4 * q + 1] = a.y, z[4 * q + 2] = a.z, z[4 * q + 3] = a.w;
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < kPackPerThread; ++k) z[k] = base + k < n ? static_cast<uint64_t>(zz[base + k]) : 0;
   }
-  uint32_t mine = 0;  // ≤ 8 values × 150 bits
+  uint32_t mine = 0;  // ≤ kPackPerThread values × 150 bits
 #pragma unroll
   for (int k = 0; k < kPackPerThread; ++k)
     if (base + k < n) mine += varint_bits(z[k], len);
