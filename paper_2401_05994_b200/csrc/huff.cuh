@@ -28,7 +28,11 @@ constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never pub
 constexpr int kSyncThreads = MGRC_SYNC_THREADS;  // subsequences (threads) per sync CTA
 constexpr int kSyncReal = kSyncThreads - kSyncWarm;
 constexpr int kSyncRounds = 1 << 20;  // in-CTA resynchronisation rounds (uncapped: capping + transfer tables measured slower)
-constexpr int kStageWords = kDecThreads * kSeqBits / 32;
+#ifndef MGRC_EMIT_THREADS
+#define MGRC_EMIT_THREADS 128
+#endif
+constexpr int kEmitThreads = MGRC_EMIT_THREADS;  // subsequences (threads) per emit CTA
+constexpr int kStageWords = kEmitThreads * kSeqBits / 32;
 constexpr int kTailWords = 32;   // look-ahead past the last subsequence (open codewords / varints)
 constexpr int kStageTotal = kWarmBits / 32 + kStageWords + kTailWords + 4;
 __host__ __device__ constexpr int stage_idx(int w) { return w + (w >> 5); }  // one pad word per 32
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ 
 // never reads them (codec.cpp:475-481).  Stores are staged per thread in
 // 32-byte aligned chunks and written as 16-byte vectors.
 template <typename Z>
-__global__ void __launch_bounds__(kDecThreads) k_huff_emit_s(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+__global__ void __launch_bounds__(kEmitThreads) k_huff_emit_s(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                              const uint16_t* __restrict__ lut_g, int maxlen,
                                                              uint64_t nseq, const SeqInfo* __restrict__ seq,
                                                              const unsigned long long* __restrict__ term_off,
@@ -316,13 +320,13 @@ __global__ void __launch_bounds__(kDecThreads) k_huff_emit_s(const uint32_t* __r
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;
   uint16_t* lut = reinterpret_cast<uint16_t*>(dyn + kStageSmemWords);
-  __shared__ __align__(16) Z slot[kDecThreads][CH];
+  __shared__ __align__(16) Z slot[kEmitThreads][CH];
   const int lutn = 1 << maxlen;
   for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kDecThreads * kSeqBits;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kEmitThreads * kSeqBits;
   stage_words(w, nw, base >> 5, sm, kStageTotal);
   __syncthreads();
-  const uint64_t j = blockIdx.x * static_cast<uint64_t>(kDecThreads) + threadIdx.x;
+  const uint64_t j = blockIdx.x * static_cast<uint64_t>(kEmitThreads) + threadIdx.x;
   if (j >= nseq) return;
   const SeqInfo s = seq[j];
   bool skipping = j > 0 && seq[j - 1].last_cont;

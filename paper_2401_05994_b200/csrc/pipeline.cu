@@ -1110,7 +1110,7 @@ template <typename Z>
 static void decode_emit(Context& ctx, const uint32_t* w, uint64_t nw, uint64_t T, const uint16_t* lut, int maxlen,
                         uint64_t nseq, const SeqInfo* seq, const unsigned long long* toff, uint64_t N, Z* zz,
                         DecodeStatus* st) {
-  k_huff_emit_s<Z><<<static_cast<unsigned>((nseq + kDecThreads - 1) / kDecThreads), kDecThreads, huff_smem(maxlen),
+  k_huff_emit_s<Z><<<static_cast<unsigned>((nseq + kEmitThreads - 1) / kEmitThreads), kEmitThreads, huff_smem(maxlen),
                      ctx.stream>>>(w, nw, T, lut, maxlen, nseq, seq, toff, N, zz, st);
   check_launch("k_huff_emit_s");
 }
