@@ -43,6 +43,22 @@ constexpr int kSyncSmemWords = stage_idx(kSyncStageTotal) + 2;
 __device__ __forceinline__ uint32_t lut_len(uint32_t ent) { return (ent >> 8) & 15u; }
 __device__ __forceinline__ uint32_t lut_term(uint32_t ent) { return (ent >> 12) & 1u; }
 
+// Decode LUT in shared memory (G = false) or read through L1 from global
+// memory (G = true: long codes, 2^maxlen entries would cost the CTA its
+// occupancy — a 15-bit table is 64 KB).
+template <bool G>
+struct Lut {
+  const uint16_t* p;
+  __device__ __forceinline__ uint32_t operator[](uint32_t i) const {
+    if constexpr (G) return __ldg(p + i);
+    else return p[i];
+  }
+};
+#ifndef MGRC_SMEM_LUT_MAXLEN
+#define MGRC_SMEM_LUT_MAXLEN 12
+#endif
+constexpr int kSmemLutMaxLen = MGRC_SMEM_LUT_MAXLEN;  // longer tables stay in global memory
+
 // Stages words [w0, w0 + nwords) of the stream (zero beyond nw).
 __device__ __forceinline__ void stage_words(const uint32_t* __restrict__ w, uint64_t nw, uint64_t w0, uint32_t* sm,
                                             int nwords) {
@@ -83,7 +99,8 @@ struct BitReader {
 
 // Skip codewords until the first boundary >= target; returns it.  tl: local
 // stream end (a codeword that would run past it stops the walk).
-__device__ __forceinline__ uint32_t walk_to(BitReader& br, const uint16_t* lut, int maxlen, uint32_t p,
+template <class LT>
+__device__ __forceinline__ uint32_t walk_to(BitReader& br, const LT& lut, int maxlen, uint32_t p,
                                             uint32_t target, uint32_t tl) {
   while (p < target) {
     br.refill();
@@ -96,7 +113,8 @@ __device__ __forceinline__ uint32_t walk_to(BitReader& br, const uint16_t* lut, 
 }
 
 // Count codewords / varint terminators starting in [p, end); returns the exit.
-__device__ __forceinline__ uint32_t count_to(BitReader& br, const uint16_t* lut, int maxlen, uint32_t p, uint32_t end,
+template <class LT>
+__device__ __forceinline__ uint32_t count_to(BitReader& br, const LT& lut, int maxlen, uint32_t p, uint32_t end,
                                              uint32_t tl, uint32_t& nterm, uint32_t& last_ent) {
   uint32_t nt = 0, last = 0;
   if (end + 16 <= tl) {  // no codeword can run past the stream end: two symbols per refill
@@ -142,18 +160,21 @@ __device__ __forceinline__ uint32_t count_to(BitReader& br, const uint16_t* lut,
 // E_{j-1} until consistent.  Subsequence 0 starts at bit 0, so consistency at
 // every boundary (CTA edges: k_huff_fix_s) proves every F_j is a true
 // codeword boundary.
+template <bool G>
 __global__ void __launch_bounds__(kSyncThreads) k_huff_sync_s(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                              const uint16_t* __restrict__ lut_g, int maxlen,
                                                              uint64_t nseq, SeqInfo* __restrict__ seq,
                                                              unsigned int* capped) {
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;
-  uint16_t* lut = reinterpret_cast<uint16_t*>(dyn + kSyncSmemWords);
+  uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + kSyncSmemWords);
   __shared__ uint32_t sexit[kSyncThreads], sstart[kSyncThreads];
   __shared__ int bad[kSyncThreads];
   __shared__ int nbad;
   const int lutn = 1 << maxlen;
-  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
+  if (!G)
+    for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut_s[k] = lut_g[k];
+  const Lut<G> lut{G ? lut_g : lut_s};
   // thread t <-> subsequence j = c·kSyncReal - kSyncWarm + t: the first
   // kSyncWarm threads re-decode the predecessor CTA's last subsequences
   // (never published) so that the CTA's first published start is true unless a
@@ -244,7 +265,8 @@ __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ 
                                                    SeqInfo* seq, unsigned int* changed) {
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;
-  uint16_t* lut = reinterpret_cast<uint16_t*>(dyn + stage_idx(kFixWords) + 2);
+  uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + stage_idx(kFixWords) + 2);
+  const Lut<false> lut{lut_s};
   __shared__ int s_go;
   __shared__ unsigned long long s_from;
   const uint64_t b = blockIdx.x + 1;  // edge b: first published subsequence of sync CTA b
@@ -262,7 +284,7 @@ __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ 
     if (!s_go) break;
     if (!lut_ready) {
       const int lutn = 1 << maxlen;
-      for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
+      for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut_s[k] = lut_g[k];
       lut_ready = true;
     }
     const uint64_t base = (s_from >> 5) << 5;
@@ -310,7 +332,7 @@ __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ 
 // Values beyond N (decoded zero padding) are never stored, as the reference
 // never reads them (codec.cpp:475-481).  Stores are staged per thread in
 // 32-byte aligned chunks and written as 16-byte vectors.
-template <typename Z>
+template <typename Z, bool G>
 __global__ void __launch_bounds__(kEmitThreads) k_huff_emit_s(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                              const uint16_t* __restrict__ lut_g, int maxlen,
                                                              uint64_t nseq, const SeqInfo* __restrict__ seq,
@@ -319,10 +341,12 @@ __global__ void __launch_bounds__(kEmitThreads) k_huff_emit_s(const uint32_t* __
   constexpr int CH = 32 / sizeof(Z);  // values per 32-byte chunk
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;
-  uint16_t* lut = reinterpret_cast<uint16_t*>(dyn + kStageSmemWords);
+  uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + kStageSmemWords);
   __shared__ __align__(16) Z slot[kEmitThreads][CH];
   const int lutn = 1 << maxlen;
-  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
+  if (!G)
+    for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut_s[k] = lut_g[k];
+  const Lut<G> lut{G ? lut_g : lut_s};
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kEmitThreads * kSeqBits;
   stage_words(w, nw, base >> 5, sm, kStageTotal);
   __syncthreads();
@@ -459,9 +483,10 @@ __global__ void __launch_bounds__(kTfThreads) k_tf_tables(const uint32_t* __rest
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;                                              // staged words
   uint32_t* maps = sm + stage_idx(kTfStage) + 2;                   // B0 | M0 | B1 | M1 per thread
-  uint16_t* lut = reinterpret_cast<uint16_t*>(maps + 4 * kTfThreads * kTfMapStride);
+  uint16_t* lut_s = reinterpret_cast<uint16_t*>(maps + 4 * kTfThreads * kTfMapStride);
+  const Lut<false> lut{lut_s};
   const int lutn = 1 << maxlen;
-  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut[k] = lut_g[k];
+  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut_s[k] = lut_g[k];
   const uint64_t j0 = j_first + static_cast<uint64_t>(blockIdx.x % kTfCtasPerWin) * kTfThreads;
   if (j0 >= j_first + count) return;
   const uint64_t base = j0 * kSeqBits;

@@ -1083,8 +1083,10 @@ ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len) {
   }
 }
 
-static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords) * 4 + (sizeof(uint16_t) << maxlen); }
-static size_t sync_smem(int maxlen) { return static_cast<size_t>(kSyncSmemWords) * 4 + (sizeof(uint16_t) << maxlen); }
+static bool lut_global(int maxlen) { return maxlen > kSmemLutMaxLen; }
+static size_t lut_smem(int maxlen) { return lut_global(maxlen) ? 0 : (sizeof(uint16_t) << maxlen); }
+static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords) * 4 + lut_smem(maxlen); }
+static size_t sync_smem(int maxlen) { return static_cast<size_t>(kSyncSmemWords) * 4 + lut_smem(maxlen); }
 
 static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
 static size_t tf_smem(int maxlen) {
@@ -1094,11 +1096,14 @@ static size_t tf_smem(int maxlen) {
 static void huff_smem_optin() {
   static thread_local bool done = false;
   if (done) return;
-  const int mx = static_cast<int>(huff_smem(kMaxCodeLen));
-  CK(cudaFuncSetAttribute(k_huff_sync_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(sync_smem(kMaxCodeLen))));
-  CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  const int mx = static_cast<int>(huff_smem(kSmemLutMaxLen));
+  const int ms = static_cast<int>(sync_smem(kSmemLutMaxLen));
+  CK(cudaFuncSetAttribute(k_huff_sync_s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ms));
+  CK(cudaFuncSetAttribute(k_huff_sync_s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ms));
+  CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(k_tf_tables, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(tf_smem(kMaxCodeLen))));
   CK(cudaFuncSetAttribute(k_huff_fix_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1110,8 +1115,13 @@ template <typename Z>
 static void decode_emit(Context& ctx, const uint32_t* w, uint64_t nw, uint64_t T, const uint16_t* lut, int maxlen,
                         uint64_t nseq, const SeqInfo* seq, const unsigned long long* toff, uint64_t N, Z* zz,
                         DecodeStatus* st) {
-  k_huff_emit_s<Z><<<static_cast<unsigned>((nseq + kEmitThreads - 1) / kEmitThreads), kEmitThreads, huff_smem(maxlen),
-                     ctx.stream>>>(w, nw, T, lut, maxlen, nseq, seq, toff, N, zz, st);
+  const unsigned grid = static_cast<unsigned>((nseq + kEmitThreads - 1) / kEmitThreads);
+  if (lut_global(maxlen))
+    k_huff_emit_s<Z, true><<<grid, kEmitThreads, huff_smem(maxlen), ctx.stream>>>(w, nw, T, lut, maxlen, nseq, seq,
+                                                                                 toff, N, zz, st);
+  else
+    k_huff_emit_s<Z, false><<<grid, kEmitThreads, huff_smem(maxlen), ctx.stream>>>(w, nw, T, lut, maxlen, nseq, seq,
+                                                                                  toff, N, zz, st);
   check_launch("k_huff_emit_s");
 }
 
@@ -1291,8 +1301,12 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         prof.begin("huff_sync", static_cast<double>(body_len));
         const uint64_t nblk = (nseq + kSyncReal - 1) / kSyncReal;
         CK(cudaMemsetAsync(&sd->raw_wide, 0, 4, s));  // reused as the "rounds capped" flag
-        k_huff_sync_s<<<static_cast<unsigned>(nblk), kSyncThreads, sync_smem(maxlen), s>>>(w, nw, T, lut, maxlen,
-                                                                                         nseq, seq, &sd->raw_wide);
+        if (lut_global(maxlen))
+          k_huff_sync_s<true><<<static_cast<unsigned>(nblk), kSyncThreads, sync_smem(maxlen), s>>>(
+              w, nw, T, lut, maxlen, nseq, seq, &sd->raw_wide);
+        else
+          k_huff_sync_s<false><<<static_cast<unsigned>(nblk), kSyncThreads, sync_smem(maxlen), s>>>(
+              w, nw, T, lut, maxlen, nseq, seq, &sd->raw_wide);
         check_launch("k_huff_sync_s");
         // CTA edges: short chains are re-walked serially (two rounds at most) ...
         static const int fix_rounds = [] {
