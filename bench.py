@@ -644,8 +644,10 @@ def main():
         single = e2e_measure(mg, u_host, shape, tdt, cap, grid, spec, local, args.steps, 1, world, coll_dev,
                              gather_sizes)
         e2e = single
-        if args.e2e_workers > 1:
-            multi = e2e_measure(mg, u_host, shape, tdt, cap, grid, spec, local, args.steps, args.e2e_workers, world,
+        # concurrent round trips only while their pinned buffers stay modest (cfg4's 8.6 GB field runs one)
+        workers = max(1, min(args.e2e_workers, int(32e9 // (cap + nbytes))))
+        if workers > 1:
+            multi = e2e_measure(mg, u_host, shape, tdt, cap, grid, spec, local, args.steps, workers, world,
                                 coll_dev, gather_sizes)
             multi["single_worker"] = {"value": single["value"], "ms_per_step": single["ms_per_step"]}
             e2e = multi
