@@ -27,7 +27,10 @@ constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never pub
 #endif
 constexpr int kSyncThreads = MGRC_SYNC_THREADS;  // subsequences (threads) per sync CTA
 constexpr int kSyncReal = kSyncThreads - kSyncWarm;
-constexpr int kSyncRounds = 1 << 20;  // in-CTA resynchronisation rounds (uncapped: capping + transfer tables measured slower)
+#ifndef MGRC_SYNC_ROUNDS
+#define MGRC_SYNC_ROUNDS (1 << 20)
+#endif
+constexpr int kSyncRounds = MGRC_SYNC_ROUNDS;  // in-CTA resynchronisation rounds; longer chains go to the tables
 #ifndef MGRC_EMIT_THREADS
 #define MGRC_EMIT_THREADS 128
 #endif
@@ -258,6 +261,10 @@ __global__ void __launch_bounds__(kSyncThreads) k_huff_sync_s(const uint32_t* __
 // unchanged.  *changed tells the host to run another round (an edge fix can
 // change the exit of a CTA's last subsequence, i.e. the next edge).
 constexpr int kFixSeqs = 4;  // subsequences staged per round
+#ifndef MGRC_FIX_WALK
+#define MGRC_FIX_WALK kSyncReal
+#endif
+constexpr int kFixWalk = MGRC_FIX_WALK;  // subsequences one edge walk may rewrite (longer chains go to the tables)
 constexpr int kFixWords = kFixSeqs * kSeqBits / 32 + kTailWords + 4;
 
 __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
@@ -271,7 +278,7 @@ __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ 
   __shared__ unsigned long long s_from;
   const uint64_t b = blockIdx.x + 1;  // edge b: first published subsequence of sync CTA b
   uint64_t j = b * kSyncReal;
-  const uint64_t jend = umin64(j + kSyncReal, nseq);
+  const uint64_t jend = umin64(j + kFixWalk, nseq);
   if (j >= nseq) return;
   bool lut_ready = false;
   while (j < jend) {
@@ -293,6 +300,7 @@ __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ 
     if (threadIdx.x == 0) {
       const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
       uint64_t jj = j;
+      bool conv = false;
       uint32_t from = static_cast<uint32_t>(s_from - base);
       // re-decode up to kFixSeqs subsequences inside the staged window
       for (int r = 0; r < kFixSeqs && jj < jend; ++r, ++jj) {
@@ -314,10 +322,15 @@ __global__ void __launch_bounds__(32) k_huff_fix_s(const uint32_t* __restrict__ 
         __threadfence();
         atomicOr(changed, 1u);
         if (old.exit == s.exit) {  // resynchronised: the rest of the CTA is consistent
-          jj = jend;
+          conv = true;
           break;
         }
         from = ex;
+      }
+      if (conv) {
+        jj = jend;
+      } else if (jj >= jend && jend < umin64((b + 1) * kSyncReal, nseq)) {
+        atomicOr(changed, 2u);  // stopped at the walk cap inside the CTA: the tables take over
       }
       s_from = jj;  // reuse as "next j"
     }
@@ -468,26 +481,28 @@ __device__ __forceinline__ uint32_t tf_terms_before(const uint32_t* Mm, uint32_t
   return c + __popc(Mm[wq] & ((1u << (rel & 31)) - 1u));
 }
 
-constexpr uint64_t kTfWin = 512;  // subsequences per window
-constexpr int kTfCtasPerWin = static_cast<int>(kTfWin) / kTfThreads;
+constexpr uint64_t kTfWin = 512;  // subsequences per window in the first round (later rounds: ×4 per round)
 
-// grid: (window, CTA within the window); window w covers [starts[w], starts[w] + kTfWin) ∩ [0, nseq)
+// grid: (window, CTA within the window); window w covers [starts[w], starts[w] + wlen) ∩ [0, nseq)
+template <bool G>
 __global__ void __launch_bounds__(kTfThreads) k_tf_tables(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                           const uint16_t* __restrict__ lut_g, int maxlen,
                                                           const unsigned long long* __restrict__ starts,
-                                                          uint64_t nseq, TfTab* __restrict__ tabs_all) {
-  const uint64_t win = blockIdx.x / kTfCtasPerWin;
+                                                          uint64_t nseq, TfTab* __restrict__ tabs_all, uint32_t wlen) {
+  const uint32_t ctas_per_win = wlen / kTfThreads;
+  const uint64_t win = blockIdx.x / ctas_per_win;
   const uint64_t j_first = starts[win];
-  const uint64_t count = umin64(kTfWin, nseq - j_first);
-  TfTab* tabs = tabs_all + win * kTfWin;
+  const uint64_t count = umin64(wlen, nseq - j_first);
+  TfTab* tabs = tabs_all + win * wlen;
   extern __shared__ uint32_t dyn[];
   uint32_t* sm = dyn;                                              // staged words
   uint32_t* maps = sm + stage_idx(kTfStage) + 2;                   // B0 | M0 | B1 | M1 per thread
   uint16_t* lut_s = reinterpret_cast<uint16_t*>(maps + 4 * kTfThreads * kTfMapStride);
-  const Lut<false> lut{lut_s};
+  const Lut<G> lut{G ? lut_g : lut_s};
   const int lutn = 1 << maxlen;
-  for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut_s[k] = lut_g[k];
-  const uint64_t j0 = j_first + static_cast<uint64_t>(blockIdx.x % kTfCtasPerWin) * kTfThreads;
+  if (!G)
+    for (int k = threadIdx.x; k < lutn; k += blockDim.x) lut_s[k] = lut_g[k];
+  const uint64_t j0 = j_first + static_cast<uint64_t>(blockIdx.x % ctas_per_win) * kTfThreads;
   if (j0 >= j_first + count) return;
   const uint64_t base = j0 * kSeqBits;
   stage_words(w, nw, base >> 5, sm, kTfStage);
@@ -595,10 +610,11 @@ constexpr int kTfResolveThreads = 512;
 // grid: one CTA per window
 __global__ void __launch_bounds__(kTfResolveThreads) k_tf_resolve(const TfTab* __restrict__ tabs_all,
                                                                   const unsigned long long* __restrict__ starts,
-                                                                  uint64_t nseq, uint64_t T, SeqInfo* seq) {
+                                                                  uint64_t nseq, uint64_t T, SeqInfo* seq,
+                                                                  uint32_t wlen) {
   const uint64_t j_first = starts[blockIdx.x];
-  const uint64_t count = umin64(kTfWin, nseq - j_first);
-  const TfTab* tabs = tabs_all + static_cast<uint64_t>(blockIdx.x) * kTfWin;
+  const uint64_t count = umin64(wlen, nseq - j_first);
+  const TfTab* tabs = tabs_all + static_cast<uint64_t>(blockIdx.x) * wlen;
   __shared__ uint8_t maps[kTfResolveThreads][kTfOffs];
   __shared__ uint8_t tmp[kTfResolveThreads][kTfOffs];
   const int t = threadIdx.x;

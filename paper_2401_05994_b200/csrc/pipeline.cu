@@ -1083,15 +1083,14 @@ ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len) {
   }
 }
 
+static size_t tf_smem_base() { return static_cast<size_t>(stage_idx(kTfStage) + 2 + 4 * kTfThreads * kTfMapStride) * 4; }
 static bool lut_global(int maxlen) { return maxlen > kSmemLutMaxLen; }
 static size_t lut_smem(int maxlen) { return lut_global(maxlen) ? 0 : (sizeof(uint16_t) << maxlen); }
 static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords) * 4 + lut_smem(maxlen); }
 static size_t sync_smem(int maxlen) { return static_cast<size_t>(kSyncSmemWords) * 4 + lut_smem(maxlen); }
+static size_t tf_smem(int maxlen) { return tf_smem_base() + lut_smem(maxlen); }
 
 static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
-static size_t tf_smem(int maxlen) {
-  return static_cast<size_t>(stage_idx(kTfStage) + 2 + 4 * kTfThreads * kTfMapStride) * 4 + (sizeof(uint16_t) << maxlen);
-}
 
 static void huff_smem_optin() {
   static thread_local bool done = false;
@@ -1104,8 +1103,10 @@ static void huff_smem_optin() {
   CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(k_tf_tables, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(tf_smem(kMaxCodeLen))));
+  CK(cudaFuncSetAttribute(k_tf_tables<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(tf_smem(kSmemLutMaxLen))));
+  CK(cudaFuncSetAttribute(k_tf_tables<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(tf_smem(kSmemLutMaxLen))));
   CK(cudaFuncSetAttribute(k_huff_fix_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(fix_smem(kMaxCodeLen))));
   done = true;
@@ -1322,6 +1323,7 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
           CK(cudaMemcpyAsync(&sh->fix_changed, &sd->fix_changed, 4, cudaMemcpyDeviceToHost, s));
           CK(cudaStreamSynchronize(s));
           pending = sh->fix_changed != 0;
+          if (sh->fix_changed & 2u) break;  // a walk hit its cap: the tables resolve the rest
           if (!pending) break;
         }
         // ... long ones (periodic stretches that stay out of phase for megabits) are resolved a window
@@ -1353,21 +1355,28 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
           }
           // non-overlapping windows from every mismatch, all resolved in one pair of launches; windows
           // whose entry is not yet true get rewritten by a later round (the earliest one always is)
+          // a chain still open after a round is long: the windows grow ×4 per round (512 … 32768
+          // subsequences), so a megabit stretch takes a few rounds instead of one per 512 kbit
+          const uint32_t wlen = static_cast<uint32_t>(kTfWin) << (2 * std::min<uint64_t>(guard, 3));
           std::vector<unsigned long long> starts;
           uint64_t covered = 0;
           for (const unsigned long long j : js) {
             if (j < covered) continue;
             starts.push_back(j);
-            covered = j + kTfWin;
+            covered = j + wlen;
           }
           const uint64_t nwin = starts.size();
           auto* st_d = ctx.tfst.get<unsigned long long>(nwin * 8);
           CK(cudaMemcpyAsync(st_d, starts.data(), nwin * 8, cudaMemcpyHostToDevice, s));
-          auto* tabs = ctx.tftab.get<TfTab>(nwin * kTfWin * sizeof(TfTab));
-          k_tf_tables<<<static_cast<unsigned>(nwin * kTfCtasPerWin), kTfThreads, tf_smem(maxlen), s>>>(
-              w, nw, T, lut, maxlen, st_d, nseq, tabs);
+          auto* tabs = ctx.tftab.get<TfTab>(nwin * wlen * sizeof(TfTab));
+          const unsigned tgrid = static_cast<unsigned>(nwin * (wlen / kTfThreads));
+          if (lut_global(maxlen))
+            k_tf_tables<true><<<tgrid, kTfThreads, tf_smem(maxlen), s>>>(w, nw, T, lut, maxlen, st_d, nseq, tabs, wlen);
+          else
+            k_tf_tables<false><<<tgrid, kTfThreads, tf_smem(maxlen), s>>>(w, nw, T, lut, maxlen, st_d, nseq, tabs,
+                                                                           wlen);
           check_launch("k_tf_tables");
-          k_tf_resolve<<<static_cast<unsigned>(nwin), kTfResolveThreads, 0, s>>>(tabs, st_d, nseq, T, seq);
+          k_tf_resolve<<<static_cast<unsigned>(nwin), kTfResolveThreads, 0, s>>>(tabs, st_d, nseq, T, seq, wlen);
           check_launch("k_tf_resolve");
           tf_windows += static_cast<int>(nwin);
         }
