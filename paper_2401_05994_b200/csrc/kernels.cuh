@@ -1019,14 +1019,19 @@ struct CrcConsts {
 };
 
 __device__ __forceinline__ uint32_t crc_shift(uint32_t crc, uint64_t nbytes, const CrcConsts& k) {
-  uint32_t m = 0x80000000u;
+  uint32_t m = 0;
+  bool have = false;  // m = x^(8·nbytes) mod P, built from the set bits (no multiply by the identity)
   for (int b = 0; nbytes; ++b, nbytes >>= 1)
-    if (nbytes & 1) m = gf2_mul(m, k.x8n[b]);
-  return gf2_mul(m, crc);
+    if (nbytes & 1) {
+      m = have ? gf2_mul(m, k.x8n[b]) : k.x8n[b];
+      have = true;
+    }
+  return have ? gf2_mul(m, crc) : crc;
 }
 
 constexpr int kCrcThreads = 256;
 constexpr int kCrcSeg = 1024;  // bytes per thread
+
 
 __global__ void __launch_bounds__(kCrcThreads) k_crc_blocks(const uint8_t* __restrict__ p, uint64_t n,
                                                             const uint32_t* __restrict__ tab_g, CrcConsts K,
@@ -1042,15 +1047,32 @@ __global__ void __launch_bounds__(kCrcThreads) k_crc_blocks(const uint8_t* __res
   uint32_t c = 0xFFFFFFFFu;
   uint64_t i = lo;
   if (hi - lo == kCrcSeg && (reinterpret_cast<uintptr_t>(p + lo) & 15) == 0) {
-    for (; i < hi; i += 16) {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p + i));
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    // four interleaved 256-byte sub-streams (independent chains: 4x the ILP of one
+    // dependent table walk), combined at the end with x^(8*256) = x8n[8]
+    constexpr int kSub = 4, kSubBytes = kCrcSeg / kSub;
+    uint32_t cs[kSub];
+#pragma unroll
+    for (int q = 0; q < kSub; ++q) cs[q] = 0xFFFFFFFFu;
+    for (int off = 0; off < kSubBytes; off += 16) {
+      uint4 wv[kSub];
+#pragma unroll
+      for (int q = 0; q < kSub; ++q) wv[q] = __ldg(reinterpret_cast<const uint4*>(p + lo + q * kSubBytes + off));
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        c ^= ws[j];
-        c = tab[3][c & 255] ^ tab[2][(c >> 8) & 255] ^ tab[1][(c >> 16) & 255] ^ tab[0][c >> 24];
+#pragma unroll
+        for (int q = 0; q < kSub; ++q) {
+          const uint32_t wj = j == 0 ? wv[q].x : j == 1 ? wv[q].y : j == 2 ? wv[q].z : wv[q].w;
+          uint32_t cq = cs[q] ^ wj;
+          cq = tab[3][cq & 255] ^ tab[2][(cq >> 8) & 255] ^ tab[1][(cq >> 16) & 255] ^ tab[0][cq >> 24];
+          cs[q] = cq;
+        }
       }
     }
+    uint32_t acc = ~cs[0];
+#pragma unroll
+    for (int q = 1; q < kSub; ++q) acc = gf2_mul(K.x8n[8], acc) ^ ~cs[q];
+    c = ~acc;  // back to the running-register convention of the tail loop below
+    i = hi;
   }
   for (; i < hi; ++i) c = tab[0][(c ^ p[i]) & 255] ^ (c >> 8);
   scrc[threadIdx.x] = ~c;
