@@ -1015,7 +1015,8 @@ __device__ __forceinline__ uint32_t gf2_mul(uint32_t a, uint32_t b) {
 }
 
 struct CrcConsts {
-  uint32_t x8n[64];  // x^(8·2^k) mod P
+  uint32_t x8n[64];    // x^(8·2^k) mod P
+  uint32_t lanec[32];  // x^(8·16·(31−l)) mod P: lane l's last 16-byte granule to the end of a warp chunk
 };
 
 __device__ __forceinline__ uint32_t crc_shift(uint32_t crc, uint64_t nbytes, const CrcConsts& k) {
@@ -1098,6 +1099,87 @@ __global__ void __launch_bounds__(kCrcThreads) k_crc_blocks(const uint8_t* __res
     blk_crc[blockIdx.x] = scrc[0];
     blk_len[blockIdx.x] = slen[0];
   }
+}
+
+// Coalesced CRC (the main path): the register is GF(2)-linear, so with
+// raw(M) = register after M from 0, raw(A‖B) = raw(A)·x^(8|B|) ⊕ raw(B) and
+// crc(M) = ~(0xFFFFFFFF·x^(8|M|) ⊕ raw(M)).  A warp owns a 16 KB chunk; lane l
+// reads the 16-byte granules l, l+32, … (every load instruction is 512
+// contiguous bytes), folds granule k into acc = acc·x^(8·512) ⊕ raw(granule)
+// with a byte-sliced multiply table, and the lanes' sums are aligned to the
+// chunk end and XOR-reduced.  The last CTA takes the sub-chunk tail (lanes
+// own 512-byte pieces).  Output: raw (crc, len) per CTA for k_crc_fold.
+constexpr int kCrcK = 32;                                   // granules per lane
+constexpr uint64_t kCrcChunk = 32ull * 16 * kCrcK;          // bytes per warp chunk (16 KB = 2^14)
+constexpr int kCrcWarps = 8;
+
+__device__ __forceinline__ uint32_t crc_slice4(const uint32_t (*tab)[256], uint32_t c) {
+  return tab[3][c & 255] ^ tab[2][(c >> 8) & 255] ^ tab[1][(c >> 16) & 255] ^ tab[0][c >> 24];
+}
+
+__global__ void __launch_bounds__(kCrcWarps * 32) k_crc_coal(const uint8_t* __restrict__ p, uint64_t nchunks,
+                                                             uint64_t tail, const uint32_t* __restrict__ tab_g,
+                                                             CrcConsts K, uint32_t* __restrict__ blk_crc,
+                                                             unsigned long long* __restrict__ blk_len) {
+  __shared__ uint32_t tab[4][256], mt[4][256];
+  __shared__ uint32_t wr[kCrcWarps];
+  for (int t = threadIdx.x; t < 1024; t += blockDim.x) {
+    tab[t >> 8][t & 255] = tab_g[t];
+    mt[t >> 8][t & 255] = tab_g[1024 + t];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t nfull = (nchunks + kCrcWarps - 1) / kCrcWarps;  // CTAs over whole chunks
+  if (blockIdx.x >= nfull) {  // the tail [nchunks·16 KB, +tail): warp 0, 512 bytes per lane, bytewise
+    if (warp == 0) {
+      const uint8_t* q = p + nchunks * kCrcChunk;
+      const uint64_t a = umin64(tail, static_cast<uint64_t>(lane) * 512), b = umin64(tail, a + 512);
+      uint32_t c = 0;
+      for (uint64_t i = a; i < b; ++i) c = tab[0][(c ^ q[i]) & 255] ^ (c >> 8);
+      c = crc_shift(c, tail - b, K);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) {
+        blk_crc[blockIdx.x] = c;
+        blk_len[blockIdx.x] = tail;
+      }
+    }
+    return;
+  }
+  const uint64_t chunk = blockIdx.x * static_cast<uint64_t>(kCrcWarps) + warp;
+  uint32_t res = 0;
+  if (chunk < nchunks) {
+    const uint4* g = reinterpret_cast<const uint4*>(p + chunk * kCrcChunk) + lane;
+    uint32_t acc = 0;
+#pragma unroll 8
+    for (int k = 0; k < kCrcK; ++k) {
+      const uint4 w = __ldg(g + 32 * k);
+      uint32_t c = crc_slice4(tab, w.x);
+      c = crc_slice4(tab, c ^ w.y);
+      c = crc_slice4(tab, c ^ w.z);
+      c = crc_slice4(tab, c ^ w.w);
+      acc = crc_slice4(mt, acc) ^ c;  // crc_slice4 over mt = multiply by x^(8·512)
+    }
+    acc = gf2_mul(K.lanec[lane], acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+    res = acc;
+  }
+  if (lane == 0) wr[warp] = res;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t first = blockIdx.x * static_cast<uint64_t>(kCrcWarps);
+    const int nw = static_cast<int>(umin64(kCrcWarps, nchunks - first));
+    uint32_t a = wr[0];
+    for (int i = 1; i < nw; ++i) a = gf2_mul(K.x8n[14], a) ^ wr[i];  // x^(8·2^14): one chunk
+    blk_crc[blockIdx.x] = a;
+    blk_len[blockIdx.x] = static_cast<unsigned long long>(nw) * kCrcChunk;
+  }
+}
+
+// raw(M) -> crc(M) in place (one thread)
+__global__ void k_crc_finish(uint32_t* crc, const unsigned long long* len, CrcConsts K) {
+  crc[0] = ~(crc_shift(0xFFFFFFFFu, len[0], K) ^ crc[0]);
 }
 
 // Folds per-block (crc, len) pairs; iterated until one pair remains.

@@ -642,9 +642,16 @@ static void ensure_crc(Context& ctx) {
   }
   for (uint32_t i = 0; i < 256; ++i)
     for (int t = 1; t < 4; ++t) tab[t][i] = (tab[t - 1][i] >> 8) ^ tab[0][tab[t - 1][i] & 0xFF];
-  uint32_t* d = ctx.crc_tab.get<uint32_t>(sizeof tab);
-  CK(cudaMemcpyAsync(d, tab, sizeof tab, cudaMemcpyHostToDevice, ctx.stream));
+  // [1024, 2048): byte-sliced multiply by x^(8·512) for the coalesced kernel (crc_slice4 order)
+  static uint32_t full[2048];
+  std::memcpy(full, tab, sizeof tab);
+  const uint32_t c512 = crc32_x8n(512);
+  for (int k = 0; k < 4; ++k)
+    for (uint32_t b = 0; b < 256; ++b) full[1024 + (3 - k) * 256 + b] = crc32_mul(b << (8 * k), c512);
+  uint32_t* d = ctx.crc_tab.get<uint32_t>(sizeof full);
+  CK(cudaMemcpyAsync(d, full, sizeof full, cudaMemcpyHostToDevice, ctx.stream));
   crc32_x8n_table(ctx.crc_k.x8n);
+  for (int l = 0; l < 32; ++l) ctx.crc_k.lanec[l] = crc32_x8n(16ull * (31 - l));
   CK(cudaStreamSynchronize(ctx.stream));
   ctx.crc_ready = true;
 }
@@ -661,6 +668,8 @@ static CrcSlot device_crc_launch(Context& ctx, const uint8_t* p, uint64_t n, cud
   if (!cs) cs = ctx.stream;
   const uint64_t per_block = static_cast<uint64_t>(kCrcThreads) * kCrcSeg;
   uint64_t nb = std::max<uint64_t>(1, (n + per_block - 1) / per_block);
+  const bool coal = (reinterpret_cast<uintptr_t>(p) & 15) == 0 && n >= kCrcChunk;
+  if (coal) nb = (n / kCrcChunk + kCrcWarps - 1) / kCrcWarps + ((n % kCrcChunk) ? 1 : 0);
   const size_t cap = ((nb + 1) * (4 + 8) + 1024 + 255) & ~size_t{255};
   uint8_t* A = ctx.crc_a.get<uint8_t>(cap * 2);
   uint32_t* c0 = reinterpret_cast<uint32_t*>(A);
@@ -668,9 +677,16 @@ static CrcSlot device_crc_launch(Context& ctx, const uint8_t* p, uint64_t n, cud
   uint8_t* B = A + cap;
   uint32_t* c1 = reinterpret_cast<uint32_t*>(B);
   unsigned long long* l1 = reinterpret_cast<unsigned long long*>(B + ((4 * (nb + 1) + 15) & ~size_t{15}));
-  k_crc_blocks<<<static_cast<unsigned>(nb), kCrcThreads, 0, cs>>>(p, n, ctx.crc_tab.get<uint32_t>(4096), ctx.crc_k,
-                                                                  c0, l0);
-  check_launch("k_crc_blocks");
+  if (coal) {  // raw (crc, len) pairs, converted by k_crc_finish below
+    const uint64_t nchunks = n / kCrcChunk, tail = n % kCrcChunk;
+    k_crc_coal<<<static_cast<unsigned>(nb), kCrcWarps * 32, 0, cs>>>(p, nchunks, tail, ctx.crc_tab.get<uint32_t>(8192),
+                                                                     ctx.crc_k, c0, l0);
+    check_launch("k_crc_coal");
+  } else {
+    k_crc_blocks<<<static_cast<unsigned>(nb), kCrcThreads, 0, cs>>>(p, n, ctx.crc_tab.get<uint32_t>(8192),
+                                                                    ctx.crc_k, c0, l0);
+    check_launch("k_crc_blocks");
+  }
   while (nb > 1) {
     const uint64_t nb2 = (nb + kCrcThreads - 1) / kCrcThreads;
     k_crc_fold<<<static_cast<unsigned>(nb2), kCrcThreads, 0, cs>>>(c0, l0, nb, ctx.crc_k, c1, l1);
@@ -678,6 +694,10 @@ static CrcSlot device_crc_launch(Context& ctx, const uint8_t* p, uint64_t n, cud
     std::swap(c0, c1);
     std::swap(l0, l1);
     nb = nb2;
+  }
+  if (coal) {
+    k_crc_finish<<<1, 1, 0, cs>>>(c0, l0, ctx.crc_k);
+    check_launch("k_crc_finish");
   }
   return {c0, l0};
 }
