@@ -535,83 +535,13 @@ struct PairCtx {
   }
 };
 
-template <int D, typename T, typename Z, class Chk>
-__global__ void __launch_bounds__(kRowThreads, 3) k_fine_pairs(GridDev g, RowTiling rt, Widths W, double inv_L,
-                                                              const T* __restrict__ u, Z* __restrict__ zz,
-                                                              unsigned long long* __restrict__ hist,
-                                                              QuantFlags* flags, const double* __restrict__ ec,
-                                                              const Z* __restrict__ zc, Chk chk,
-                                                              unsigned long long* __restrict__ red_out) {
-  __shared__ RowMeta meta[kRowMaxR];
-  __shared__ uint32_t sh[256];
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  PairCtx<T, Z, Chk> P;
-  P.g = &g;
-  P.u = u;
-  P.zz = zz;
-  P.ec = ec;
-  P.zc = zc;
-  P.colc4 = reinterpret_cast<const uint4*>(g.ax[D - 1].colc);
-  P.colw = reinterpret_cast<const double2*>(g.ax[D - 1].colw);
-  P.dL = W.w[g.L];
-  P.inv_L = inv_L;
-  P.chk = chk;
-  P.sh = sh;
-  P.hsym = P.hcnt = 0;
-  P.ovf = 0;
-  P.wide = 0;
-  P.red = 0.0;
-  const uint64_t ntiles = ((rt.nrows + rt.R - 1) / rt.R) * rt.ncol_tiles;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t row_tile = tile / rt.ncol_tiles;
-    const uint32_t col_tile = static_cast<uint32_t>(tile - row_tile * rt.ncol_tiles);
-    const uint64_t r0 = row_tile * rt.R;
-    const uint32_t R = static_cast<uint32_t>(umin64(rt.R, rt.nrows - r0));
-    const uint32_t k0 = col_tile * rt.K;  // even (K is n_last or 4096)
-    const uint32_t Kt = min(rt.K, rt.n_last - k0);
-    __syncthreads();
-    build_rows<D>(g, rt, r0, R, meta);
-    __syncthreads();
-    const uint32_t nchunks = (Kt + kUnitCols - 1) / kUnitCols;
-    uint32_t rr = 0, ch = warp;
-    while (ch >= nchunks && rr < R) {
-      ch -= nchunks;
-      ++rr;
-    }
-    for (; rr < R;) {
-      const RowMeta& m = meta[rr];
-      const uint32_t kk = ch * kUnitCols + 2 * lane;
-      if (!m.all_fine) P.template unit<1>(m, k0, kk, Kt, lane);
-      else if (D >= 4 && m.nsub == 8) P.template unit<(D >= 4 ? 8 : 2)>(m, k0, kk, Kt, lane);
-      else if (D >= 3 && m.nsub == 4) P.template unit<(D >= 3 ? 4 : 2)>(m, k0, kk, Kt, lane);
-      else P.template unit<2>(m, k0, kk, Kt, lane);
-      ch += kRowThreads / 32;
-      while (ch >= nchunks && rr < R) {
-        ch -= nchunks;
-        ++rr;
-      }
-    }
-  }
-  hist_flush(sh, P.hsym, P.hcnt);
-  if (P.ovf) atomicAdd(&flags->overflow, P.ovf);
-  if (P.wide) atomicOr(&flags->wide, 1u);
-  if (red_out) {
-    double red = P.red;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) red = fmax(red, __shfl_xor_sync(0xffffffffu, red, o));
-    if (lane == 0 && red > 0.0) atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < 256; t += blockDim.x)
-    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
-}
 
-// Warp-per-row form of the fused pass: a warp owns whole row segments (no
-// CTA barriers), builds the row's corner metadata itself (lane j computes
-// outer corner row j, broadcast by shuffles) and software-pipelines its
-// 64-column units: the gathers of unit i+1 are in flight while unit i is
-// computed.
+// Warp-per-row form of the fused pass: a warp takes row segments from a
+// dynamic queue (no CTA barriers), builds the row's corner metadata itself
+// (lane j computes outer corner row j, broadcast by shuffles), prefetches its
+// next segment of u into L2 and walks the segment in 64-column units.
+// (Keeping the next unit's gathers in registers while one is computed was
+// measured slower: 128 registers and spills.)
 template <int NS>
 struct RowLite {                 // warp-uniform row metadata in registers
   uint64_t uoff[NS], coff[NS];
