@@ -561,7 +561,7 @@ struct FinePairs {
     static void run(cudaStream_t s, const GridDev& g, const RowTiling& rt, const Widths& W, double inv_L, const T* u,
                     Z* zz, unsigned long long* hist, QuantFlags* fl, const double* ec, const Z* zc, const Chk& chk,
                     unsigned long long* red, int blocks) {
-      k_fine_warp<D, T, Z, Chk><<<num_sms() * 2, kRowThreads, 0, s>>>(g, rt, W, inv_L, u, zz, hist, fl, ec, zc, chk,
+      k_fine_warp<D, T, Z, Chk><<<num_sms() * MGRC_FINE_MINB, kFineThreads, 0, s>>>(g, rt, W, inv_L, u, zz, hist, fl, ec, zc, chk,
                                                                        red, &fl->queue);
       check_launch("k_fine_warp");
       (void)blocks;
@@ -600,7 +600,7 @@ struct ReconRows {
                     const double* vc, const Out& out, unsigned long long* queue) {
       if (g.L >= 1) {
         CK(cudaMemsetAsync(queue, 0, 8, s));
-        k_recon_warp<D, Z, Out><<<num_sms() * 3, kRowThreads, 0, s>>>(g, rt, W, zz, vc, out, queue);
+        k_recon_warp<D, Z, Out><<<num_sms() * MGRC_RECON_MINB, kReconThreads, 0, s>>>(g, rt, W, zz, vc, out, queue);
         check_launch("k_recon_warp");
       } else {
         k_recon_rows<D, Z, Out><<<static_cast<unsigned>(row_tiles(rt)), kRowThreads, 0, s>>>(g, rt, W, zz, vc, out);

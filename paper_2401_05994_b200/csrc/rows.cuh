@@ -23,17 +23,29 @@
 
 #include "kernels.cuh"
 
+// CTA shape of the warp-per-row kernels: 128 x 5 (20 warps/SM at <= 102
+// registers) measured best for the fused pass among 64..288 threads x 2..9
+// CTAs (1.09 ms vs 1.30 ms for 256 x 2 on 513^3 f32)
 #ifndef MGRC_FINE_MINB
-#define MGRC_FINE_MINB 2  // resident CTAs per SM the fused pass is compiled for
+#define MGRC_FINE_MINB 5  // resident CTAs per SM the fused pass is compiled for
+#endif
+#ifndef MGRC_FINE_THREADS
+#define MGRC_FINE_THREADS 128
+#endif
+#ifndef MGRC_RECON_THREADS
+#define MGRC_RECON_THREADS 128  // with MGRC_RECON_MINB 7: 28 warps/SM, measured best of 96..256 x 3..8
 #endif
 #ifndef MGRC_RECON_MINB
-#define MGRC_RECON_MINB 3
+#define MGRC_RECON_MINB 7
 #endif
 
 namespace mgrc_gpu {
 namespace dev {
 
 constexpr int kRowThreads = 256;
+constexpr int kFineThreads = MGRC_FINE_THREADS;  // k_fine_warp CTA size
+constexpr int kReconThreads = MGRC_RECON_THREADS;  // k_recon_warp CTA size
+static_assert(kFineThreads % 32 == 0 && kReconThreads % 32 == 0, "whole warps");
 constexpr int kRowTileElems = 4096;  // nodes per CTA (rows × columns)
 constexpr int kRowMaxR = 16;         // rows per CTA
 
@@ -628,7 +640,7 @@ struct UnitLoads {
 };
 
 template <int D, typename T, typename Z, class Chk>
-__global__ void __launch_bounds__(kRowThreads, MGRC_FINE_MINB) k_fine_warp(GridDev g, RowTiling rt, Widths W, double inv_L,
+__global__ void __launch_bounds__(kFineThreads, MGRC_FINE_MINB) k_fine_warp(GridDev g, RowTiling rt, Widths W, double inv_L,
                                                              const T* __restrict__ u, Z* __restrict__ zz,
                                                              unsigned long long* __restrict__ hist, QuantFlags* flags,
                                                              const double* __restrict__ ec, const Z* __restrict__ zc,
@@ -892,7 +904,7 @@ struct ReconCtx {
 };
 
 template <int D, typename Z, class Out>
-__global__ void __launch_bounds__(kRowThreads, MGRC_RECON_MINB) k_recon_warp(GridDev g, RowTiling rt, Widths W,
+__global__ void __launch_bounds__(kReconThreads, MGRC_RECON_MINB) k_recon_warp(GridDev g, RowTiling rt, Widths W,
                                                               const Z* __restrict__ zz, const double* __restrict__ vc,
                                                               Out out, unsigned long long* queue) {
   const int lane = threadIdx.x & 31;
