@@ -532,7 +532,7 @@ struct CoarseQuantRows {
                     double inv, const T* u, double* ec, Z* zc, QuantFlags* fl, unsigned long long* queue) {
       const RowTiling rt = row_tiling(gc);
       CK(cudaMemsetAsync(queue, 0, 8, s));
-      k_cq_warp<D, T, Z><<<num_sms() * 3, kRowThreads, 0, s>>>(g, gc, rt, W, inv, u, ec, zc, fl, queue);
+      k_cq_warp<D, T, Z><<<num_sms() * MGRC_BOX_MINB, kBoxThreads, 0, s>>>(g, gc, rt, W, inv, u, ec, zc, fl, queue);
       check_launch("k_cq_warp");
       k_cq_box<D, T, Z><<<grid_blocks(box2.count, 256), 256, 0, s>>>(g, box2, W, u, ec, zc, fl);
       check_launch("k_cq_box");
@@ -575,7 +575,7 @@ struct InvWarp {
     static void run(cudaStream_t s, const GridDev& g, double* v, unsigned long long* queue) {
       const RowTiling rt = row_tiling(g);
       CK(cudaMemsetAsync(queue, 0, 8, s));
-      k_inv_warp<D><<<num_sms() * 3, kRowThreads, 0, s>>>(g, rt, v, queue);
+      k_inv_warp<D><<<num_sms() * MGRC_BOX_MINB, kBoxThreads, 0, s>>>(g, rt, v, queue);
       check_launch("k_inv_warp");
     }
   };

@@ -38,6 +38,12 @@
 #ifndef MGRC_RECON_MINB
 #define MGRC_RECON_MINB 7
 #endif
+#ifndef MGRC_BOX_THREADS
+#define MGRC_BOX_THREADS 128  // coarse-box row kernels (k_cq_warp, k_inv_warp)
+#endif
+#ifndef MGRC_BOX_MINB
+#define MGRC_BOX_MINB 7
+#endif
 
 namespace mgrc_gpu {
 namespace dev {
@@ -45,7 +51,8 @@ namespace dev {
 constexpr int kRowThreads = 256;
 constexpr int kFineThreads = MGRC_FINE_THREADS;  // k_fine_warp CTA size
 constexpr int kReconThreads = MGRC_RECON_THREADS;  // k_recon_warp CTA size
-static_assert(kFineThreads % 32 == 0 && kReconThreads % 32 == 0, "whole warps");
+constexpr int kBoxThreads = MGRC_BOX_THREADS;
+static_assert(kFineThreads % 32 == 0 && kReconThreads % 32 == 0 && kBoxThreads % 32 == 0, "whole warps");
 constexpr int kRowTileElems = 4096;  // nodes per CTA (rows × columns)
 constexpr int kRowMaxR = 16;         // rows per CTA
 
@@ -1046,7 +1053,7 @@ __device__ __forceinline__ void inv_unit(const GridDev& g, const RowU<NS>& m, do
 }
 
 template <int D>
-__global__ void __launch_bounds__(kRowThreads, 3) k_inv_warp(GridDev g, RowTiling rt, double* v,
+__global__ void __launch_bounds__(kBoxThreads, MGRC_BOX_MINB) k_inv_warp(GridDev g, RowTiling rt, double* v,
                                                             unsigned long long* queue) {
   const int lane = threadIdx.x & 31;
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
@@ -1194,7 +1201,7 @@ __device__ __forceinline__ void cq_unit(const GridDev& g, const GridDev& gc, con
 }
 
 template <int D, typename T, typename Z>
-__global__ void __launch_bounds__(kRowThreads, 3) k_cq_warp(GridDev g, GridDev gc, RowTiling rt, Widths W, double inv,
+__global__ void __launch_bounds__(kBoxThreads, MGRC_BOX_MINB) k_cq_warp(GridDev g, GridDev gc, RowTiling rt, Widths W, double inv,
                                                            const T* __restrict__ u, double* __restrict__ ec,
                                                            Z* __restrict__ zc, QuantFlags* flags,
                                                            unsigned long long* queue) {
