@@ -21,7 +21,10 @@ namespace dev {
 #define MGRC_WARM_BITS 512
 #endif
 constexpr int kWarmBits = MGRC_WARM_BITS;  // warm-up decoded before each subsequence's nominal start
-constexpr int kSyncWarm = 8;     // overlap subsequences per sync CTA (never published)
+#ifndef MGRC_SYNC_WARM
+#define MGRC_SYNC_WARM 16
+#endif
+constexpr int kSyncWarm = MGRC_SYNC_WARM;  // overlap subsequences per sync CTA (never published)
 #ifndef MGRC_SYNC_THREADS
 #define MGRC_SYNC_THREADS 128
 #endif
