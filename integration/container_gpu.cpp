@@ -166,7 +166,7 @@ std::string describe(const ContainerInfo& info) {
   put(&info.codec_id, 1);
   put(&info.payload_len, 8);
   put(&info.checksum, 4);
-  hdr.resize(hdr.size() + info.payload_len, 0);  // parse checks the payload length only
+  // header bytes only: parse_header never reads the payload
   char* text = nullptr;
   check(mgrc_gpu_describe(hdr.data(), hdr.size(), &text));
   std::string s(text);

@@ -176,11 +176,23 @@ def _grid_args(grid: TensorGrid):
     return shape, arr, cs
 
 
+def _check_grid(grid: TensorGrid, shape) -> None:
+    """ShapeMismatch when the grid and the array disagree on the element count (container.cpp:76-77).
+
+    An invalid grid shape is left to the library, which reports InvalidShape / TooManyDims first
+    (make_grid validates before compress ever runs, grid.cpp:20-31) without reading the array."""
+    if not (1 <= len(grid.shape) <= 4) or any(int(n) < 2 for n in grid.shape):
+        return
+    if int(np.prod(grid.shape, dtype=np.uint64)) != int(np.prod(shape, dtype=np.uint64)):
+        raise MgrcError(4, "ShapeMismatch: array does not match the grid")
+
+
 def compress(u, grid: Optional[TensorGrid] = None, spec: Optional[ErrorSpec] = None,
              codec: Codec = Codec.huffman) -> bytes:
     """mgrc::compress (container.hpp:69-74) on the GPU; returns the container bytes."""
     ptr, dt, shape, keep = _array_ptr(u)
     grid = grid or make_grid(shape)
+    _check_grid(grid, shape)
     spec = spec or ErrorSpec(tol=1e-3)
     gshape, coords, ckeep = _grid_args(grid)
     out = P()
@@ -200,6 +212,7 @@ def compress_to(u, dst, grid: Optional[TensorGrid] = None, spec: Optional[ErrorS
     With ``dst=None`` only the length is computed (the container stays staged on the device)."""
     ptr, dt, shape, keep = _array_ptr(u)
     grid = grid or make_grid(shape)
+    _check_grid(grid, shape)
     spec = spec or ErrorSpec(tol=1e-3)
     gshape, coords, ckeep = _grid_args(grid)
     if dst is None:

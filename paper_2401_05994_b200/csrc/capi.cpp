@@ -222,6 +222,44 @@ const void* copy_box(cudaStream_t st, const void* data, size_t unit, int d, cons
   return tmp.p;
 }
 
+// Block `rng` of a HOST array: a pointer into it when the block is contiguous,
+// else the box gathered row by row into `tmp` (write_block's inverse).
+const void* host_box(const void* data, size_t unit, int d, const uint64_t* shape, const std::vector<Range>& rng,
+                     std::vector<uint8_t>& tmp) {
+  uint64_t stride[kMaxDims];
+  stride[d - 1] = 1;
+  for (int a = d - 1; a > 0; --a) stride[a - 1] = stride[a] * shape[a];
+  int first_partial = -1;
+  for (int a = 0; a < d; ++a)
+    if (rng[a].length() != shape[a]) {
+      first_partial = a;
+      break;
+    }
+  bool contiguous = true;
+  for (int a = first_partial + 1; first_partial >= 0 && a < d; ++a)
+    if (rng[a].length() != shape[a]) contiguous = false;
+  uint64_t origin = 0, bcount = 1;
+  for (int a = 0; a < d; ++a) {
+    origin += rng[a].begin * stride[a];
+    bcount *= rng[a].length();
+  }
+  const uint8_t* base = static_cast<const uint8_t*>(data);
+  if (contiguous) return base + origin * unit;
+  tmp.resize(bcount * unit);
+  const uint64_t run = rng[d - 1].length();
+  std::vector<uint64_t> pos(d, 0);
+  for (uint64_t row = 0; row < bcount / run; ++row) {
+    uint64_t off = rng[d - 1].begin;
+    for (int a = 0; a + 1 < d; ++a) off += (rng[a].begin + pos[a]) * stride[a];
+    std::memcpy(tmp.data() + row * run * unit, base + off * unit, run * unit);
+    for (int a = d - 2; a >= 0; --a) {
+      if (++pos[a] < rng[a].length()) break;
+      pos[a] = 0;
+    }
+  }
+  return tmp.data();
+}
+
 }  // namespace
 
 extern "C" {
@@ -445,57 +483,31 @@ int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndims, const uint
       ErrorSpec bspec = spec;
       bspec.mode = Mode::abs;
       const uint64_t count = whole.count();
-      // the whole array on the device once; blocks are cut from it there
       cudaStream_t st = context_stream(ctx);
-      DeviceArray staged;
-      const void* ddata = data;
-      if (!is_device_pointer(data)) {
-        staged.alloc(count * unit);
-        if (cudaMemcpyAsync(staged.p, data, count * unit, cudaMemcpyHostToDevice, st) != cudaSuccess)
-          raise(Errc::cuda, "input upload failed");
-        ddata = staged.p;
-      }
-      if (spec.mode == Mode::rel) {  // global normalisation (tools/mgrc.cpp:405-418)
-        const FieldStats fs = field_stats(ctx, ddata, dt, count);
-        if (fs.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
-        double nrm = fs.max - fs.min;
-        if (spec.norm == Norm::s) {
-          // RMS over the whole array in the CLI's fully serial order (mgrc.cpp:197-233)
-          std::vector<uint8_t> host;
-          const void* src = data;
-          if (is_device_pointer(data)) {
-            host.resize(count * unit);
-            if (cudaMemcpyAsync(host.data(), data, count * unit, cudaMemcpyDeviceToHost, context_stream(ctx)) != cudaSuccess ||
-                cudaStreamSynchronize(context_stream(ctx)) != cudaSuccess)
-              raise(Errc::cuda, "copy failed");
-            src = host.data();
-          }
-          double ss = 0.0;
-          for (uint64_t i = 0; i < count; ++i) {
-            const double v = dt == DType::f32 ? static_cast<double>(static_cast<const float*>(src)[i])
-                                              : static_cast<const double*>(src)[i];
-            ss += v * v;
-          }
-          nrm = std::sqrt(ss / static_cast<double>(count));
-        }
+      const bool on_dev = is_device_pointer(data);
+      if (spec.mode == Mode::rel) {  // global normalisation (tools/mgrc.cpp:405-418, scan_stats :197-233)
+        const GlobalStats gs = global_stats(ctx, data, dt, count, spec.norm == Norm::s);
+        if (gs.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
+        const double nrm = spec.norm == Norm::s ? std::sqrt(gs.sumsq / static_cast<double>(count)) : gs.max - gs.min;
         if (nrm == 0.0) raise(Errc::degenerate_data, "relative bound on a constant file");
         bspec.tol = spec.tol * nrm;
       }
+      // one block at a time (read_block, tools/mgrc.cpp:91-145): device inputs are cut on the device;
+      // host inputs are uploaded block by block, so memory stays bounded by the largest block
       DeviceArray gather;
+      std::vector<uint8_t> hostbox;
       for (uint64_t b = 0; b < nb; ++b) {
         const auto rng = plan.block(b);
         uint64_t bshape[kMaxDims];
         std::vector<double> bc[kMaxDims];
         const double* cptr[kMaxDims];
-        uint64_t bcount = 1;
         for (int a = 0; a < ndims; ++a) {
           bshape[a] = rng[a].length();
-          bcount *= bshape[a];
           bc[a].assign(whole.coords[a].begin() + rng[a].begin, whole.coords[a].begin() + rng[a].end);
           cptr[a] = bc[a].data();
         }
-        const void* bdata = copy_box(st, ddata, unit, ndims, shape, rng, gather);
-        (void)bcount;
+        const void* bdata = on_dev ? copy_box(st, data, unit, ndims, shape, rng, gather)
+                                   : host_box(data, unit, ndims, shape, rng, hostbox);
         const Grid bg = make_grid(ndims, bshape, cptr);
         const ContainerParts parts = compress(ctx, bdata, dt, bg, bspec, cd);
         blocks[b].resize(parts.total());

@@ -471,17 +471,17 @@ std::vector<uint16_t> build_decode_lut(const CodeTable& t) {
 // CRC-32 (IEEE, reflected 0xEDB88320) and GF(2) combination
 
 static const uint32_t* crc_table() {
-  static uint32_t t[256];
-  static bool init = false;
-  if (!init) {
+  // magic static: initialised once, thread-safe (concurrent compress calls share it)
+  static const std::array<uint32_t, 256> t = [] {
+    std::array<uint32_t, 256> a{};
     for (uint32_t i = 0; i < 256; ++i) {
       uint32_t c = i;
       for (int k = 0; k < 8; ++k) c = (c & 1u) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-      t[i] = c;
+      a[i] = c;
     }
-    init = true;
-  }
-  return t;
+    return a;
+  }();
+  return t.data();
 }
 
 uint32_t crc32_host(const uint8_t* p, uint64_t n, uint32_t crc) {
@@ -510,12 +510,11 @@ void crc32_x8n_table(uint32_t* t64) {
 }
 
 uint32_t crc32_x8n(uint64_t nbytes) {
-  static uint32_t t[64];
-  static bool init = false;
-  if (!init) {
-    crc32_x8n_table(t);
-    init = true;
-  }
+  static const std::array<uint32_t, 64> t = [] {
+    std::array<uint32_t, 64> a{};
+    crc32_x8n_table(a.data());
+    return a;
+  }();
   uint32_t p = 0x80000000u;  // 1
   for (int k = 0; nbytes; ++k, nbytes >>= 1)
     if (nbytes & 1) p = crc32_mul(p, t[k]);

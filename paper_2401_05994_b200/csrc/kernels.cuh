@@ -265,14 +265,12 @@ __global__ void __launch_bounds__(128) k_block_sumsq(const T* __restrict__ v, ui
 }
 
 // ---------------------------------------------------------------------------
-// K2: fused forward transform + level-wise quantisation + varint-byte
-// histogram.  One pass over the original array: the forward sweep only ever
-// reads coarse nodes that the sweep has not yet modified (transform.cpp:65-67,
-// L→1), so c(node) = u(node) − I(u)(node) with the node's own tag
-// (SURVEY §0.3).  Quantisation follows quantize.cpp:105-123.
-//   zz[n]   zigzag(q)            (Z = u32 with a "wide" flag, or u64)
-//   r[n]    c − q·δ              (residual, for the a-posteriori check)
-//   hist    256-bin counts of the LEB128 bytes of zz (codec.cpp:445-449)
+// Shared state of the quantising passes (rows.cuh): the forward sweep only
+// ever reads coarse nodes that it has not yet modified (transform.cpp:65-67,
+// L→1), so c(node) = u(node) − I(u)(node) with the node's own tag (SURVEY
+// §0.3); quantisation follows quantize.cpp:105-123; codes are stored as
+// zigzag(q) (Z = u32 with a "wide" flag, or u64) and the LEB128 bytes of
+// zigzag(q) are histogrammed for the codebook (codec.cpp:445-449).
 struct QuantFlags {
   unsigned long long overflow;  // |c/δ| ≥ 2^63 (quantize.cpp:113-116)
   unsigned int wide;            // some zz does not fit the u32 store
@@ -306,72 +304,6 @@ __device__ __forceinline__ void hist_varint(uint32_t* sh, uint64_t z, uint32_t& 
   }
 }
 
-template <int D, typename T, typename Z>
-__global__ void __launch_bounds__(256) k_forward_quant(GridDev g, Widths W, const T* __restrict__ u,
-                                                       Z* __restrict__ zz, double* __restrict__ r,
-                                                       unsigned long long* __restrict__ hist, QuantFlags* flags,
-                                                       int vec_ok) {
-  __shared__ uint32_t sh[256];
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
-  __syncthreads();
-  uint32_t hsym = 0, hcnt = 0;
-  unsigned long long ovf = 0;
-  unsigned wide = 0;
-  auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
-  const uint64_t nruns = (g.N + 3) / 4;
-  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t run = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; run < nruns; run += step) {
-    const uint64_t e0 = run * 4;
-    const int cnt = static_cast<int>(umin64(4, g.N - e0));
-    uint32_t i[4] = {0, 0, 0, 0};
-    decompose<D>(g, e0, i);
-    double cv[4] = {0, 0, 0, 0};
-    if (cnt == 4 && vec_ok) {
-      load4<T>(u + e0, cv);
-    } else {
-      for (int k = 0; k < cnt; ++k) cv[k] = static_cast<double>(u[e0 + k]);
-    }
-    uint64_t zv[4] = {0, 0, 0, 0};
-    double rv[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < cnt) {
-        const int tag = node_tag<D>(g, i);
-        double c = cv[k];
-        if (tag > 0) c = __dsub_rn(c, interp<D>(g, i, tag, ld));
-        const double delta = W.w[tag];
-        const double scaled = __ddiv_rn(c, delta);
-        if (!(fabs(scaled) < 9223372036854775808.0)) {
-          ++ovf;
-        } else {
-          const long long q = __double2ll_rn(scaled);
-          rv[k] = __dsub_rn(c, __dmul_rn(__ll2double_rn(q), delta));
-          const uint64_t z = zigzag(q);
-          if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
-          zv[k] = z;
-          hist_varint(sh, z, hsym, hcnt);
-        }
-        advance<D>(g, i);
-      }
-    }
-    if (cnt == 4 && vec_ok) {
-      store4z(zz + e0, zv);
-      store4(r + e0, rv);
-    } else {
-      for (int k = 0; k < cnt; ++k) {
-        zz[e0 + k] = static_cast<Z>(zv[k]);
-        r[e0 + k] = rv[k];
-      }
-    }
-  }
-  hist_flush(sh, hsym, hcnt);
-  if (ovf) atomicAdd(&flags->overflow, ovf);
-  if (wide) atomicOr(&flags->wide, 1u);
-  __syncthreads();
-  for (int t = threadIdx.x; t < 256; t += blockDim.x)
-    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
-}
-
 // ---------------------------------------------------------------------------
 // Inverse transform, coarse → fine (transform.cpp:155-159).  Level l ≥ 1
 // touches only nodes tagged l and reads only nodes of lower tag, which are
@@ -382,15 +314,6 @@ __global__ void __launch_bounds__(256) k_forward_quant(GridDev g, Widths W, cons
 struct SrcResidual {
   const double* r;
   __device__ __forceinline__ double operator()(uint64_t n, int) const { return r[n]; }
-};
-
-template <typename Z>
-struct SrcDequant {
-  const Z* zz;
-  Widths W;
-  __device__ __forceinline__ double operator()(uint64_t n, int tag) const {
-    return __dmul_rn(__ll2double_rn(unzigzag(static_cast<uint64_t>(zz[n]))), W.w[tag]);
-  }
 };
 
 // Box pass for level l < L (and level 0): enumerates the level-l box with
@@ -416,194 +339,6 @@ __global__ void __launch_bounds__(256) k_inverse_box(GridDev g, BoxDev box, int 
     double val = src(n, l);
     if (l > 0) val = __dadd_rn(val, interp<D>(g, i, l, ld));
     v[n] = val;
-  }
-}
-
-// Epilogues of the finest pass.
-struct EpiMaxAbs {  // max|e| (error_control.cpp:105, exec.cpp:75-87)
-  double* dummy;
-  __device__ __forceinline__ void operator()(uint64_t, double e, double& red) const { red = fmax(red, fabs(e)); }
-};
-template <typename T>
-struct EpiCastMaxAbs {  // f32 bound on the cast-back output (container.cpp:96-107)
-  const T* src;
-  __device__ __forceinline__ void operator()(uint64_t n, double e, double& red) const {
-    const double s = static_cast<double>(src[n]);
-    const double ce = __dsub_rn(s, static_cast<double>(__double2float_rn(__dsub_rn(s, e))));
-    red = fmax(red, fabs(ce));
-  }
-};
-struct EpiStore64 {  // e (S(0) check) or decompressed f64 values
-  double* out;
-  __device__ __forceinline__ void operator()(uint64_t n, double e, double&) const { out[n] = e; }
-};
-template <typename T>
-struct EpiCastStore {  // f32 cast error, stored for the ordered RMS
-  const T* src;
-  double* out;
-  __device__ __forceinline__ void operator()(uint64_t n, double e, double&) const {
-    const double s = static_cast<double>(src[n]);
-    out[n] = __dsub_rn(s, static_cast<double>(__double2float_rn(__dsub_rn(s, e))));
-  }
-};
-struct EpiNarrow32 {  // decompressed f32 values (container.cpp:252-256)
-  float* out;
-  __device__ __forceinline__ void operator()(uint64_t n, double e, double&) const { out[n] = __double2float_rn(e); }
-};
-
-// Finest pass over the whole grid: nodes tagged L are reconstructed from
-// their source value plus the interpolation of the (final) coarse values,
-// coarser nodes are read back; the epilogue consumes every node's final
-// value (reduction, cast, narrowing).  With L == 0 every node is level 0.
-// SKIP_COARSE: the epilogue does not need coarse nodes (in-place f64 output).
-template <int D, class Src, class Epi, bool SKIP_COARSE>
-__global__ void __launch_bounds__(256) k_inverse_finest(GridDev g, Src src, const double* v, Epi epi,
-                                                        unsigned long long* red_out) {
-  auto ld = [v](uint64_t off) { return v[off]; };
-  double red = 0.0;
-  const uint64_t nruns = (g.N + 3) / 4;
-  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t run = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; run < nruns; run += step) {
-    const uint64_t e0 = run * 4;
-    const int cnt = static_cast<int>(umin64(4, g.N - e0));
-    uint32_t i[4] = {0, 0, 0, 0};
-    decompose<D>(g, e0, i);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < cnt) {
-        const uint64_t n = e0 + k;
-        if (g.L == 0) {
-          epi(n, src(n, 0), red);
-        } else {
-          const int tag = node_tag<D>(g, i);
-          if (tag == g.L) {
-            epi(n, __dadd_rn(src(n, tag), interp<D>(g, i, tag, ld)), red);
-          } else if (!SKIP_COARSE) {
-            epi(n, v[n], red);
-          }
-        }
-        advance<D>(g, i);
-      }
-    }
-  }
-  if (red_out) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) red = fmax(red, __shfl_xor_sync(0xffffffffu, red, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
-  }
-}
-
-// Level-weighted residual aggregate for S(s≠0) (error_control.cpp:72-100):
-// Σ_n 2^{2s(tag−L)}·r² — deterministic fixed-order tree, not the reference's
-// serial sum (documented: the estimator is uncertified and only drives the
-// accept decision; it is never stored).
-template <int D>
-__global__ void __launch_bounds__(256) k_level_weighted(GridDev g, Widths lw, const double* __restrict__ r,
-                                                        double* __restrict__ partials) {
-  __shared__ double sh[256];
-  double acc = 0.0;
-  const uint64_t chunk = (g.N + gridDim.x - 1) / gridDim.x;
-  const uint64_t lo = blockIdx.x * chunk, hi = min(lo + chunk, g.N);
-  for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-    uint32_t i[4] = {0, 0, 0, 0};
-    decompose<D>(g, e, i);
-    const double x = r[e];
-    acc = __dadd_rn(acc, __dmul_rn(lw.w[node_tag<D>(g, i)], __dmul_rn(x, x)));
-  }
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int s = 128; s; s >>= 1) {
-    if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
-}
-
-// ---------------------------------------------------------------------------
-// Compress, v2: the a-posteriori check without a full residual array.
-//
-// The inverse of the residuals (container.cpp:96-110, error_control.cpp:103)
-// only needs e on the coarse box (tag < L, 1/2^d of the grid) before the
-// finest level: e(tag L node) = r + I(e)(node), and every corner of a tag-L
-// node lies in the coarse box.  So
-//   (a) k_coarse_resid   r on the coarse box, compact (Nc doubles)
-//   (b) inverse levels 1..L-1 on the compact box (k_inverse_box/finest on the
-//       compact GridDev), in place: ec = e on the coarse box
-//   (c) k_fine           ONE pass over u: forward + quantise + zigzag store +
-//       varint histogram + e = r + I(ec) (or ec) + the check epilogue.
-// The residual array of v1 (8 B/elt written and read back) disappears.
-
-__device__ __forceinline__ uint64_t coarse_index(const GridDev& g, const uint32_t (&i)[4], int D) {
-  uint64_t o = 0;
-  for (int a = 0; a < D; ++a) o += static_cast<uint64_t>(__ldg(g.ax[a].cpos + i[a])) * g.cstride[a];
-  return o;
-}
-
-// interp() of a tag-L node over the compact coarse box (same corner order).
-template <int D>
-__device__ __forceinline__ double interp_coarse(const GridDev& g, const uint32_t (&i)[4], int tag,
-                                                const double* __restrict__ ec) {
-  uint32_t F = 0;
-  uint64_t base = 0;
-  double wl[D], wr[D];
-  uint64_t ol[D], orr[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    wl[a] = wr[a] = 0.0;
-    ol[a] = orr[a] = 0;
-    if (__ldg(g.ax[a].lvl + i[a]) == tag) {
-      F |= 1u << a;
-      wl[a] = __ldg(g.ax[a].wl + i[a]);
-      wr[a] = __ldg(g.ax[a].wr + i[a]);
-      ol[a] = static_cast<uint64_t>(__ldg(g.ax[a].cl + i[a])) * g.cstride[a];
-      orr[a] = static_cast<uint64_t>(__ldg(g.ax[a].cr + i[a])) * g.cstride[a];
-    } else {
-      base += static_cast<uint64_t>(__ldg(g.ax[a].cpos + i[a])) * g.cstride[a];
-    }
-  }
-  double acc = 0.0;
-  uint32_t s = 0;
-  do {
-    double w = 1.0;
-    uint64_t off = base;
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-      if ((F >> a) & 1u) {
-        const bool right = (s >> a) & 1u;
-        w = __dmul_rn(w, right ? wr[a] : wl[a]);
-        off += right ? orr[a] : ol[a];
-      }
-    acc = __dadd_rn(acc, __dmul_rn(w, ec[off]));
-    s = (s - F) & F;
-  } while (s);
-  return acc;
-}
-
-// (a) residuals of the coarse-box nodes, compact layout.
-template <int D, typename T>
-__global__ void __launch_bounds__(256) k_coarse_resid(GridDev g, Widths W, const T* __restrict__ u,
-                                                      double* __restrict__ ec) {
-  auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
-  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < g.Nc; j += step) {
-    uint32_t i[4] = {0, 0, 0, 0};
-    uint64_t q = j, n = 0;
-#pragma unroll
-    for (int a = D - 1; a >= 0; --a) {
-      const uint64_t qq = q / g.cshape[a];
-      i[a] = __ldg(g.ax[a].cset + (q - qq * g.cshape[a]));
-      n += static_cast<uint64_t>(i[a]) * g.stride[a];
-      q = qq;
-    }
-    const int tag = node_tag<D>(g, i);
-    double c = static_cast<double>(u[n]);
-    if (tag > 0) c = __dsub_rn(c, interp<D>(g, i, tag, ld));
-    const double delta = W.w[tag];
-    const double scaled = __ddiv_rn(c, delta);
-    double r = 0.0;
-    if (fabs(scaled) < 9223372036854775808.0)
-      r = __dsub_rn(c, __dmul_rn(__ll2double_rn(__double2ll_rn(scaled)), delta));
-    ec[j] = r;
   }
 }
 
@@ -644,95 +379,6 @@ struct ChkLevelWeighted {
   static constexpr bool kNeedsE = true;  // S(s≠0): Σ 2^{2s(tag−L)} r² (error_control.cpp:72-100), r passed as e
   __device__ __forceinline__ void operator()(uint64_t, double, double, double&) const {}
 };
-
-// (c) the fused pass.  LW: level-weighted estimator (no inverse needed).
-template <int D, typename T, typename Z, class Chk, bool LW>
-__global__ void __launch_bounds__(256) k_fine(GridDev g, Widths W, const T* __restrict__ u, Z* __restrict__ zz,
-                                              unsigned long long* __restrict__ hist, QuantFlags* flags,
-                                              const double* __restrict__ ec, Chk chk,
-                                              unsigned long long* __restrict__ red_out, Widths lw,
-                                              double* __restrict__ partials, int vec_ok) {
-  __shared__ uint32_t sh[256];
-  __shared__ double sred[256 / 32];
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
-  __syncthreads();
-  uint32_t hsym = 0, hcnt = 0;
-  unsigned long long ovf = 0;
-  unsigned wide = 0;
-  double red = 0.0;
-  auto ld = [u](uint64_t off) { return static_cast<double>(__ldg(u + off)); };
-  const uint64_t nruns = (g.N + 3) / 4;
-  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t run = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; run < nruns; run += step) {
-    const uint64_t e0 = run * 4;
-    const int cnt = static_cast<int>(umin64(4, g.N - e0));
-    uint32_t i[4] = {0, 0, 0, 0};
-    decompose<D>(g, e0, i);
-    double cv[4] = {0, 0, 0, 0};
-    if (cnt == 4 && vec_ok) {
-      load4<T>(u + e0, cv);
-    } else {
-      for (int k = 0; k < cnt; ++k) cv[k] = static_cast<double>(u[e0 + k]);
-    }
-    uint64_t zv[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < cnt) {
-        const int tag = node_tag<D>(g, i);
-        double c = cv[k];
-        if (tag > 0) c = __dsub_rn(c, interp<D>(g, i, tag, ld));
-        const double delta = W.w[tag];
-        const double scaled = __ddiv_rn(c, delta);
-        double r = 0.0;
-        if (!(fabs(scaled) < 9223372036854775808.0)) {
-          ++ovf;
-        } else {
-          const long long q = __double2ll_rn(scaled);
-          r = __dsub_rn(c, __dmul_rn(__ll2double_rn(q), delta));
-          const uint64_t z = zigzag(q);
-          if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
-          zv[k] = z;
-          hist_varint(sh, z, hsym, hcnt);
-        }
-        if (LW) {
-          red = __dadd_rn(red, __dmul_rn(lw.w[tag], __dmul_rn(r, r)));
-        } else {
-          double e;
-          if (g.L == 0) e = r;
-          else if (tag == g.L) e = __dadd_rn(r, interp_coarse<D>(g, i, tag, ec));
-          else e = ec[coarse_index(g, i, D)];
-          chk(e0 + k, e, cv[k], red);
-        }
-        advance<D>(g, i);
-      }
-    }
-    if (cnt == 4 && vec_ok) {
-      store4z(zz + e0, zv);
-    } else {
-      for (int k = 0; k < cnt; ++k) zz[e0 + k] = static_cast<Z>(zv[k]);
-    }
-  }
-  hist_flush(sh, hsym, hcnt);
-  if (ovf) atomicAdd(&flags->overflow, ovf);
-  if (wide) atomicOr(&flags->wide, 1u);
-  if (LW) {  // fixed-order block sum → partials[block] (deterministic for a fixed grid)
-#pragma unroll
-    for (int o = 16; o; o >>= 1) red = __dadd_rn(red, __shfl_down_sync(0xffffffffu, red, o));
-    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = red;
-  } else if (red_out) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) red = fmax(red, __shfl_xor_sync(0xffffffffu, red, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(red_out, static_cast<unsigned long long>(__double_as_longlong(red)));
-  }
-  __syncthreads();
-  if (LW && threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 256 / 32; ++w) t = __dadd_rn(t, sred[w]);
-    partials[blockIdx.x] = t;
-  }
-  for (int t = threadIdx.x; t < 256; t += blockDim.x)
-    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
-}
 
 // ---------------------------------------------------------------------------
 // Decoupled look-back (single-pass prefix) helpers.  A tile publishes

@@ -1,15 +1,19 @@
 // Host orchestration of the sm_100a compress / decompress path.
 //
 //  compress   (container.cpp:71-131)
-//    K1  k_stats              non-finite / min / max  (+ k_block_sumsq for S-REL)
-//    K2  k_forward_quant      forward transform + quantise + varint histogram
-//    K3  k_inverse_box/finest a-posteriori error of the residuals (shrink loop)
-//    K4  (host)               Huffman lengths + canonical codes (256 symbols)
-//    K5  k_pack_lb/k_pack_edges  single-pass look-back bit packing (MSB-first)
-//    K5b k_crc_blocks/fold    CRC-32 of the payload
+//    K1  k_stats (+ k_block_sumsq for S-REL)    non-finite / min / max (Σu²)
+//    K2a k_cq_warp + k_cq_box                   r and codes of the coarse box (tag < L)
+//    K2b k_inverse_box + k_inv_warp             a-posteriori inverse on the coarse box
+//    K2c k_fine_warp / k_fine_rows              ONE pass over u: forward + quantise +
+//                                               zigzag store + varint histogram + check
+//    host                                       accept / halve δ (≤ 10 passes)
+//    K4  host                                   Huffman lengths + canonical codes
+//    K5  k_pack_lb + k_pack_edges               single-pass look-back bit packing
+//    K5b k_crc_coal / k_crc_fold / k_crc_finish CRC-32 of the payload
 //  decompress (container.cpp:210-261)
-//    CRC → k_huff_sync/fix (self-synchronising decode) → k_huff_emit
-//    → k_inverse_box (levels 0..L-1, dequantised) → k_inverse_finest (+narrow)
+//    K5b CRC (auxiliary stream) → K6 k_huff_sync_s / k_huff_fix_s / k_tf_* (self-
+//    synchronising decode) → k_seq_counts + k_scan_lb → k_huff_emit_s → K7
+//    k_recon_coarse + k_inverse_box + k_inv_warp (coarse box) → k_recon_warp (+narrow)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,6 +30,7 @@
 #include "kernels.cuh"
 #include "rows.cuh"
 #include "huff.cuh"
+#include "serial_sum.cuh"
 #include "pipeline.hpp"
 
 namespace mgrc_gpu {
@@ -128,6 +133,7 @@ struct Scratch {  // small device-side results read back at sync points
   unsigned int raw_wide;
   unsigned long long hist[256];
   unsigned long long queues[4];  // dynamic work queues of the row kernels (zeroed per launch)
+  double ssum;                   // running value of the exact serial sum
 };
 
 class Context {
@@ -138,10 +144,12 @@ class Context {
   bool profiling = false;
   std::vector<PhaseTime> profile;
   // workspace
+  DevBuf ssmaps;
+  PinnedBuf ssmaps_h;
   DevBuf in, zz, zc, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws, tfst, tftab;
   DevBuf scratch_d;
   PinnedBuf scratch_h, partial_h;
-  std::unique_ptr<DevHier> hier;
+  std::vector<std::unique_ptr<DevHier>> hiers;  // most recently used first (chunked slabs alternate shapes)
   cudaStream_t aux = nullptr;            // concurrent side work (decompress CRC)
   cudaEvent_t ev_in = nullptr, ev_crc = nullptr;
   CrcConsts crc_k{};
@@ -235,9 +243,7 @@ static int num_sms() {
 }
 
 static int grid_blocks(uint64_t work_items, int threads, int per_sm = 8) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = num_sms();
   const uint64_t need = (work_items + threads - 1) / threads;
   return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(need, static_cast<uint64_t>(sms) * per_sm)));
 }
@@ -254,7 +260,11 @@ static std::string hier_key(const Grid& g) {
 
 static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
   const std::string key = hier_key(grid);
-  if (ctx.hier && ctx.hier->key == key) return *ctx.hier;
+  for (size_t i = 0; i < ctx.hiers.size(); ++i)
+    if (ctx.hiers[i]->key == key) {
+      std::rotate(ctx.hiers.begin(), ctx.hiers.begin() + i, ctx.hiers.begin() + i + 1);
+      return *ctx.hiers[0];
+    }
   auto dh = std::make_unique<DevHier>();
   dh->key = key;
   dh->h = build_hierarchy(grid);
@@ -410,8 +420,10 @@ static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
       }
     }
   }
-  ctx.hier = std::move(dh);
-  return *ctx.hier;
+  constexpr size_t kHierCache = 4;
+  if (ctx.hiers.size() >= kHierCache) ctx.hiers.pop_back();
+  ctx.hiers.insert(ctx.hiers.begin(), std::move(dh));
+  return *ctx.hiers[0];
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -437,19 +449,6 @@ static void by_dim(int d, Args&&... args) {
   }
 }
 
-template <typename T, typename Z>
-struct FwdQuant {
-  template <int D>
-  struct L {
-    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const T* u, Z* zz, double* r,
-                    unsigned long long* hist, QuantFlags* fl, int vec) {
-      const int blocks = grid_blocks((g.N + 3) / 4, 256);
-      k_forward_quant<D, T, Z><<<blocks, 256, 0, s>>>(g, W, u, zz, r, hist, fl, vec);
-      check_launch("k_forward_quant");
-    }
-  };
-};
-
 template <class Src>
 struct InvBox {
   template <int D>
@@ -458,43 +457,6 @@ struct InvBox {
       const int blocks = grid_blocks(b.count, 256);
       k_inverse_box<D, Src><<<blocks, 256, 0, s>>>(g, b, l, src, v);
       check_launch("k_inverse_box");
-    }
-  };
-};
-
-template <class Src, class Epi, bool SKIP>
-struct InvFinest {
-  template <int D>
-  struct L {
-    static void run(cudaStream_t s, const GridDev& g, const Src& src, const double* v, const Epi& epi,
-                    unsigned long long* red) {
-      const int blocks = grid_blocks((g.N + 3) / 4, 256);
-      k_inverse_finest<D, Src, Epi, SKIP><<<blocks, 256, 0, s>>>(g, src, v, epi, red);
-      check_launch("k_inverse_finest");
-    }
-  };
-};
-
-template <typename T>
-struct CoarseResid {
-  template <int D>
-  struct L {
-    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const T* u, double* ec) {
-      k_coarse_resid<D, T><<<grid_blocks(g.Nc, 256), 256, 0, s>>>(g, W, u, ec);
-      check_launch("k_coarse_resid");
-    }
-  };
-};
-
-template <typename T, typename Z, class Chk, bool LW>
-struct Fine {
-  template <int D>
-  struct L {
-    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const T* u, Z* zz,
-                    unsigned long long* hist, QuantFlags* fl, const double* ec, const Chk& chk,
-                    unsigned long long* red, const Widths& lw, double* partials, int blocks, int vec) {
-      k_fine<D, T, Z, Chk, LW><<<blocks, 256, 0, s>>>(g, W, u, zz, hist, fl, ec, chk, red, lw, partials, vec);
-      check_launch("k_fine");
     }
   };
 };
@@ -610,25 +572,6 @@ struct ReconRows {
   };
 };
 
-struct LevelWeighted {
-  template <int D>
-  struct L {
-    static void run(cudaStream_t s, const GridDev& g, const Widths& lw, const double* r, double* partials,
-                    int blocks) {
-      k_level_weighted<D><<<blocks, 256, 0, s>>>(g, lw, r, partials);
-      check_launch("k_level_weighted");
-    }
-  };
-};
-
-// Coarse levels 1..L-1 of the inverse (level 0 is the identity on the
-// residual buffer / handled by the caller for decompress).
-template <class Src>
-static void inverse_coarse_levels(Context& ctx, DevHier& dh, const Src& src, double* v, int first_level) {
-  for (int l = first_level; l < dh.h.L; ++l)
-    by_dim<InvBox<Src>::template L>(dh.g.d, ctx.stream, dh.g, dh.boxes[l], l, src, v);
-}
-
 // ---------------------------------------------------------------------------
 // CRC of a device byte range
 
@@ -643,7 +586,7 @@ static void ensure_crc(Context& ctx) {
   for (uint32_t i = 0; i < 256; ++i)
     for (int t = 1; t < 4; ++t) tab[t][i] = (tab[t - 1][i] >> 8) ^ tab[0][tab[t - 1][i] & 0xFF];
   // [1024, 2048): byte-sliced multiply by x^(8·512) for the coalesced kernel (crc_slice4 order)
-  static uint32_t full[2048];
+  uint32_t full[2048];  // local: alive until the synchronize below
   std::memcpy(full, tab, sizeof tab);
   const uint32_t c512 = crc32_x8n(512);
   for (int k = 0; k < 4; ++k)
@@ -720,19 +663,90 @@ static double key_to_double(unsigned long long k) {
   return d;
 }
 
-// Serial sum of 4096-block partials (exec.cpp:68-70).
+// ---------------------------------------------------------------------------
+// Exact serial double sums on the device (serial_sum.cuh)
+
+template <typename T, bool SQ>
+static double exact_serial_sum_t(Context& ctx, const T* v, uint64_t n, double s0) {
+  cudaStream_t s = ctx.stream;
+  Scratch* sd = ctx.sd();
+  Scratch* sh = ctx.sh();
+  double acc = s0;
+  auto serial = [&](uint64_t a, uint64_t b) {  // one thread continues the sum over [a, b)
+    sh->ssum = acc;
+    CK(cudaMemcpyAsync(&sd->ssum, &sh->ssum, 8, cudaMemcpyHostToDevice, s));
+    k_ss_serial<T, SQ><<<1, 32, 0, s>>>(v, a, b, &sd->ssum);
+    check_launch("k_ss_serial");
+    CK(cudaMemcpyAsync(&sh->ssum, &sd->ssum, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    acc = sh->ssum;
+  };
+  constexpr uint64_t kB = kSsBlock;
+  constexpr uint64_t kMaxChunkBlocks = 1ull << 16;  // ≤ 2^31 terms per sweep
+  uint64_t pos = 0;
+  while (pos < n) {
+    int ex = 0;
+    std::frexp(acc, &ex);
+    const int e = ex - 1;  // acc ∈ [2^e, 2^(e+1))
+    if (!(acc > 0.0) || !std::isnormal(acc) || e < -900 || e > 900 || n - pos <= kB) {
+      const uint64_t b = std::min(n, pos + kB);  // head (s = 0) / degenerate binade: serial
+      serial(pos, b);
+      pos = b;
+      continue;
+    }
+    uint64_t m = static_cast<uint64_t>(std::ldexp(acc, 52 - e));
+    // expected terms until the next binade crossing, from the mean term so far
+    const double mean = pos > 0 && acc > s0 ? (acc - s0) / static_cast<double>(pos) : 0.0;
+    const double expect = mean > 0.0 ? (std::ldexp(1.0, e + 1) - acc) / mean : 1e30;
+    uint64_t nb = static_cast<uint64_t>(std::min(1.25 * expect / static_cast<double>(kB) + 1.0,
+                                                 static_cast<double>(kMaxChunkBlocks)));
+    nb = std::max<uint64_t>(nb, 8);
+    const uint64_t end = std::min(n, pos + nb * kB);
+    nb = (end - pos + kB - 1) / kB;
+    auto* maps = ctx.ssmaps.get<SsMap>(nb * sizeof(SsMap));
+    k_ss_blocks<T, SQ><<<static_cast<unsigned>(nb), kSsThreads, 0, s>>>(v, pos, end, std::ldexp(1.0, 52 - e), maps);
+    check_launch("k_ss_blocks");
+    auto* hm = ctx.ssmaps_h.get<SsMap>(nb * sizeof(SsMap));
+    CK(cudaMemcpyAsync(hm, maps, nb * sizeof(SsMap), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    uint64_t b = 0;
+    for (; b < nb; ++b) {
+      const unsigned long long t = hm[b].t[m & 1ull];
+      if (t >= kSsSat || m + t >= (1ull << 53)) break;  // binade crossing inside block b
+      m += t;
+    }
+    acc = std::ldexp(static_cast<double>(m), e - 52);  // exact: m < 2^53
+    const uint64_t at = pos + b * kB;
+    if (b == nb) {
+      pos = end;
+    } else {  // the crossing block, serially; then the next binade
+      const uint64_t bend = std::min(end, at + kB);
+      serial(at, bend);
+      pos = bend;
+    }
+  }
+  return acc;
+}
+
+double exact_serial_sum(Context& ctx, const void* v, DType dtype, uint64_t n, bool square, double s0) {
+  if (n == 0) return s0;
+  if (dtype == DType::f32) {
+    const float* p = static_cast<const float*>(v);
+    return square ? exact_serial_sum_t<float, true>(ctx, p, n, s0) : exact_serial_sum_t<float, false>(ctx, p, n, s0);
+  }
+  const double* p = static_cast<const double*>(v);
+  return square ? exact_serial_sum_t<double, true>(ctx, p, n, s0) : exact_serial_sum_t<double, false>(ctx, p, n, s0);
+}
+
+// blocked_reduce's Σv² (exec.cpp:47-71, :108-117): serial 4096-blocks, then a
+// serial combine of the partials from 0.0 — both on the device.
 template <typename T>
 static double blocked_sumsq(Context& ctx, const T* v, uint64_t n) {
   const uint64_t nb = (n + 4095) / 4096;
   double* part = ctx.partial.get<double>(nb * 8);
   k_block_sumsq<T><<<static_cast<unsigned>((nb + 127) / 128), 128, 0, ctx.stream>>>(v, n, part, aligned16(v));
   check_launch("k_block_sumsq");
-  double* hp = ctx.partial_h.get<double>(nb * 8);
-  CK(cudaMemcpyAsync(hp, part, nb * 8, cudaMemcpyDeviceToHost, ctx.stream));
-  CK(cudaStreamSynchronize(ctx.stream));
-  double acc = 0.0;
-  for (uint64_t b = 0; b < nb; ++b) acc = acc + hp[b];
-  return acc;
+  return exact_serial_sum(ctx, part, DType::f64, nb, false, 0.0);
 }
 
 FieldStats field_stats(Context& ctx, const void* data, DType dtype, uint64_t n) {
@@ -748,6 +762,34 @@ FieldStats field_stats(Context& ctx, const void* data, DType dtype, uint64_t n) 
   CK(cudaMemcpyAsync(&sh->stats, &sd->stats, sizeof(Stats), cudaMemcpyDeviceToHost, ctx.stream));
   CK(cudaStreamSynchronize(ctx.stream));
   return {key_to_double(sh->stats.min_key), key_to_double(sh->stats.max_key), sh->stats.nonfinite != 0};
+}
+
+GlobalStats global_stats(Context& ctx, const void* data, DType dtype, uint64_t n, bool want_sumsq) {
+  GlobalStats g{0.0, 0.0, 0.0, false};
+  const size_t unit = dtype_size(dtype);
+  const bool dev = is_device_pointer(data);
+  // host arrays are streamed through a bounded staging buffer in file order
+  const uint64_t chunk = dev ? n : std::max<uint64_t>(1, (uint64_t{256} << 20) / unit);
+  bool first = true;
+  for (uint64_t at = 0; at < n; at += chunk) {
+    const uint64_t cnt = std::min(chunk, n - at);
+    const void* p = static_cast<const uint8_t*>(data) + at * unit;
+    if (!dev) {
+      void* d = ctx.in.get<uint8_t>(cnt * unit);
+      CK(cudaMemcpyAsync(d, p, cnt * unit, cudaMemcpyHostToDevice, ctx.stream));
+      p = d;
+    }
+    const FieldStats fs = field_stats(ctx, p, dtype, cnt);
+    if (fs.nonfinite) {
+      g.nonfinite = true;
+      return g;
+    }
+    g.min = first ? fs.min : std::min(g.min, fs.min);
+    g.max = first ? fs.max : std::max(g.max, fs.max);
+    first = false;
+    if (want_sumsq) g.sumsq = exact_serial_sum(ctx, p, dtype, cnt, true, g.sumsq);
+  }
+  return g;
 }
 
 // ---------------------------------------------------------------------------
@@ -1113,8 +1155,12 @@ static size_t tf_smem(int maxlen) { return tf_smem_base() + lut_smem(maxlen); }
 static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
 
 static void huff_smem_optin() {
-  static thread_local bool done = false;
-  if (done) return;
+  // the attribute is per device: track the opt-in per (thread, device)
+  static thread_local uint64_t done_mask = 0;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done_mask & bit) return;
   const int mx = static_cast<int>(huff_smem(kSmemLutMaxLen));
   const int ms = static_cast<int>(sync_smem(kSmemLutMaxLen));
   CK(cudaFuncSetAttribute(k_huff_sync_s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ms));
@@ -1129,7 +1175,7 @@ static void huff_smem_optin() {
                           static_cast<int>(tf_smem(kSmemLutMaxLen))));
   CK(cudaFuncSetAttribute(k_huff_fix_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(fix_smem(kMaxCodeLen))));
-  done = true;
+  done_mask |= bit;
 }
 
 template <typename Z>

@@ -64,4 +64,17 @@ struct FieldStats {
 };
 FieldStats field_stats(Context& ctx, const void* data, DType dtype, uint64_t n);
 
+// Whole-array statistics of the CLI's scan_stats (tools/mgrc.cpp:197-233):
+// min, max, non-finite flag and Σv² summed serially in index order, bit-exact
+// (host arrays are streamed through a bounded device staging buffer).
+struct GlobalStats {
+  double min, max, sumsq;
+  bool nonfinite;
+};
+GlobalStats global_stats(Context& ctx, const void* data, DType dtype, uint64_t n, bool want_sumsq);
+
+// s0 + Σ p_i in index order with one rounding per addition (p_i = v_i² when
+// `square`), reproduced exactly on the device (serial_sum.cuh).  Terms ≥ 0.
+double exact_serial_sum(Context& ctx, const void* v, DType dtype, uint64_t n, bool square, double s0);
+
 }  // namespace mgrc_gpu
