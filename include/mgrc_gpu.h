@@ -114,6 +114,33 @@ MGRC_GPU_API int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndim
 MGRC_GPU_API int mgrc_gpu_decompress_chunked(const uint8_t* in, uint64_t len, void** out, int* dtype, int* ndims,
                                              uint64_t* shape);
 
+/* ---- the decomposition and the quantiser as entry points of their own ----
+ * f64 arrays, row-major over the grid (shape, coords as in mgrc_gpu_compress);
+ * host or device pointers.  Bit-identical to the reference library. */
+
+/* GridHierarchy::nlevels of make_grid(shape[, coords]) (grid.cpp:100-153). */
+MGRC_GPU_API int mgrc_gpu_nlevels(int ndims, const uint64_t* shape, const double* const* coords, int* nlevels);
+/* initial_bin_widths (error_control.cpp:42-60): widths[0..nlevels]. */
+MGRC_GPU_API int mgrc_gpu_initial_bin_widths(double tau_abs, int norm, double smoothness, int ndims, int nlevels,
+                                             double* widths);
+/* Replaces forward_transform (transform.hpp:24-26, transform.cpp:163-178):
+ * c = multilevel coefficients of u.  NonFiniteInput on NaN/Inf. */
+MGRC_GPU_API int mgrc_gpu_forward_transform(const double* u, int ndims, const uint64_t* shape,
+                                            const double* const* coords, double* c);
+/* Replaces inverse_transform (transform.hpp:28-30, transform.cpp:180-191). */
+MGRC_GPU_API int mgrc_gpu_inverse_transform(const double* c, int ndims, const uint64_t* shape,
+                                            const double* const* coords, double* u);
+/* Replaces quantize (quantize.hpp:32-36, quantize.cpp:72-132): q = rne(c/delta_tag)
+ * and (if residuals != NULL) r = c - q*delta_tag; nwidths must be nlevels+1
+ * (ShapeMismatch), widths > 0 (InvalidState); Overflow when |c/delta| >= 2^63;
+ * *outliers (nullable) = count of |q| > 2^31-1. */
+MGRC_GPU_API int mgrc_gpu_quantize(const double* c, int ndims, const uint64_t* shape, const double* const* coords,
+                                   const double* widths, int nwidths, int64_t* q, double* residuals,
+                                   uint64_t* outliers);
+/* Replaces dequantize (quantize.hpp:38-40, quantize.cpp:134-158): c = (double)q*delta_tag. */
+MGRC_GPU_API int mgrc_gpu_dequantize(const int64_t* q, int ndims, const uint64_t* shape, const double* const* coords,
+                                     const double* widths, int nwidths, double* c);
+
 /* Non-finite flag, min and max of an array (host or device) — the per-rank
  * statistics of the multi-GPU driver's global REL normalisation. */
 MGRC_GPU_API int mgrc_gpu_field_stats(const void* data, int dtype, uint64_t n, double* min, double* max,
@@ -134,6 +161,15 @@ MGRC_GPU_API int mgrc_gpu_set_profiling(int on);
 MGRC_GPU_API int mgrc_gpu_profile_count(void);
 MGRC_GPU_API int mgrc_gpu_profile_entry(int i, const char** name, double* ms, double* bytes);
 MGRC_GPU_API const char* mgrc_gpu_version(void);
+/* Accept decision of the calling thread's last compress (container.cpp:93-123):
+ * the absolute tolerance tau, the achieved error the decision compared with
+ * tau*(1-1e-9) (error_control.cpp:62-101; for S(s!=0) the reference's
+ * level-weighted estimator), the shrink passes run, and how it was decided:
+ * 0 none (constant field), 1 a-priori bound (L+1)*max|r| (reported in
+ * *achieved), 2 the exact a-posteriori value, 3 the same after the S(s!=0)
+ * estimator's fixed-order sum could not certify the decision and the
+ * reference's serial per-level sums were reproduced exactly. */
+MGRC_GPU_API int mgrc_gpu_last_compress_stats(double* tau_abs, double* achieved, int* passes, int* decided_by);
 /* Kernels launched by the calling thread through this library so far. */
 MGRC_GPU_API uint64_t mgrc_gpu_launch_count(void);
 

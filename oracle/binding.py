@@ -120,7 +120,7 @@ class Oracle:
             raise OracleError(rc, self.lib.oc_last_error().decode())
 
     def _take_bytes(self, p, n):
-        b = C.string_at(p, n) if n else b""
+        b = bytes((C.c_uint8 * n).from_address(p.value if hasattr(p, "value") else p)) if n else b""
         self.lib.oc_free(p)
         return b
 
@@ -163,7 +163,8 @@ class Oracle:
         sh = tuple(int(x) for x in shape[: nd.value])
         npdt = np.float32 if dt.value == 0 else np.float64
         cnt = int(np.prod(sh))
-        arr = np.frombuffer(C.string_at(out, cnt * np.dtype(npdt).itemsize), dtype=npdt).reshape(sh).copy()
+        nb = cnt * np.dtype(npdt).itemsize  # (ctypes.string_at truncates sizes beyond 2 GiB)
+        arr = np.frombuffer((C.c_uint8 * nb).from_address(out.value), dtype=npdt).reshape(sh).copy()
         self.lib.oc_free(out)
         return arr
 

@@ -31,7 +31,8 @@ __all__ = [
     "Norm", "Mode", "Codec", "DType", "ErrorSpec", "TensorGrid", "ContainerInfo", "MgrcError", "make_grid",
     "compress", "compress_to", "decompress", "decompress_into", "inspect", "describe", "plan_chunks",
     "compress_chunked", "decompress_chunked", "field_stats", "set_device", "set_stream", "set_profiling",
-    "last_profile", "launch_count", "ERRC_NAMES",
+    "last_profile", "launch_count", "last_compress_stats", "nlevels", "initial_bin_widths", "forward_transform",
+    "inverse_transform", "quantize", "dequantize", "ERRC_NAMES",
 ]
 
 
@@ -123,6 +124,14 @@ def make_grid(shape: Sequence[int], coords: Optional[Sequence[Sequence[float]]] 
                                                                                for c in coords])
 
 
+def _take(ptr, nbytes: int) -> memoryview:
+    """A view of ``nbytes`` at a library-allocated address (ctypes.string_at takes a C int size, which
+    truncates containers and arrays beyond 2 GiB)."""
+    if nbytes == 0:
+        return memoryview(b"")
+    return memoryview((C.c_uint8 * nbytes).from_address(ptr.value if hasattr(ptr, "value") else ptr)).cast("B")
+
+
 def _check(rc: int) -> None:
     if rc != 0:
         raise MgrcError(rc, _lib.lib().mgrc_gpu_last_error().decode(errors="replace"))
@@ -200,7 +209,7 @@ def compress(u, grid: Optional[TensorGrid] = None, spec: Optional[ErrorSpec] = N
     _check(_lib.lib().mgrc_gpu_compress(ptr, int(dt), len(gshape), gshape.ctypes.data, coords, spec.tol,
                                         int(spec.norm), spec.smoothness, int(spec.mode), int(codec), C.byref(out),
                                         C.byref(n)))
-    b = C.string_at(out, n.value)
+    b = bytes(_take(out, n.value))
     _lib.lib().mgrc_gpu_free(out)
     return b
 
@@ -237,7 +246,7 @@ def decompress(blob) -> np.ndarray:
     sh = tuple(int(s) for s in shape[: nd.value])
     npdt = np.float32 if dt.value == 0 else np.float64
     cnt = int(np.prod(sh))
-    arr = np.frombuffer(C.string_at(out, cnt * np.dtype(npdt).itemsize), dtype=npdt).reshape(sh).copy()
+    arr = np.frombuffer(_take(out, cnt * np.dtype(npdt).itemsize), dtype=npdt).reshape(sh).copy()
     _lib.lib().mgrc_gpu_free(out)
     return arr
 
@@ -303,7 +312,7 @@ def compress_chunked(u, spec: ErrorSpec, codec: Codec = Codec.huffman, chunk_mem
     _check(_lib.lib().mgrc_gpu_compress_chunked(ptr, int(dt), len(gshape), gshape.ctypes.data, cs, spec.tol,
                                                 int(spec.norm), spec.smoothness, int(spec.mode), int(codec),
                                                 chunk_mem, C.byref(out), C.byref(n)))
-    b = C.string_at(out, n.value)
+    b = bytes(_take(out, n.value))
     _lib.lib().mgrc_gpu_free(out)
     return b
 
@@ -320,7 +329,7 @@ def decompress_chunked(blob) -> np.ndarray:
     sh = tuple(int(s) for s in shape[: nd.value])
     npdt = np.float32 if dt.value == 0 else np.float64
     cnt = int(np.prod(sh))
-    arr = np.frombuffer(C.string_at(out, cnt * np.dtype(npdt).itemsize), dtype=npdt).reshape(sh).copy()
+    arr = np.frombuffer(_take(out, cnt * np.dtype(npdt).itemsize), dtype=npdt).reshape(sh).copy()
     _lib.lib().mgrc_gpu_free(out)
     return arr
 
@@ -365,3 +374,123 @@ def last_profile() -> list:
         _check(L.mgrc_gpu_profile_entry(i, C.byref(name), C.byref(ms), C.byref(by)))
         out.append((name.value.decode(), ms.value, by.value))
     return out
+
+
+def last_compress_stats() -> dict:
+    """Accept decision of this thread's last compress (container.cpp:93-123): ``tau_abs``, the ``achieved``
+    error compared with tau_abs*(1-1e-9) (the reference's estimator; for ``decided_by == "bound"`` the
+    a-priori bound (L+1)*max|r| that already passes), the shrink ``passes`` run."""
+    L = _lib.lib()
+    tau, ach = C.c_double(), C.c_double()
+    passes, how = C.c_int(), C.c_int()
+    L.mgrc_gpu_last_compress_stats(C.byref(tau), C.byref(ach), C.byref(passes), C.byref(how))
+    return {"tau_abs": tau.value, "achieved": ach.value, "passes": passes.value,
+            "decided_by": {0: "none", 1: "bound", 2: "exact", 3: "exact-serial"}.get(how.value, str(how.value))}
+
+
+# ---------------------------------------------------------------------------
+# the decomposition and the quantiser as entry points of their own
+# (transform.hpp:24-30, quantize.hpp:32-42); f64 numpy arrays or torch tensors
+# (host or CUDA) — outputs live where the input lives.
+
+
+def _f64_ptr(a, what):
+    if _is_torch(a):
+        import torch
+
+        if a.dtype != torch.float64:
+            raise TypeError(f"{what} must be float64")
+        a = a.contiguous()
+        return a.data_ptr(), tuple(a.shape), a
+    a = np.ascontiguousarray(a)
+    if a.dtype != np.float64:
+        raise TypeError(f"{what} must be float64")
+    return a.ctypes.data, a.shape, a
+
+
+def _empty_like(ref, dtype_np):
+    if _is_torch(ref):
+        import torch
+
+        tdt = {np.float64: torch.float64, np.int64: torch.int64}[dtype_np]
+        t = torch.empty(tuple(ref.shape), dtype=tdt, device=ref.device)
+        return t, t.data_ptr()
+    a = np.empty(ref.shape, dtype=dtype_np)
+    return a, a.ctypes.data
+
+
+def nlevels(grid: TensorGrid) -> int:
+    """GridHierarchy::nlevels of the grid (grid.cpp:100-153)."""
+    shape, coords, keep = _grid_args(grid)
+    n = C.c_int()
+    _check(_lib.lib().mgrc_gpu_nlevels(len(shape), shape.ctypes.data, coords, C.byref(n)))
+    return n.value
+
+
+def initial_bin_widths(tau_abs: float, spec: ErrorSpec, ndims: int, nlev: int) -> np.ndarray:
+    """initial_bin_widths (error_control.cpp:42-60)."""
+    out = np.zeros(nlev + 1, dtype=np.float64)
+    _check(_lib.lib().mgrc_gpu_initial_bin_widths(tau_abs, int(spec.norm), spec.smoothness, ndims, nlev,
+                                                  out.ctypes.data))
+    return out
+
+
+def forward_transform(u, grid: Optional[TensorGrid] = None):
+    """forward_transform (transform.cpp:163-178) on the GPU: the multilevel coefficients of ``u``."""
+    ptr, shape, keep = _f64_ptr(u, "u")
+    grid = grid or make_grid(shape)
+    _check_grid(grid, shape)
+    gshape, coords, ck = _grid_args(grid)
+    c, cp = _empty_like(keep, np.float64)
+    _check(_lib.lib().mgrc_gpu_forward_transform(ptr, len(gshape), gshape.ctypes.data, coords, cp))
+    return c
+
+
+def inverse_transform(c, grid: Optional[TensorGrid] = None):
+    """inverse_transform (transform.cpp:180-191) on the GPU."""
+    ptr, shape, keep = _f64_ptr(c, "c")
+    grid = grid or make_grid(shape)
+    _check_grid(grid, shape)
+    gshape, coords, ck = _grid_args(grid)
+    u, up = _empty_like(keep, np.float64)
+    _check(_lib.lib().mgrc_gpu_inverse_transform(ptr, len(gshape), gshape.ctypes.data, coords, up))
+    return u
+
+
+def quantize(c, widths, grid: Optional[TensorGrid] = None, residuals: bool = True):
+    """quantize (quantize.cpp:72-132) on the GPU: (q int64, r float64 or None, outlier count)."""
+    ptr, shape, keep = _f64_ptr(c, "c")
+    grid = grid or make_grid(shape)
+    _check_grid(grid, shape)
+    gshape, coords, ck = _grid_args(grid)
+    w = np.ascontiguousarray(widths, dtype=np.float64)
+    q, qp = _empty_like(keep, np.int64)
+    r, rp = _empty_like(keep, np.float64) if residuals else (None, None)
+    o = C.c_uint64()
+    _check(_lib.lib().mgrc_gpu_quantize(ptr, len(gshape), gshape.ctypes.data, coords, w.ctypes.data, w.size, qp, rp,
+                                        C.byref(o)))
+    return q, r, o.value
+
+
+def dequantize(q, widths, grid: Optional[TensorGrid] = None):
+    """dequantize (quantize.cpp:134-158) on the GPU."""
+    if _is_torch(q):
+        qq = q.contiguous()
+        ptr, shape = qq.data_ptr(), tuple(qq.shape)
+    else:
+        qq = np.ascontiguousarray(q, dtype=np.int64)
+        ptr, shape = qq.ctypes.data, qq.shape
+    grid = grid or make_grid(shape)
+    _check_grid(grid, shape)
+    gshape, coords, ck = _grid_args(grid)
+    w = np.ascontiguousarray(widths, dtype=np.float64)
+    if _is_torch(q):
+        import torch
+
+        c = torch.empty(shape, dtype=torch.float64, device=q.device)
+        cp = c.data_ptr()
+    else:
+        c = np.empty(shape, dtype=np.float64)
+        cp = c.ctypes.data
+    _check(_lib.lib().mgrc_gpu_dequantize(ptr, len(gshape), gshape.ctypes.data, coords, w.ctypes.data, w.size, cp))
+    return c

@@ -54,6 +54,13 @@ SIGNATURES = {
                                          C.POINTER(C.c_double)]),
     "mgrc_gpu_version": (C.c_char_p, []),
     "mgrc_gpu_launch_count": (C.c_uint64, []),
+    "mgrc_gpu_nlevels": (C.c_int, [C.c_int, P, P, IP]),
+    "mgrc_gpu_initial_bin_widths": (C.c_int, [C.c_double, C.c_int, C.c_double, C.c_int, C.c_int, P]),
+    "mgrc_gpu_forward_transform": (C.c_int, [P, C.c_int, P, P, P]),
+    "mgrc_gpu_inverse_transform": (C.c_int, [P, C.c_int, P, P, P]),
+    "mgrc_gpu_quantize": (C.c_int, [P, C.c_int, P, P, P, C.c_int, P, P, U64P]),
+    "mgrc_gpu_dequantize": (C.c_int, [P, C.c_int, P, P, P, C.c_int, P]),
+    "mgrc_gpu_last_compress_stats": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), IP, IP]),
 }
 
 _lib = None

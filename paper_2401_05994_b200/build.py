@@ -16,7 +16,7 @@ CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libmgrc_gpu.so"
 
-SOURCES = ["pipeline.cu", "host.cpp", "capi.cpp"]
+SOURCES = ["pipeline.cu", "transform.cu", "host.cpp", "capi.cpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -24,8 +24,8 @@ NVCC_FLAGS = [
     "--fmad=false",                 # no FMA contraction anywhere
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
     "-Xptxas", "-warn-spills",
-    "-shared", "-cudart", "static",
 ]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static"]
 
 
 def nvcc() -> str:
@@ -45,18 +45,34 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Each translation unit compiles to an object in parallel (nvcc -c), then one nvcc link."""
     if not force and not needs_build():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp")
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
     extra = os.environ.get("MGRC_NVCC_EXTRA", "").split()  # experiments only (e.g. -DMGRC_WARM_BITS=512)
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
+
+    def compile_one(src):
+        obj = objdir / (src + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", "-o", str(obj), str(CSRC / src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src} ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+        if verbose and r.stderr:
+            print(r.stderr, file=sys.stderr)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [nvcc(), *LINK_FLAGS, "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
-    if verbose and r.stderr:
-        print(r.stderr, file=sys.stderr)
+        raise RuntimeError(f"nvcc link failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
     tmp.replace(LIB)
     return LIB
 

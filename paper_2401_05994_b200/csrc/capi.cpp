@@ -13,6 +13,7 @@
 #include "../../include/mgrc_gpu.h"
 #include "host.hpp"
 #include "pipeline.hpp"
+#include "transform.hpp"
 
 using namespace mgrc_gpu;
 
@@ -269,6 +270,15 @@ const char* mgrc_gpu_last_error(void) { return g_last_error.c_str(); }
 void mgrc_gpu_free(void* p) { std::free(p); }
 uint64_t mgrc_gpu_launch_count(void) { return launch_count(); }
 
+int mgrc_gpu_last_compress_stats(double* tau_abs, double* achieved, int* passes, int* decided_by) {
+  const CompressStats& c = last_compress_stats();
+  if (tau_abs) *tau_abs = c.tau_abs;
+  if (achieved) *achieved = c.achieved;
+  if (passes) *passes = c.passes;
+  if (decided_by) *decided_by = c.decided_by;
+  return MGRC_OK;
+}
+
 int mgrc_gpu_host_alloc(uint64_t bytes, void** p) {
   return guarded([&] {
     require(p != nullptr, "null output pointer");
@@ -454,6 +464,64 @@ int mgrc_gpu_field_stats(const void* data, int dtype, uint64_t n, double* mn, do
     if (mn) *mn = st.min;
     if (mx) *mx = st.max;
     if (nonfinite) *nonfinite = st.nonfinite;
+  });
+}
+
+// ---- decomposition / quantiser entry points (transform.hpp:24-30, quantize.hpp:32-42) ----
+
+int mgrc_gpu_nlevels(int ndims, const uint64_t* shape, const double* const* coords, int* nlevels) {
+  return guarded([&] {
+    require(nlevels != nullptr, "null argument");
+    *nlevels = build_hierarchy(grid_from(ndims, shape, coords)).L;
+  });
+}
+
+int mgrc_gpu_initial_bin_widths(double tau_abs, int norm, double smoothness, int ndims, int nlevels, double* widths) {
+  return guarded([&] {
+    require(widths != nullptr && nlevels >= 0 && nlevels < 64, "bad argument");
+    const auto w = initial_bin_widths(tau_abs, to_spec(tau_abs, norm, smoothness, 0), ndims, nlevels);
+    for (int l = 0; l <= nlevels; ++l) widths[l] = w[l];
+  });
+}
+
+int mgrc_gpu_forward_transform(const double* u, int ndims, const uint64_t* shape, const double* const* coords,
+                               double* c) {
+  return guarded([&] {
+    require(u != nullptr && c != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    ensure_device();
+    forward_transform(context_for_current_device(), u, c, g);
+  });
+}
+
+int mgrc_gpu_inverse_transform(const double* c, int ndims, const uint64_t* shape, const double* const* coords,
+                               double* u) {
+  return guarded([&] {
+    require(u != nullptr && c != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    ensure_device();
+    inverse_transform(context_for_current_device(), c, u, g);
+  });
+}
+
+int mgrc_gpu_quantize(const double* c, int ndims, const uint64_t* shape, const double* const* coords,
+                      const double* widths, int nwidths, int64_t* q, double* residuals, uint64_t* outliers) {
+  return guarded([&] {
+    require(c != nullptr && q != nullptr && widths != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    ensure_device();
+    const uint64_t o = quantize_coefficients(context_for_current_device(), c, g, widths, nwidths, q, residuals);
+    if (outliers) *outliers = o;
+  });
+}
+
+int mgrc_gpu_dequantize(const int64_t* q, int ndims, const uint64_t* shape, const double* const* coords,
+                        const double* widths, int nwidths, double* c) {
+  return guarded([&] {
+    require(c != nullptr && q != nullptr && widths != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    ensure_device();
+    dequantize_coefficients(context_for_current_device(), q, g, widths, nwidths, c);
   });
 }
 

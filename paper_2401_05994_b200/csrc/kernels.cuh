@@ -202,7 +202,7 @@ struct Stats {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_stats(const T* __restrict__ u, uint64_t n, Stats* out, int vec_ok) {
+static __global__ void __launch_bounds__(256) k_stats(const T* __restrict__ u, uint64_t n, Stats* out, int vec_ok) {
   double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
   unsigned bad = 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) k_stats(const T* __restrict__ u, uint64_t
 // per block, serial in index order, no FMA.  Partials are combined serially
 // on the host, exactly as blocked_reduce does.
 template <typename T>
-__global__ void __launch_bounds__(128) k_block_sumsq(const T* __restrict__ v, uint64_t n, double* __restrict__ partials,
+static __global__ void __launch_bounds__(128) k_block_sumsq(const T* __restrict__ v, uint64_t n, double* __restrict__ partials,
                                                      int vec_ok) {
   const uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t nb = (n + 4095) / 4096;
@@ -319,7 +319,7 @@ struct SrcResidual {
 // Box pass for level l < L (and level 0): enumerates the level-l box with
 // the level index sets and updates the nodes tagged l.
 template <int D, class Src>
-__global__ void __launch_bounds__(256) k_inverse_box(GridDev g, BoxDev box, int l, Src src, double* v) {
+static __global__ void __launch_bounds__(256) k_inverse_box(GridDev g, BoxDev box, int l, Src src, double* v) {
   auto ld = [v](uint64_t off) { return v[off]; };
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < box.count; p += step) {
@@ -377,8 +377,24 @@ struct ChkBound {
 };
 struct ChkLevelWeighted {
   static constexpr bool kNeedsE = true;  // S(s≠0): Σ 2^{2s(tag−L)} r² (error_control.cpp:72-100), r passed as e
-  __device__ __forceinline__ void operator()(uint64_t, double, double, double&) const {}
+  double* rstore;  // non-null on the certified fallback: every node's r, row-major, for the serial level sums
+  __device__ __forceinline__ void operator()(uint64_t n, double r, double, double&) const {
+    if (rstore) rstore[n] = r;
+  }
 };
+
+// out[n] = r[n] if tag(n) == l else 0: the masked sequence whose SERIAL sum of squares equals the
+// reference's level_sumsq[l] (error_control.cpp:77-90 adds v*v in row-major order over the tag-l nodes;
+// the zero terms leave the running sum unchanged).
+template <int D>
+static __global__ void k_level_mask(GridDev g, const double* __restrict__ r, int l, double* __restrict__ out) {
+  for (uint64_t n = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; n < g.N;
+       n += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    decompose<D>(g, n, i);
+    out[n] = node_tag<D>(g, i) == l ? r[n] : 0.0;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Decoupled look-back (single-pass prefix) helpers.  A tile publishes
@@ -422,7 +438,7 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
 // Tiles are claimed through a ticket so that predecessors always run first.
 constexpr int kScanThreads = 256, kScanPer = 8, kScanTile = kScanThreads * kScanPer;
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_lb(const unsigned long long* __restrict__ in,
+static __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const unsigned long long* __restrict__ in,
                                                           unsigned long long* __restrict__ out, uint64_t n,
                                                           unsigned long long* status, unsigned int* ticket) {
   __shared__ unsigned long long wsum[kScanThreads / 32];
@@ -496,7 +512,7 @@ __device__ __forceinline__ uint32_t varint_bits(uint64_t z, const uint8_t* len) 
 // tile (possibly shared with a neighbour) go to edge slots merged by
 // k_pack_edges.  Output words hold the stream MSB-first in memory byte order.
 template <typename Z>
-__global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ zz, uint64_t n,
+static __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ zz, uint64_t n,
                                                           const uint32_t* __restrict__ code_g,
                                                           const uint8_t* __restrict__ len_g,
                                                           unsigned long long* status, unsigned int* ticket,
@@ -609,7 +625,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __restrict__ 
 // Merges the edge words: word W receives the OR of every tile's first / last
 // word that falls on W (only neighbours can share a word: a full tile spans
 // ≥ 2048 bits).  tile_start has ntiles+1 entries (the last = total bits).
-__global__ void k_pack_edges(const unsigned long long* __restrict__ tile_start, uint64_t ntiles,
+static __global__ void k_pack_edges(const unsigned long long* __restrict__ tile_start, uint64_t ntiles,
                              const uint32_t* __restrict__ edge_first, const uint32_t* __restrict__ edge_last,
                              uint32_t* __restrict__ out) {
   const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -639,7 +655,7 @@ __global__ void k_pack_edges(const unsigned long long* __restrict__ tile_start, 
 
 // Codec 0 (raw little-endian int64, codec.cpp:437-441).
 template <typename Z>
-__global__ void k_raw_encode(const Z* __restrict__ zz, uint64_t n, long long* __restrict__ out) {
+static __global__ void k_raw_encode(const Z* __restrict__ zz, uint64_t n, long long* __restrict__ out) {
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += step)
     out[k] = unzigzag(static_cast<uint64_t>(zz[k]));
@@ -680,7 +696,7 @@ constexpr int kCrcThreads = 256;
 constexpr int kCrcSeg = 1024;  // bytes per thread
 
 
-__global__ void __launch_bounds__(kCrcThreads) k_crc_blocks(const uint8_t* __restrict__ p, uint64_t n,
+static __global__ void __launch_bounds__(kCrcThreads) k_crc_blocks(const uint8_t* __restrict__ p, uint64_t n,
                                                             const uint32_t* __restrict__ tab_g, CrcConsts K,
                                                             uint32_t* __restrict__ blk_crc,
                                                             unsigned long long* __restrict__ blk_len) {
@@ -763,7 +779,7 @@ __device__ __forceinline__ uint32_t crc_slice4(const uint32_t (*tab)[256], uint3
   return tab[3][c & 255] ^ tab[2][(c >> 8) & 255] ^ tab[1][(c >> 16) & 255] ^ tab[0][c >> 24];
 }
 
-__global__ void __launch_bounds__(kCrcWarps * 32) k_crc_coal(const uint8_t* __restrict__ p, uint64_t nchunks,
+static __global__ void __launch_bounds__(kCrcWarps * 32) k_crc_coal(const uint8_t* __restrict__ p, uint64_t nchunks,
                                                              uint64_t tail, const uint32_t* __restrict__ tab_g,
                                                              CrcConsts K, uint32_t* __restrict__ blk_crc,
                                                              unsigned long long* __restrict__ blk_len) {
@@ -824,12 +840,12 @@ __global__ void __launch_bounds__(kCrcWarps * 32) k_crc_coal(const uint8_t* __re
 }
 
 // raw(M) -> crc(M) in place (one thread)
-__global__ void k_crc_finish(uint32_t* crc, const unsigned long long* len, CrcConsts K) {
+static __global__ void k_crc_finish(uint32_t* crc, const unsigned long long* len, CrcConsts K) {
   crc[0] = ~(crc_shift(0xFFFFFFFFu, len[0], K) ^ crc[0]);
 }
 
 // Folds per-block (crc, len) pairs; iterated until one pair remains.
-__global__ void __launch_bounds__(kCrcThreads) k_crc_fold(const uint32_t* __restrict__ in_crc,
+static __global__ void __launch_bounds__(kCrcThreads) k_crc_fold(const uint32_t* __restrict__ in_crc,
                                                           const unsigned long long* __restrict__ in_len, uint64_t n,
                                                           CrcConsts K, uint32_t* __restrict__ out_crc,
                                                           unsigned long long* __restrict__ out_len) {
@@ -882,7 +898,7 @@ struct SeqInfo {
   uint32_t pad;
 };
 
-__global__ void k_seq_counts(const SeqInfo* __restrict__ seq, uint64_t nseq, unsigned long long* __restrict__ nterm) {
+static __global__ void k_seq_counts(const SeqInfo* __restrict__ seq, uint64_t nseq, unsigned long long* __restrict__ nterm) {
   const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (j < nseq) nterm[j] = seq[j].nterm;
 }
@@ -896,7 +912,7 @@ struct DecodeStatus {
 
 // Codec 0 decode: raw little-endian int64 → zigzag.
 template <typename Z>
-__global__ void k_raw_decode(const long long* __restrict__ in, uint64_t n, Z* __restrict__ zz, unsigned int* wide) {
+static __global__ void k_raw_decode(const long long* __restrict__ in, uint64_t n, Z* __restrict__ zz, unsigned int* wide) {
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   unsigned wd = 0;
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += step) {
@@ -908,7 +924,7 @@ __global__ void k_raw_decode(const long long* __restrict__ in, uint64_t n, Z* __
 }
 
 template <typename T>
-__global__ void k_fill(T* __restrict__ out, uint64_t n, T value) {
+static __global__ void k_fill(T* __restrict__ out, uint64_t n, T value) {
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += step) out[k] = value;
 }

@@ -32,139 +32,12 @@
 #include "huff.cuh"
 #include "serial_sum.cuh"
 #include "pipeline.hpp"
+#include "context.hpp"
 
 namespace mgrc_gpu {
 
-using namespace dev;
-
-#define CK(x)                                                                                        \
-  do {                                                                                               \
-    cudaError_t e_ = (x);                                                                            \
-    if (e_ != cudaSuccess) raise(Errc::cuda, std::string(#x) + ": " + cudaGetErrorString(e_));       \
-  } while (0)
-
-static thread_local unsigned long long g_launches = 0;  // kernels launched by this thread
-
 unsigned long long launch_count() { return g_launches; }
-
-static void check_launch(const char* what) {
-  ++g_launches;
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) raise(Errc::cuda, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-bool is_device_pointer(const void* p) {
-  cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
-// ---------------------------------------------------------------------------
-// workspace
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  template <typename T = void>
-  T* get(size_t bytes) {
-    if (bytes > cap) {
-      if (p) cudaFree(p);
-      p = nullptr;
-      const size_t want = std::max(bytes, cap + cap / 4);
-      if (cudaMalloc(&p, want) != cudaSuccess) {
-        cudaGetLastError();
-        cap = 0;
-        if (cudaMalloc(&p, bytes) != cudaSuccess) {
-          cudaGetLastError();
-          p = nullptr;
-          raise(Errc::cuda, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
-        }
-        cap = bytes;
-      } else {
-        cap = want;
-      }
-    }
-    return static_cast<T*>(p);
-  }
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
-};
-
-struct PinnedBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  template <typename T = void>
-  T* get(size_t bytes) {
-    if (bytes > cap) {
-      if (p) cudaFreeHost(p);
-      CK(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
-      cap = bytes;
-    }
-    return static_cast<T*>(p);
-  }
-  ~PinnedBuf() {
-    if (p) cudaFreeHost(p);
-  }
-};
-
-// Device copy of a hierarchy's tables: the finest grid (g, boxes) and the
-// compact coarse box = the level-(L-1) box as a grid of its own (gc, cboxes)
-// carrying the same stencils, on which the coarse part of the inverse runs.
-struct DevHier {
-  std::string key;
-  Hierarchy h;
-  DevBuf buf;
-  GridDev g{};
-  std::vector<BoxDev> boxes;   // per level, finest-grid indices
-  GridDev gc{};                // coarse box (valid when h.L >= 1)
-  std::vector<BoxDev> cboxes;  // per level 0..L-1, compact indices
-};
-
-struct Scratch {  // small device-side results read back at sync points
-  Stats stats;
-  QuantFlags qflags;
-  unsigned long long red_bits;
-  DecodeStatus dstat;
-  unsigned int fix_changed;
-  unsigned int raw_wide;
-  unsigned long long hist[256];
-  unsigned long long queues[4];  // dynamic work queues of the row kernels (zeroed per launch)
-  double ssum;                   // running value of the exact serial sum
-};
-
-class Context {
- public:
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  bool profiling = false;
-  std::vector<PhaseTime> profile;
-  // workspace
-  DevBuf ssmaps;
-  PinnedBuf ssmaps_h;
-  DevBuf in, zz, zc, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws, tfst, tftab;
-  DevBuf scratch_d;
-  PinnedBuf scratch_h, partial_h;
-  std::vector<std::unique_ptr<DevHier>> hiers;  // most recently used first (chunked slabs alternate shapes)
-  cudaStream_t aux = nullptr;            // concurrent side work (decompress CRC)
-  cudaEvent_t ev_in = nullptr, ev_crc = nullptr;
-  CrcConsts crc_k{};
-  bool crc_ready = false;
-
-  Scratch* sd() { return scratch_d.get<Scratch>(sizeof(Scratch)); }
-  Scratch* sh() { return scratch_h.get<Scratch>(sizeof(Scratch)); }
-
-  ~Context() {
-    if (aux) cudaStreamDestroy(aux);
-    if (ev_in) cudaEventDestroy(ev_in);
-    if (ev_crc) cudaEventDestroy(ev_crc);
-    if (own_stream && stream) cudaStreamDestroy(stream);
-  }
-};
+const CompressStats& last_compress_stats() { return g_cstats; }
 
 Context& context_for_current_device() {
   thread_local std::map<int, std::unique_ptr<Context>> ctxs;
@@ -191,61 +64,13 @@ cudaStream_t context_stream(Context& c) { return c.stream; }
 void context_set_profiling(Context& c, bool on) { c.profiling = on; }
 const std::vector<PhaseTime>& context_profile(Context& c) { return c.profile; }
 
-// Named CUDA-event brackets on the context stream (profiling mode only).
-class Prof {
- public:
-  explicit Prof(Context& c) : c_(c) { c_.profile.clear(); }
-  void begin(const char* name, double bytes = 0) {
-    if (!c_.profiling) return;
-    Rec r;
-    r.name = name;
-    r.bytes = bytes;
-    cudaEventCreate(&r.a);
-    cudaEventCreate(&r.b);
-    cudaEventRecord(r.a, c_.stream);
-    recs_.push_back(r);
+bool is_device_pointer(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
   }
-  void end() {
-    if (!c_.profiling || recs_.empty()) return;
-    cudaEventRecord(recs_.back().b, c_.stream);
-  }
-  ~Prof() {
-    if (!c_.profiling) return;
-    cudaStreamSynchronize(c_.stream);
-    for (auto& r : recs_) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, r.a, r.b);
-      c_.profile.push_back({r.name, ms, r.bytes});
-      cudaEventDestroy(r.a);
-      cudaEventDestroy(r.b);
-    }
-  }
-
- private:
-  struct Rec {
-    std::string name;
-    double bytes;
-    cudaEvent_t a, b;
-  };
-  Context& c_;
-  std::vector<Rec> recs_;
-};
-
-static int num_sms() {
-  static thread_local int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-
-static int grid_blocks(uint64_t work_items, int threads, int per_sm = 8) {
-  const int sms = num_sms();
-  const uint64_t need = (work_items + threads - 1) / threads;
-  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(need, static_cast<uint64_t>(sms) * per_sm)));
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
 static std::string hier_key(const Grid& g) {
@@ -258,7 +83,7 @@ static std::string hier_key(const Grid& g) {
   return k;
 }
 
-static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
+DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
   const std::string key = hier_key(grid);
   for (size_t i = 0; i < ctx.hiers.size(); ++i)
     if (ctx.hiers[i]->key == key) {
@@ -426,29 +251,6 @@ static DevHier& device_hierarchy(Context& ctx, const Grid& grid) {
   return *ctx.hiers[0];
 }
 
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-static Widths to_widths(const std::vector<double>& w) {
-  Widths W{};
-  for (size_t l = 0; l < w.size() && l < static_cast<size_t>(kMaxL); ++l) W.w[l] = w[l];
-  return W;
-}
-
-
-// ---------------------------------------------------------------------------
-// dispatch helpers over the dimension count
-
-template <template <int> class F, class... Args>
-static void by_dim(int d, Args&&... args) {
-  switch (d) {
-    case 1: F<1>::run(args...); break;
-    case 2: F<2>::run(args...); break;
-    case 3: F<3>::run(args...); break;
-    case 4: F<4>::run(args...); break;
-    default: raise(Errc::too_many_dims, "unsupported dimension count");
-  }
-}
-
 template <class Src>
 struct InvBox {
   template <int D>
@@ -457,6 +259,16 @@ struct InvBox {
       const int blocks = grid_blocks(b.count, 256);
       k_inverse_box<D, Src><<<blocks, 256, 0, s>>>(g, b, l, src, v);
       check_launch("k_inverse_box");
+    }
+  };
+};
+
+struct LevelMask {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const double* r, int l, double* out) {
+      k_level_mask<D><<<num_sms() * 8, 256, 0, s>>>(g, r, l, out);
+      check_launch("k_level_mask");
     }
   };
 };
@@ -648,21 +460,6 @@ static CrcSlot device_crc_launch(Context& ctx, const uint8_t* p, uint64_t n, cud
 // ---------------------------------------------------------------------------
 // input statistics
 
-template <typename T>
-static void launch_stats(Context& ctx, const T* u, uint64_t n, Stats* out) {
-  Stats init{~0ull, 0ull, 0u};
-  CK(cudaMemcpyAsync(out, &init, sizeof init, cudaMemcpyHostToDevice, ctx.stream));
-  k_stats<T><<<grid_blocks((n + 3) / 4, 256, 4), 256, 0, ctx.stream>>>(u, n, out, aligned16(u));
-  check_launch("k_stats");
-}
-
-static double key_to_double(unsigned long long k) {
-  const unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
-  double d;
-  std::memcpy(&d, &b, 8);
-  return d;
-}
-
 // ---------------------------------------------------------------------------
 // Exact serial double sums on the device (serial_sum.cuh)
 
@@ -802,6 +599,7 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
   cudaStream_t s = ctx.stream;
   const uint64_t N = grid.count();
   const T* u = u_in;
+  g_cstats = CompressStats{0.0, -1.0, 0, 0};
   if (!on_device) {
     prof.begin("h2d_input", static_cast<double>(N * sizeof(T)));
     T* d = ctx.in.get<T>(N * sizeof(T));
@@ -857,6 +655,7 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
   const GridDev& g = dh.g;
   const int L = dh.h.L;
   std::vector<double> widths = initial_bin_widths(tau, spec, grid.d, L);
+  g_cstats = CompressStats{tau, -1.0, 0, 0};
 
   const bool level_weighted = spec.norm == Norm::s && spec.smoothness != 0.0;
   const bool s0 = spec.norm == Norm::s && !level_weighted;
@@ -883,6 +682,12 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
                          static_cast<double>(L + 1) * 0.5 * *std::max_element(widths.begin(), widths.end()) <
                              0.99 * tau;
   const double umax = std::max(std::fabs(mn), std::fabs(mx));
+  // S(s≠0): the fused pass sums w·r² in a fixed-order tree; when that value
+  // cannot certify the reference's decision, the pass re-runs storing r and
+  // the reference's serial per-level sums are reproduced exactly (below).
+  double* lw_rstore = nullptr;
+  const char* lw_env = std::getenv("MGRC_LW_CERTIFY");
+  const bool lw_force_serial = lw_env && std::strcmp(lw_env, "serial") == 0;  // tests: always take the fallback
   for (int pass = 0; pass < 10; ++pass) {
     const Widths W = to_widths(widths);
     bool bound = try_bound;
@@ -916,7 +721,7 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
         prof.begin("fine", static_cast<double>(N) * (sizeof(T) + zb + (s0 ? 8 : 0)));
         if (level_weighted)
           by_dim<FineRows<T, Z, ChkLevelWeighted, true>::template L>(grid.d, s, g, rt, W, u, zz, sd->hist,
-                                                                     &sd->qflags, ec, zc, ChkLevelWeighted{}, nullptr,
+                                                                     &sd->qflags, ec, zc, ChkLevelWeighted{lw_rstore}, nullptr,
                                                                      lw, part, fine_blocks);
         else if (L >= 1) {
           const double inv_L = 1.0 / widths[L];
@@ -978,6 +783,9 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
       double B = static_cast<double>(L + 1) * std::max(rf, rc) * slack;
       if (dtype == DType::f32) B = B + (umax + B) * std::ldexp(1.0, -24) * slack + std::ldexp(1.0, -149);
       if (B <= tau * (1.0 - 1e-9)) {
+        g_cstats.achieved = B;
+        g_cstats.passes = pass + 1;
+        g_cstats.decided_by = 1;
         accepted = true;
         break;
       }
@@ -985,13 +793,43 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
       goto retry_exact;
     }
     double achieved;
-    if (level_weighted) {  // error_control.cpp:72-100 (fixed-order tree)
+    if (level_weighted && !lw_rstore) {  // error_control.cpp:72-100, fixed-order tree
       double* hp = ctx.partial_h.get<double>(static_cast<size_t>(fine_blocks) * 8);
       CK(cudaMemcpyAsync(hp, part, static_cast<size_t>(fine_blocks) * 8, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       double acc = 0.0;
       for (int b = 0; b < fine_blocks; ++b) acc = acc + hp[b];
       achieved = std::sqrt(acc / static_cast<double>(N));
+      // Certify the accept decision against the reference's serial per-level
+      // sums R.  Both sums add N non-negative products w·r² (w exact or
+      // rounded once), so each is within γ_{N+2}·E of the exact value E
+      // (any summation order: Higham, Accuracy and Stability of Numerical
+      // Algorithms, §4.2), hence
+      // |acc − R| ≤ 2γ·E ≤ 2.5γ·acc.  sqrt(fl(x/N)) is monotone in x, so if
+      // the decision is the same at acc(1 ± 2.5γ) it is the reference's.
+      const double nn = static_cast<double>(N) + 8.0;
+      const double gam = nn * std::ldexp(1.0, -53) / (1.0 - nn * std::ldexp(1.0, -53));
+      const double thr = tau * (1.0 - 1e-9);
+      const double hi = acc + acc * (2.5 * gam), lo = acc - acc * (2.5 * gam);
+      const bool acc_hi = std::sqrt(hi / static_cast<double>(N)) <= thr;
+      const bool acc_lo = std::sqrt(lo / static_cast<double>(N)) <= thr;
+      if (lw_force_serial || acc_hi != acc_lo) {
+        lw_rstore = ctx.e.get<double>(N * 8);  // undecided: re-run the pass storing r, then sum serially
+        goto retry_exact;
+      }
+    } else if (level_weighted) {  // the reference's serial per-level sums, reproduced exactly
+      prof.begin("lw_serial", static_cast<double>(N) * 8 * (L + 1));
+      double* masked = ctx.bits.get<double>(N * 8 + 16);
+      double acc = 0.0;
+      for (int l = 0; l <= L; ++l) {
+        by_dim<LevelMask::L>(grid.d, s, g, static_cast<const double*>(lw_rstore), l, masked);
+        const double sl = exact_serial_sum(ctx, masked, DType::f64, N, true, 0.0);
+        acc += lw.w[l] * sl;  // error_control.cpp:94-96 (host code: no contraction)
+      }
+      prof.end();
+      achieved = std::sqrt(acc / static_cast<double>(N));
+      lw_rstore = nullptr;
+      g_cstats.decided_by = 3;
     } else if (s0) {  // ordered RMS of e / of the f32 cast error (exec.cpp:47-71)
       prof.begin("sumsq_check", static_cast<double>(N) * 8);
       achieved = std::sqrt(blocked_sumsq(ctx, static_cast<const double*>(ctx.e.get<double>(N * 8)), N) /
@@ -1000,6 +838,9 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
     } else {
       std::memcpy(&achieved, &sh->red_bits, 8);
     }
+    g_cstats.achieved = achieved;
+    g_cstats.passes = pass + 1;
+    if (g_cstats.decided_by != 3) g_cstats.decided_by = 2;
     if (achieved <= tau * (1.0 - 1e-9)) {
       accepted = true;
       break;

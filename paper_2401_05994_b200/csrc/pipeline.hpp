@@ -54,6 +54,17 @@ ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len);
 
 bool is_device_pointer(const void* p);
 
+// Accept decision of the last compress on this thread (container.cpp:93-123):
+// τ_abs, the achieved error the decision used (the reference's exact value, or
+// for decided_by == 1 the a-priori bound (L+1)·max|r| that already passes),
+// the number of shrink passes, and how it was decided (0 = constant field /
+// not run, 1 = bound, 2 = exact a-posteriori value).
+struct CompressStats {
+  double tau_abs, achieved;
+  int passes, decided_by;
+};
+const CompressStats& last_compress_stats();
+
 // Number of kernels this thread has launched through the library.
 unsigned long long launch_count();
 

@@ -351,8 +351,12 @@ __global__ void __launch_bounds__(kRowThreads) k_fine_rows(GridDev g, RowTiling 
         if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
         zz[n] = static_cast<Z>(z);
         hist_varint(sh, z, hsym, hcnt);
-        if (LW) red = __dadd_rn(red, __dmul_rn(lw.w[tag], __dmul_rn(r, r)));
-        else chk(n, e, src, red);
+        if (LW) {
+          red = __dadd_rn(red, __dmul_rn(lw.w[tag], __dmul_rn(r, r)));
+          chk(n, r, src, red);
+        } else {
+          chk(n, e, src, red);
+        }
       }
     }
   }

@@ -77,7 +77,7 @@ __device__ __forceinline__ SsMap ss_elem(double p, double scale) {
 
 // One map per block of kSsBlock terms of v[lo, hi).
 template <typename T, bool SQ>
-__global__ void __launch_bounds__(kSsThreads) k_ss_blocks(const T* __restrict__ v, uint64_t lo, uint64_t hi,
+static __global__ void __launch_bounds__(kSsThreads) k_ss_blocks(const T* __restrict__ v, uint64_t lo, uint64_t hi,
                                                           double scale, SsMap* __restrict__ out) {
   __shared__ SsMap wm[kSsThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kSsThreads) k_ss_blocks(const T* __restrict__ 
 
 // Serial continuation on one thread: s = fl(s + p_i) for i in [lo, hi).
 template <typename T, bool SQ>
-__global__ void k_ss_serial(const T* __restrict__ v, uint64_t lo, uint64_t hi, double* __restrict__ s) {
+static __global__ void k_ss_serial(const T* __restrict__ v, uint64_t lo, uint64_t hi, double* __restrict__ s) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   double acc = *s;
   for (uint64_t i = lo; i < hi; ++i) acc = __dadd_rn(acc, ss_term<T, SQ>(v[i]));

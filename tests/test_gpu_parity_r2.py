@@ -166,10 +166,12 @@ def test_rounding_edge_sweep_matches_reference(mg, oracle):
 
 
 def test_exact_check_path_is_taken(mg, oracle):
-    """At 1e-7 on f32 data the a-priori bound cannot decide: the exact cast check runs."""
-    u = make_field(oracle, "multisine", (33, 17, 9), "f32")
-    mg.compress(u, mg.make_grid(u.shape), mg.ErrorSpec(1e-7, mg.Norm.inf, 0.0, mg.Mode.rel))
-    assert mg.last_compress_stats()["decided_by"] == "exact"
+    """Where rounding makes max|r| exceed delta/2 the a-priori bound cannot decide: the exact a-posteriori
+    check runs (and here the loop shrinks twice); at an ordinary tolerance the bound decides."""
+    u = make_field(oracle, "multisine", (65,), "f64")
+    mg.compress(u, mg.make_grid(u.shape), mg.ErrorSpec(1.1231045018329515e-16, mg.Norm.inf, 0.0, mg.Mode.abs))
+    st = mg.last_compress_stats()
+    assert st["decided_by"] == "exact" and st["passes"] == 2
     mg.compress(u, mg.make_grid(u.shape), mg.ErrorSpec(1e-4, mg.Norm.inf, 0.0, mg.Mode.rel))
     assert mg.last_compress_stats()["decided_by"] == "bound"
 
@@ -277,3 +279,36 @@ def test_cfg5_slabs_parity(mg, oracle):
         assert np.array_equal(back, ref.decompress(want)), b
         assert float(np.max(np.abs(back.astype(np.float64) - slab.astype(np.float64)))) <= tau
         del slab, want, back
+
+
+# ---------------------------------------------------------------------------
+# S(s != 0): the accept decision is certified against the reference's serial
+# per-level sums (error_control.cpp:72-101); the exact serial fallback is
+# forced here (MGRC_LW_CERTIFY=serial) and must give the same containers.
+
+
+@pytest.mark.parametrize("case", [
+    ((129, 130), "noisy", 1e-3, 1.0),
+    ((65, 33, 17), "noisy", 1e-3, 1.0),
+    ((257, 256), "multisine", 1e-4, 0.5),
+    ((33, 9, 8, 5), "noisy", 1e-2, 2.0),
+], ids=lambda c: "x".join(map(str, c[0])) + f"-s{c[3]}")
+def test_level_weighted_serial_fallback(mg, oracle, case, monkeypatch):
+    shape, kind, tol, s = case
+    u = make_field(oracle, kind, shape, "f64")
+    want = oracle.compress(u, tol, 1, s, 1, 2)
+    spec = mg.ErrorSpec(tol, mg.Norm.s, s, mg.Mode.rel)
+    got = mg.compress(u, mg.make_grid(shape), spec, mg.Codec.huffman)
+    assert got == want
+    fast = mg.last_compress_stats()
+    assert fast["decided_by"] == "exact"
+    monkeypatch.setenv("MGRC_LW_CERTIFY", "serial")
+    got2 = mg.compress(u, mg.make_grid(shape), spec, mg.Codec.huffman)
+    st = mg.last_compress_stats()
+    assert st["decided_by"] == "exact-serial"
+    assert got2 == want
+    # the exact fallback reproduces the reference's estimator bit for bit (one pass: final widths = initial)
+    _, r, _ = oracle.quantize(oracle.forward(u), mg.inspect(want).bin_widths)
+    assert st["achieved"] == oracle.achieved_error(r, 1, s)
+    # the tree estimate is within the certified window of the serial value
+    assert abs(fast["achieved"] - st["achieved"]) <= 1e-12 * st["achieved"]
