@@ -105,7 +105,7 @@ def multisine_torch(shape, device):
 
 
 # dominant phase -> its main kernel (for the ncu DRAM traffic lookup)
-PHASE_KERNEL = {"fine": "k_fine_warp", "huff_decode": "k_huff_tfd", "huff_sync": "k_huff_sync_s", "huff_emit": "k_huff_emit_s",
+PHASE_KERNEL = {"fine": "k_fine_warp", "huff_maps": "k_tfd_maps", "huff_count": "k_tfd_count", "huff_emit": "k_tfd_emit",
                 "recon": "k_recon_warp", "pack": "k_pack_lb", "coarse_check": "k_cq_warp", "crc": "k_crc_coal",
                 "stats": "k_stats"}
 

@@ -1,0 +1,368 @@
+// One-pass Huffman decode of the varint byte stream by transfer functions.
+//
+// The reference decodes serially from bit 0 (codec.cpp:354-395); the stream
+// has no sync points.  Cut it into subsequences of kSeqBits bits; the first
+// codeword boundary at or after a subsequence's nominal start S lies in
+// [S, S + maxlen), so a subsequence's parse is described by its TRANSFER
+// FUNCTION over the maxlen possible entry offsets: entry e -> exit offset into
+// the next subsequence (a map of 16 nibbles, one 64-bit word; 15 = the parse
+// ran into the stream end).  Maps compose associatively, so the true path is
+// found by a scan — no serial chains, however long a stream stays out of
+// phase (periodic stretches keep parses desynchronised for megabits).
+//
+// Five launches; the three stream passes give each warp a tile of kTfdTile
+// consecutive subsequences staged in shared memory (coalesced, byte-swapped):
+//   K1 k_tfd_maps   every lane evaluates its subsequence's map: one cursor per
+//                   entry, always advancing the smallest position, so all live
+//                   cursors lie within maxlen bits of it (a 16-bit occupancy
+//                   mask) and two parses that meet are at the same position at
+//                   some step and merge (union-find on 4-bit cursor ids, all in
+//                   registers); a lone cursor finishes by a plain walk; a warp
+//                   scan composes the maps across the tile;
+//   K2 k_tfd_tiles  one CTA scans the tile maps: the true entry of every tile
+//                   (tile 0 starts at bit 0);
+//   K3 k_tfd_count  every lane decodes its subsequence once along the true
+//                   path: varint terminators, and whether it ends inside one;
+//   K4 k_scan_lb    exclusive scan of the terminator counts: value offsets;
+//   K5 k_tfd_emit   every lane decodes its subsequence again and writes the
+//                   zigzag codes of the varints that start in it (an open value
+//                   is finished by decoding on, <= 10 bytes), stopping at the
+//                   N-th value; the first error in stream order, the end of the
+//                   N-th varint and the padding check follow codec.cpp:75-86
+//                   and :370-375.
+// The passes have no cross-CTA waits: tiles of very different cost (parses
+// that stay apart for megabits) cannot stall their successors.
+#pragma once
+
+#include "huff.cuh"
+
+namespace mgrc_gpu {
+namespace dev {
+
+constexpr int kTfdThreads = 128;  // threads per CTA: 4 independent warp tiles sharing the decode table
+constexpr int kTfdTile = 32;      // subsequences per tile (one warp): the look-back unit
+constexpr int kTfdStage = kTfdTile * kSeqBits / 32 + kTailWords + 4;
+constexpr int kTfdStageSmem = stage_idx(kTfdStage) + 2;
+constexpr int kTfdWarpSmem = kTfdStageSmem;  // words per warp tile
+constexpr unsigned long long kNibId = 0xFEDCBA9876543210ull;  // identity map of 16 nibbles
+constexpr uint32_t kDeadEx = 15u;                              // "the parse ran into the stream end"
+
+__device__ __forceinline__ uint32_t nib(unsigned long long m, uint32_t i) {
+  return static_cast<uint32_t>(m >> (4u * i)) & 15u;
+}
+__device__ __forceinline__ unsigned long long nib_set(unsigned long long m, uint32_t i, uint32_t v) {
+  return (m & ~(15ull << (4u * i))) | (static_cast<unsigned long long>(v) << (4u * i));
+}
+// first f, then g (dead stays dead)
+__device__ __forceinline__ unsigned long long nib_then(unsigned long long f, unsigned long long g, int ne) {
+  unsigned long long r = ~0ull;
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    if (e < ne) {
+      const uint32_t x = nib(f, e);
+      r = nib_set(r, e, x == kDeadEx ? kDeadEx : nib(g, x));
+    }
+  return r;
+}
+
+// the true path through one subsequence (k_tfd_count -> k_tfd_emit)
+struct TfdSeq {
+  uint8_t entry;  // first codeword boundary at or after S (offset; kDeadEx: the stream ended before)
+  uint8_t exit;   // first boundary at or after the next S (offset; kDeadEx: stream end)
+  uint8_t lc;     // its last codeword continues a varint
+  uint8_t pad;
+};
+
+// A warp stages its tile [base, base + kTfdStage words) of the stream.
+__device__ __forceinline__ void tfd_stage(const uint32_t* __restrict__ w, uint64_t nw, uint64_t base, uint32_t* sm,
+                                          int lane) {
+  for (int i = lane; i < kTfdStage; i += 32) {
+    const uint64_t gw = (base >> 5) + i;
+    sm[stage_idx(i)] = gw < nw ? bswap32(__ldg(w + gw)) : 0u;
+  }
+  __syncwarp();
+}
+
+// Exit map of one subsequence [S, end) (S a multiple of 16).
+template <class LT>
+__device__ __forceinline__ unsigned long long tfd_map(const uint32_t* sm, const LT& lut, int maxlen, int ne,
+                                                      uint32_t S, uint32_t end, uint32_t tl) {
+  uint32_t base = S;
+  uint32_t occ = (1u << ne) - 1u;
+  unsigned long long slotid = kNibId;  // cursor id at slot (position & 15)
+  unsigned long long parent = kNibId;  // union-find parent of each cursor id
+  const bool near_end = end + 32 >= tl;
+  BitReader br;
+  br.init(sm, base);
+  while (__popc(occ) > 1 && base < end) {
+    const uint32_t id = nib(slotid, base & 15u);
+    br.refill();
+    const uint32_t l = lut_len(lut[br.peek(maxlen)]);
+    occ &= ~1u;
+    if (near_end && base + l > tl) {
+      // the stream ends inside this codeword: the cursor dies (its root keeps no live position)
+    } else if ((occ >> l) & 1u) {  // another parse is already there: merge
+      parent = nib_set(parent, id, nib(slotid, (base + l) & 15u));
+    } else {
+      slotid = nib_set(slotid, (base + l) & 15u, id);
+      occ |= 1u << l;
+    }
+    if (!occ) break;
+    const int sh = __ffs(occ) - 1;
+    occ >>= sh;
+    base += sh;
+    br.refill();
+    br.consume(static_cast<uint32_t>(sh));
+  }
+  if (__popc(occ) == 1 && base < end) {  // one parse left: walk it to the exit
+    uint32_t p = base;
+    while (p < end) {
+      br.refill();
+      const uint32_t l = lut_len(lut[br.peek(maxlen)]);
+      if (near_end && p + l > tl) break;
+      p += l;
+      br.consume(l);
+    }
+    if (p < end) {
+      occ = 0;  // died at the stream end
+    } else {
+      slotid = nib_set(slotid, p & 15u, nib(slotid, base & 15u));
+      base = p;
+    }
+  }
+  // exits of the live cursors, then every entry through its union-find root
+  unsigned long long exit_of = ~0ull;  // id -> exit offset (15: dead)
+  while (occ) {
+    const int i = __ffs(occ) - 1;
+    occ &= occ - 1;
+    const uint32_t pos = base + i;
+    exit_of = nib_set(exit_of, nib(slotid, pos & 15u), min(pos - end, 14u));
+  }
+  unsigned long long f = ~0ull;
+  for (int e = 0; e < ne; ++e) {
+    uint32_t r = e;
+    for (uint32_t q = nib(parent, r); q != r; q = nib(parent, r)) r = q;
+    f = nib_set(f, e, nib(exit_of, r));
+  }
+  return f;
+}
+
+// K1: exit maps, scanned within the tile: gmap[j] = map of subsequences
+// [tile start, j] (entry of the tile -> exit of j).
+template <bool G>
+__global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+                                                          const uint16_t* __restrict__ lut_g, int maxlen, int ne,
+                                                          uint64_t nseq, unsigned long long* __restrict__ gmap) {
+  extern __shared__ uint32_t dyn[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + (kTfdThreads / 32) * kTfdWarpSmem);
+  uint32_t* sm = dyn + wid * kTfdWarpSmem;
+  if (!G)
+    for (int k = threadIdx.x; k < (1 << maxlen); k += kTfdThreads) lut_s[k] = lut_g[k];
+  __syncthreads();
+  const Lut<G> lut{G ? lut_g : lut_s};
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * (kTfdThreads / 32) + wid;
+  if (c * kTfdTile >= nseq) return;
+  const uint64_t base = c * kTfdTile * kSeqBits;
+  tfd_stage(w, nw, base, sm, lane);
+  const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
+  const uint64_t j = c * kTfdTile + lane;
+  const uint32_t S = static_cast<uint32_t>(lane) * kSeqBits;
+  const uint32_t end = min(S + static_cast<uint32_t>(kSeqBits), tl);
+  // the last subsequence ends the stream (all dead); identity past it
+  unsigned long long g = j < nseq ? (j + 1 < nseq ? tfd_map(sm, lut, maxlen, ne, S, end, tl) : ~0ull) : kNibId;
+#pragma unroll
+  for (int d = 1; d < kTfdTile; d <<= 1) {
+    const unsigned long long h = __shfl_up_sync(0xffffffffu, g, d);
+    if (lane >= d) g = nib_then(h, g, ne);
+  }
+  if (j < nseq) gmap[j] = g;
+}
+
+// K2 (one CTA): the true entry of every tile.  Each thread composes the tile
+// maps of its chunk, a block scan combines the chunks, and each thread walks
+// its chunk from the true entry (tile 0 starts at offset 0).
+constexpr int kTfdScanThreads = 1024;
+__global__ void __launch_bounds__(kTfdScanThreads) k_tfd_tiles(const unsigned long long* __restrict__ gmap,
+                                                               uint64_t nseq, uint64_t ntile, int ne,
+                                                               uint8_t* __restrict__ etile) {
+  __shared__ unsigned long long sm[kTfdScanThreads];
+  const int t = threadIdx.x;
+  const uint64_t per = (ntile + kTfdScanThreads - 1) / kTfdScanThreads;
+  const uint64_t a = umin64(ntile, t * per), b = umin64(ntile, a + per);
+  auto tile_agg = [&](uint64_t i) { return gmap[umin64(i * kTfdTile + kTfdTile - 1, nseq - 1)]; };
+  unsigned long long f = kNibId;
+  for (uint64_t i = a; i < b; ++i) f = nib_then(f, tile_agg(i), ne);
+  sm[t] = f;
+  __syncthreads();
+  for (int d = 1; d < kTfdScanThreads; d <<= 1) {  // inclusive Hillis-Steele
+    const unsigned long long h = t >= d ? sm[t - d] : kNibId;
+    __syncthreads();
+    if (t >= d) sm[t] = nib_then(h, sm[t], ne);
+    __syncthreads();
+  }
+  uint32_t e = t > 0 ? nib(sm[t - 1], 0) : 0u;
+  for (uint64_t i = a; i < b; ++i) {
+    etile[i] = static_cast<uint8_t>(e);
+    if (e != kDeadEx) e = nib(tile_agg(i), e);
+  }
+}
+
+// K3: decode every subsequence once along the true path: terminators (for the
+// value offsets) and whether it ends inside a varint.
+template <bool G>
+__global__ void __launch_bounds__(kTfdThreads) k_tfd_count(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+                                                           const uint16_t* __restrict__ lut_g, int maxlen,
+                                                           uint64_t nseq, const unsigned long long* __restrict__ gmap,
+                                                           const uint8_t* __restrict__ etile, TfdSeq* __restrict__ seqs,
+                                                           unsigned long long* __restrict__ cnt) {
+  extern __shared__ uint32_t dyn[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + (kTfdThreads / 32) * kTfdWarpSmem);
+  uint32_t* sm = dyn + wid * kTfdWarpSmem;
+  if (!G)
+    for (int k = threadIdx.x; k < (1 << maxlen); k += kTfdThreads) lut_s[k] = lut_g[k];
+  __syncthreads();
+  const Lut<G> lut{G ? lut_g : lut_s};
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * (kTfdThreads / 32) + wid;
+  if (c * kTfdTile >= nseq) return;
+  const uint64_t base = c * kTfdTile * kSeqBits;
+  tfd_stage(w, nw, base, sm, lane);
+  const uint64_t j = c * kTfdTile + lane;
+  if (j >= nseq) return;
+  const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
+  const uint32_t S = static_cast<uint32_t>(lane) * kSeqBits;
+  const uint32_t e = etile[c];
+  const uint32_t entry = e == kDeadEx ? kDeadEx : (lane > 0 ? nib(gmap[j - 1], e) : e);
+  const uint32_t exo = e == kDeadEx ? kDeadEx : nib(gmap[j], e);
+  TfdSeq q{static_cast<uint8_t>(entry), static_cast<uint8_t>(exo), 0, 0};
+  uint32_t nterm = 0;
+  if (entry != kDeadEx) {
+    const uint32_t ex = (j + 1 == nseq || exo == kDeadEx) ? tl : S + kSeqBits + exo;
+    BitReader br;
+    br.init(sm, S + entry);
+    uint32_t last = 0;
+    count_to(br, lut, maxlen, S + entry, ex, tl, nterm, last);
+    q.lc = last ? static_cast<uint8_t>(lut_term(last) ^ 1u) : 0;
+  }
+  seqs[j] = q;
+  cnt[j] = nterm;
+}
+
+// K5: decode every subsequence along the true path and write the zigzag codes
+// of the varints that start in it.
+template <typename Z, bool G>
+__global__ void __launch_bounds__(kTfdThreads) k_tfd_emit(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+                                                          const uint16_t* __restrict__ lut_g, int maxlen,
+                                                          uint64_t nseq, uint64_t N, const TfdSeq* __restrict__ seqs,
+                                                          const unsigned long long* __restrict__ toff,
+                                                          Z* __restrict__ zz, DecodeStatus* st,
+                                                          unsigned long long* first_err) {
+  constexpr int CH = 32 / sizeof(Z);  // values per 32-byte output chunk
+  extern __shared__ uint32_t dyn[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + (kTfdThreads / 32) * kTfdWarpSmem);
+  uint32_t* sm = dyn + wid * kTfdWarpSmem;
+  __shared__ __align__(16) Z slot[kTfdThreads][CH];
+  if (!G)
+    for (int k = threadIdx.x; k < (1 << maxlen); k += kTfdThreads) lut_s[k] = lut_g[k];
+  __syncthreads();
+  const Lut<G> lut{G ? lut_g : lut_s};
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * (kTfdThreads / 32) + wid;
+  if (c * kTfdTile >= nseq) return;
+  const uint64_t base = c * kTfdTile * kSeqBits;
+  tfd_stage(w, nw, base, sm, lane);
+  const uint64_t j = c * kTfdTile + lane;
+  if (j >= nseq) return;
+  const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
+  const uint32_t S = static_cast<uint32_t>(lane) * kSeqBits;
+  const TfdSeq q = seqs[j];
+  const uint32_t entry = q.entry;
+  if (entry == kDeadEx) return;  // the true path already ran into the stream end (reported by its owner)
+  const uint32_t ex = (j + 1 == nseq || q.exit == kDeadEx) ? tl : S + kSeqBits + q.exit;
+  bool skipping = j > 0 && seqs[j - 1].lc != 0;
+  uint64_t k = toff[j];
+  if (k >= N) return;  // every value that starts here is past the N-th (never read, codec.cpp:475-481)
+  const uint64_t k_first = k + (skipping ? 1 : 0);
+  uint32_t p = S + entry;
+  Z* my = slot[threadIdx.x];
+  auto flush = [&](uint64_t upto) {  // values [chunk start, upto) of the current chunk
+    const uint64_t c0 = (upto - 1) & ~static_cast<uint64_t>(CH - 1);
+    if (c0 >= k_first && upto - c0 == CH) {
+      const uint4* src = reinterpret_cast<const uint4*>(my);
+      uint4* dst = reinterpret_cast<uint4*>(zz + c0);
+      dst[0] = src[0];
+      dst[1] = src[1];
+    } else {
+      for (uint64_t q = umax64(c0, k_first); q < upto; ++q) zz[q] = my[q & (CH - 1)];
+    }
+  };
+  const bool near_end = ex + 256 >= tl;  // only then can a codeword run past the stream end
+  uint32_t err = 0, err_at = 0, wide = 0;
+  BitReader br;
+  br.init(sm, p);
+  if (skipping) {  // the value open at the entry began in the previous subsequence: skip to its end
+    for (;;) {
+      br.refill();
+      const uint32_t ent = lut[br.peek(maxlen)];
+      const uint32_t l = lut_len(ent);
+      if (p + l > tl) return;  // truncated inside that value: its owner (the previous thread) reports it
+      p += l;
+      br.consume(l);
+      if (lut_term(ent)) {
+        ++k;
+        break;
+      }
+    }
+  }
+  const uint64_t room64 = k < N ? N - k : 0;
+  const uint32_t room = static_cast<uint32_t>(umin64(room64, 0xFFFFFFFFu));
+  const uint32_t k_lo = static_cast<uint32_t>(k);
+  uint32_t kk = 0;
+  uint64_t acc = 0;
+  uint32_t sh = 0;  // 7 x bytes of the open value
+  while (!err) {
+    if (p >= ex && sh == 0) break;
+    if (kk >= room) break;
+    br.refill();
+    const uint32_t ent = lut[br.peek(maxlen)];
+    const uint32_t l = lut_len(ent);
+    if (near_end && p + l > tl) {  // the stream ends inside an open value
+      err = 2;
+      err_at = tl;
+      break;
+    }
+    if (sh == 63 && (ent & 0xFEu)) {  // varint overflows 64 bits (codec.cpp:80-81)
+      err = 1;
+      err_at = p;
+      break;
+    }
+    p += l;
+    br.consume(l);
+    acc |= static_cast<uint64_t>(ent & 0x7Fu) << sh;
+    if (!lut_term(ent)) {
+      sh += 7;
+      continue;
+    }
+    if (sizeof(Z) == 4 && (acc >> 32)) wide = 1;
+    const uint32_t ki = k_lo + kk;
+    my[ki & (CH - 1)] = static_cast<Z>(acc);
+    if (((ki + 1) & (CH - 1)) == 0) flush(k + kk + 1);
+    if (kk + 1 == room && room64 <= 0xFFFFFFFFu) {  // the N-th value: exhausted_clean (codec.cpp:370-375)
+      st->end_bit = base + p;
+      const uint32_t rest = tl - p;
+      br.refill();
+      st->clean = rest < 8 && (rest == 0 || (static_cast<uint32_t>(br.buf >> 32) >> (32 - rest)) == 0);
+    }
+    ++kk;
+    acc = 0;
+    sh = 0;
+  }
+  k += kk;
+  if ((k & (CH - 1)) != 0 && k > k_first) flush(k);
+  if (err) atomicMin(first_err, ((base + err_at) << 2) | err);  // the first error in stream order
+  if (wide) atomicOr(&st->wide, 1u);
+}
+
+}  // namespace dev
+}  // namespace mgrc_gpu

@@ -30,6 +30,7 @@
 #include "kernels.cuh"
 #include "rows.cuh"
 #include "huff.cuh"
+#include "huff_tf.cuh"
 #include "serial_sum.cuh"
 #include "pipeline.hpp"
 #include "context.hpp"
@@ -993,6 +994,10 @@ static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords
 static size_t sync_smem(int maxlen) { return static_cast<size_t>(kSyncSmemWords) * 4 + lut_smem(maxlen); }
 static size_t tf_smem(int maxlen) { return tf_smem_base() + lut_smem(maxlen); }
 
+static size_t tfd_smem(int maxlen) {
+  return static_cast<size_t>((kTfdThreads / 32) * kTfdWarpSmem) * 4 + lut_smem(maxlen);
+}
+
 static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
 
 static void huff_smem_optin() {
@@ -1016,6 +1021,15 @@ static void huff_smem_optin() {
                           static_cast<int>(tf_smem(kSmemLutMaxLen))));
   CK(cudaFuncSetAttribute(k_huff_fix_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(fix_smem(kMaxCodeLen))));
+  const int mt = static_cast<int>(tfd_smem(kSmemLutMaxLen));
+  CK(cudaFuncSetAttribute(k_tfd_maps<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_maps<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_emit<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_emit<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_emit<unsigned long long, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_emit<unsigned long long, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   done_mask |= bit;
 }
 
@@ -1206,6 +1220,84 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         const uint32_t* w = reinterpret_cast<const uint32_t*>(body);
         const uint64_t nw = (body_len + 64) / 4;
         huff_smem_optin();
+        static const bool old_decoder = [] {
+          const char* e = std::getenv("MGRC_DECODER");
+          return e && std::strcmp(e, "sync") == 0;
+        }();
+        if (!old_decoder) {
+          // one-pass transfer-function decoder (huff_tf.cuh)
+          int minlen = 99;
+          for (int b = 0; b < 256; ++b)
+            if (table.lengths[b]) minlen = std::min<int>(minlen, table.lengths[b]);
+          const int ne = (minlen == maxlen && kSeqBits % maxlen == 0) ? 1 : maxlen;  // equal lengths: aligned
+          const uint64_t ntile = (nseq + kTfdTile - 1) / kTfdTile;
+          const unsigned ncta = static_cast<unsigned>((ntile + kTfdThreads / 32 - 1) / (kTfdThreads / 32));
+          const bool glut = lut_global(maxlen);
+          const size_t smem = tfd_smem(maxlen);
+          auto* gmap = ctx.tftab.get<unsigned long long>(nseq * 8);
+          auto* etile = ctx.tfst.get<uint8_t>(ntile + 16);
+          auto* seqs = ctx.seq.get<TfdSeq>(nseq * sizeof(TfdSeq));
+          auto* cnt = ctx.tiles.get<unsigned long long>(nseq * 8);
+          auto* toff = ctx.scan.get<unsigned long long>((nseq + 1) * 8);
+          const uint64_t nst = (nseq + kScanTile - 1) / kScanTile;
+          auto* lbst = ctx.lbws.get<unsigned long long>(nst * 8 + 32);
+          auto* lbticket = reinterpret_cast<unsigned int*>(lbst + nst);
+          auto* first_err = reinterpret_cast<unsigned long long*>(lbst + nst + 2);
+          prof.begin("huff_maps", static_cast<double>(body_len));
+          if (glut)
+            k_tfd_maps<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap);
+          else
+            k_tfd_maps<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap);
+          check_launch("k_tfd_maps");
+          k_tfd_tiles<<<1, kTfdScanThreads, 0, s>>>(gmap, nseq, ntile, ne, etile);
+          check_launch("k_tfd_tiles");
+          prof.end();
+          prof.begin("huff_count", static_cast<double>(body_len));
+          if (glut)
+            k_tfd_count<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, gmap, etile, seqs, cnt);
+          else
+            k_tfd_count<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, gmap, etile, seqs, cnt);
+          check_launch("k_tfd_count");
+          CK(cudaMemsetAsync(lbst, 0, nst * 8 + 16, s));
+          k_scan_lb<<<static_cast<unsigned>(nst), kScanThreads, 0, s>>>(cnt, toff, nseq, lbst, lbticket);
+          check_launch("k_scan_lb");
+          prof.end();
+          for (;;) {
+            CK(cudaMemsetAsync(first_err, 0xFF, 8, s));
+            DecodeStatus init{~0ull, 0u, 0u, 0u};
+            CK(cudaMemcpyAsync(&sd->dstat, &init, sizeof init, cudaMemcpyHostToDevice, s));
+            prof.begin("huff_emit", static_cast<double>(body_len) + static_cast<double>(N) * (wide ? 8 : 4));
+            auto launch = [&](auto* zz) {
+              using Z = std::remove_pointer_t<decltype(zz)>;
+              if (glut)
+                k_tfd_emit<Z, true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, toff, zz,
+                                                                     &sd->dstat, first_err);
+              else
+                k_tfd_emit<Z, false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, toff, zz,
+                                                                      &sd->dstat, first_err);
+              check_launch("k_tfd_emit");
+            };
+            if (wide) launch(ctx.zz.get<unsigned long long>(N * 8));
+            else launch(ctx.zz.get<uint32_t>(N * 4));
+            prof.end();
+            unsigned long long ferr = 0;
+            CK(cudaMemcpyAsync(&sh->dstat, &sd->dstat, sizeof(DecodeStatus), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&sh->red_bits, first_err, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            ferr = sh->red_bits;
+            if (ferr != ~0ull && (ferr & 3u) == 1u) raise(Errc::corrupt_stream, "varint overflows 64 bits");
+            if (ferr != ~0ull || sh->dstat.end_bit == ~0ull)
+              raise(Errc::corrupt_stream, info.codec_id == 2 ? "Huffman stream truncated" : "truncated varint stream");
+            if (!sh->dstat.clean)
+              raise(Errc::corrupt_stream, info.codec_id == 2 ? "trailing bits after Huffman stream"
+                                                             : "trailing bytes after varint stream");
+            if (sh->dstat.wide && !wide) {
+              wide = true;
+              continue;
+            }
+            break;
+          }
+        } else {
         prof.begin("huff_sync", static_cast<double>(body_len));
         const uint64_t nblk = (nseq + kSyncReal - 1) / kSyncReal;
         CK(cudaMemsetAsync(&sd->raw_wide, 0, 4, s));  // reused as the "rounds capped" flag
@@ -1325,6 +1417,7 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
           }
           break;
         }
+        }  // old decoder
       }
     }
     prof.begin("recon", static_cast<double>(N) * ((wide ? 8 : 4) + dtype_size(info.dtype)));
