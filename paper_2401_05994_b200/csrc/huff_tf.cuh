@@ -83,68 +83,73 @@ __device__ __forceinline__ void tfd_stage(const uint32_t* __restrict__ w, uint64
   __syncwarp();
 }
 
-// Exit map of one subsequence [S, end) (S a multiple of 16).
-template <class LT>
-__device__ __forceinline__ unsigned long long tfd_map(const uint32_t* sm, const LT& lut, int maxlen, int ne,
-                                                      uint32_t S, uint32_t end, uint32_t tl) {
+// Exit map of one subsequence [S, end).
+//
+// Live cursors are kept as a 64-bit map `r` of 16 nibbles over the positions
+// [base, base + 16): nibble i = 1 + id of the cursor at base + i (0: none).
+// The smallest cursor (nibble 0) is always the one decoded; its codeword of
+// length l <= 15 lands on nibble l — occupied means two parses met (merge:
+// union-find parent of the cursor id) — and the map is rebased to the next
+// smallest cursor by one shift.  Everything stays in registers.
+template <bool NEAR_END, class LT>
+__device__ __forceinline__ unsigned long long tfd_map_impl(const uint32_t* sm, const LT& lut, int maxlen, int ne,
+                                                           uint32_t S, uint32_t end, uint32_t tl) {
   uint32_t base = S;
-  uint32_t occ = (1u << ne) - 1u;
-  unsigned long long slotid = kNibId;  // cursor id at slot (position & 15)
+  unsigned long long r = 0;
+  for (int e = 0; e < ne; ++e) r |= static_cast<unsigned long long>(e + 1) << (4 * e);
   unsigned long long parent = kNibId;  // union-find parent of each cursor id
-  const bool near_end = end + 32 >= tl;
   BitReader br;
   br.init(sm, base);
-  while (__popc(occ) > 1 && base < end) {
-    const uint32_t id = nib(slotid, base & 15u);
+  while ((r & ~15ull) && base < end) {
+    const uint32_t id = static_cast<uint32_t>(r) & 15u;
     br.refill();
     const uint32_t l = lut_len(lut[br.peek(maxlen)]);
-    occ &= ~1u;
-    if (near_end && base + l > tl) {
-      // the stream ends inside this codeword: the cursor dies (its root keeps no live position)
-    } else if ((occ >> l) & 1u) {  // another parse is already there: merge
-      parent = nib_set(parent, id, nib(slotid, (base + l) & 15u));
+    r &= ~15ull;
+    if (NEAR_END && base + l > tl) {
+      // the stream ends inside this codeword: the cursor dies
     } else {
-      slotid = nib_set(slotid, (base + l) & 15u, id);
-      occ |= 1u << l;
+      const uint32_t there = static_cast<uint32_t>(r >> (4u * l)) & 15u;
+      if (there) parent = nib_set(parent, id - 1u, there - 1u);  // two parses met: merge
+      else r |= static_cast<unsigned long long>(id) << (4u * l);
     }
-    if (!occ) break;
-    const int sh = __ffs(occ) - 1;
-    occ >>= sh;
+    if (!r) break;
+    const uint32_t sh = static_cast<uint32_t>(__ffsll(static_cast<long long>(r)) - 1) >> 2;
+    r >>= 4u * sh;
     base += sh;
-    br.refill();
-    br.consume(static_cast<uint32_t>(sh));
+    br.consume(sh);
   }
-  if (__popc(occ) == 1 && base < end) {  // one parse left: walk it to the exit
+  if (r && !(r & ~15ull) && base < end) {  // one parse left: walk it to the exit
     uint32_t p = base;
     while (p < end) {
       br.refill();
       const uint32_t l = lut_len(lut[br.peek(maxlen)]);
-      if (near_end && p + l > tl) break;
+      if (NEAR_END && p + l > tl) break;
       p += l;
       br.consume(l);
     }
-    if (p < end) {
-      occ = 0;  // died at the stream end
-    } else {
-      slotid = nib_set(slotid, p & 15u, nib(slotid, base & 15u));
-      base = p;
-    }
+    if (p < end) r = 0;  // died at the stream end
+    else base = p;
   }
   // exits of the live cursors, then every entry through its union-find root
   unsigned long long exit_of = ~0ull;  // id -> exit offset (15: dead)
-  while (occ) {
-    const int i = __ffs(occ) - 1;
-    occ &= occ - 1;
-    const uint32_t pos = base + i;
-    exit_of = nib_set(exit_of, nib(slotid, pos & 15u), min(pos - end, 14u));
+  for (uint32_t i = 0; r; ++i, r >>= 4) {
+    const uint32_t id = static_cast<uint32_t>(r) & 15u;
+    if (id) exit_of = nib_set(exit_of, id - 1u, min(base + i - end, 14u));
   }
   unsigned long long f = ~0ull;
   for (int e = 0; e < ne; ++e) {
-    uint32_t r = e;
-    for (uint32_t q = nib(parent, r); q != r; q = nib(parent, r)) r = q;
-    f = nib_set(f, e, nib(exit_of, r));
+    uint32_t q = e;
+    for (uint32_t pq = nib(parent, q); pq != q; pq = nib(parent, q)) q = pq;
+    f = nib_set(f, e, nib(exit_of, q));
   }
   return f;
+}
+
+template <class LT>
+__device__ __forceinline__ unsigned long long tfd_map(const uint32_t* sm, const LT& lut, int maxlen, int ne,
+                                                      uint32_t S, uint32_t end, uint32_t tl) {
+  return end + 32 >= tl ? tfd_map_impl<true>(sm, lut, maxlen, ne, S, end, tl)
+                        : tfd_map_impl<false>(sm, lut, maxlen, ne, S, end, tl);
 }
 
 // K1: exit maps, scanned within the tile: gmap[j] = map of subsequences
@@ -249,16 +254,100 @@ __global__ void __launch_bounds__(kTfdThreads) k_tfd_count(const uint32_t* __res
   cnt[j] = nterm;
 }
 
+// The varints of one subsequence: `nv` values starting at index k_first (the
+// first one at bit p, after the skip of a value begun earlier); NE: the
+// stream end is within reach (codewords may run past it).
+template <bool NE, typename Z, class LT>
+__device__ __forceinline__ void tfd_emit_values(const uint32_t* sm, const LT& lut, int maxlen, uint32_t p,
+                                                uint32_t tl, bool skipping, uint64_t k_first, uint32_t nv,
+                                                bool has_last, uint64_t base, Z* __restrict__ zz, Z* my,
+                                                DecodeStatus* st, unsigned long long* first_err) {
+  constexpr int CH = 32 / sizeof(Z);  // values per 32-byte output chunk
+  auto flush = [&](uint64_t upto) {   // values [chunk start, upto) of the current chunk
+    const uint64_t c0 = (upto - 1) & ~static_cast<uint64_t>(CH - 1);
+    if (c0 >= k_first && upto - c0 == CH) {
+      const uint4* src = reinterpret_cast<const uint4*>(my);
+      uint4* dst = reinterpret_cast<uint4*>(zz + c0);
+      dst[0] = src[0];
+      dst[1] = src[1];
+    } else {
+      for (uint64_t q = umax64(c0, k_first); q < upto; ++q) zz[q] = my[q & (CH - 1)];
+    }
+  };
+  BitReader br;
+  br.init(sm, p);
+  if (skipping) {  // the value open at the entry began in the previous subsequence: skip to its end
+    for (;;) {
+      br.refill();
+      const uint32_t ent = lut[br.peek(maxlen)];
+      const uint32_t l = lut_len(ent);
+      if (NE && p + l > tl) return;  // truncated inside that value: its owner (the previous lane) reports it
+      p += l;
+      br.consume(l);
+      if (lut_term(ent)) break;
+    }
+  }
+  uint32_t err = 0, err_at = 0, wide = 0, v = 0;
+  uint32_t ki = static_cast<uint32_t>(k_first);  // low bits pick the chunk slot
+  for (; v < nv; ++v) {
+    br.refill();
+    uint32_t ent = lut[br.peek(maxlen)];
+    uint32_t l = lut_len(ent);
+    if (NE && p + l > tl) {
+      err = 2, err_at = tl;
+      break;
+    }
+    p += l;
+    br.consume(l);
+    uint64_t acc = ent & 0x7Fu;
+    if (!lut_term(ent)) {  // continuation bytes (codec.cpp:75-86)
+      for (uint32_t sh = 7;; sh += 7) {
+        br.refill();
+        ent = lut[br.peek(maxlen)];
+        l = lut_len(ent);
+        if (NE && p + l > tl) {
+          err = 2, err_at = tl;
+          break;
+        }
+        if (sh == 63 && (ent & 0xFEu)) {  // varint overflows 64 bits (codec.cpp:80-81)
+          err = 1, err_at = p;
+          break;
+        }
+        p += l;
+        br.consume(l);
+        acc |= static_cast<uint64_t>(ent & 0x7Fu) << sh;
+        if (lut_term(ent)) break;
+      }
+      if (err) break;
+      if (sizeof(Z) == 4 && (acc >> 32)) wide = 1;
+    }
+    my[ki & (CH - 1)] = static_cast<Z>(acc);
+    ++ki;
+    if ((ki & (CH - 1)) == 0) flush(k_first + v + 1);
+  }
+  const uint64_t kend = k_first + v;
+  if ((kend & (CH - 1)) != 0 && kend > k_first) flush(kend);
+  if (!err && has_last) {  // the N-th value ends here: exhausted_clean (codec.cpp:370-375)
+    st->end_bit = base + p;
+    const uint32_t rest = tl - p;
+    br.refill();
+    st->clean = rest < 8 && (rest == 0 || (static_cast<uint32_t>(br.buf >> 32) >> (32 - rest)) == 0);
+  }
+  if (err) atomicMin(first_err, ((base + err_at) << 2) | err);  // the first error in stream order
+  if (wide) atomicOr(&st->wide, 1u);
+}
+
 // K5: decode every subsequence along the true path and write the zigzag codes
 // of the varints that start in it.
 template <typename Z, bool G>
 __global__ void __launch_bounds__(kTfdThreads) k_tfd_emit(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                           const uint16_t* __restrict__ lut_g, int maxlen,
                                                           uint64_t nseq, uint64_t N, const TfdSeq* __restrict__ seqs,
+                                                          const unsigned long long* __restrict__ cnt,
                                                           const unsigned long long* __restrict__ toff,
                                                           Z* __restrict__ zz, DecodeStatus* st,
                                                           unsigned long long* first_err) {
-  constexpr int CH = 32 / sizeof(Z);  // values per 32-byte output chunk
+  constexpr int CH = 32 / sizeof(Z);
   extern __shared__ uint32_t dyn[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + (kTfdThreads / 32) * kTfdWarpSmem);
@@ -277,91 +366,22 @@ __global__ void __launch_bounds__(kTfdThreads) k_tfd_emit(const uint32_t* __rest
   const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
   const uint32_t S = static_cast<uint32_t>(lane) * kSeqBits;
   const TfdSeq q = seqs[j];
-  const uint32_t entry = q.entry;
-  if (entry == kDeadEx) return;  // the true path already ran into the stream end (reported by its owner)
+  if (q.entry == kDeadEx) return;  // the true path already ran into the stream end (reported by its owner)
   const uint32_t ex = (j + 1 == nseq || q.exit == kDeadEx) ? tl : S + kSeqBits + q.exit;
-  bool skipping = j > 0 && seqs[j - 1].lc != 0;
-  uint64_t k = toff[j];
-  if (k >= N) return;  // every value that starts here is past the N-th (never read, codec.cpp:475-481)
-  const uint64_t k_first = k + (skipping ? 1 : 0);
-  uint32_t p = S + entry;
-  Z* my = slot[threadIdx.x];
-  auto flush = [&](uint64_t upto) {  // values [chunk start, upto) of the current chunk
-    const uint64_t c0 = (upto - 1) & ~static_cast<uint64_t>(CH - 1);
-    if (c0 >= k_first && upto - c0 == CH) {
-      const uint4* src = reinterpret_cast<const uint4*>(my);
-      uint4* dst = reinterpret_cast<uint4*>(zz + c0);
-      dst[0] = src[0];
-      dst[1] = src[1];
-    } else {
-      for (uint64_t q = umax64(c0, k_first); q < upto; ++q) zz[q] = my[q & (CH - 1)];
-    }
-  };
-  const bool near_end = ex + 256 >= tl;  // only then can a codeword run past the stream end
-  uint32_t err = 0, err_at = 0, wide = 0;
-  BitReader br;
-  br.init(sm, p);
-  if (skipping) {  // the value open at the entry began in the previous subsequence: skip to its end
-    for (;;) {
-      br.refill();
-      const uint32_t ent = lut[br.peek(maxlen)];
-      const uint32_t l = lut_len(ent);
-      if (p + l > tl) return;  // truncated inside that value: its owner (the previous thread) reports it
-      p += l;
-      br.consume(l);
-      if (lut_term(ent)) {
-        ++k;
-        break;
-      }
-    }
-  }
-  const uint64_t room64 = k < N ? N - k : 0;
-  const uint32_t room = static_cast<uint32_t>(umin64(room64, 0xFFFFFFFFu));
-  const uint32_t k_lo = static_cast<uint32_t>(k);
-  uint32_t kk = 0;
-  uint64_t acc = 0;
-  uint32_t sh = 0;  // 7 x bytes of the open value
-  while (!err) {
-    if (p >= ex && sh == 0) break;
-    if (kk >= room) break;
-    br.refill();
-    const uint32_t ent = lut[br.peek(maxlen)];
-    const uint32_t l = lut_len(ent);
-    if (near_end && p + l > tl) {  // the stream ends inside an open value
-      err = 2;
-      err_at = tl;
-      break;
-    }
-    if (sh == 63 && (ent & 0xFEu)) {  // varint overflows 64 bits (codec.cpp:80-81)
-      err = 1;
-      err_at = p;
-      break;
-    }
-    p += l;
-    br.consume(l);
-    acc |= static_cast<uint64_t>(ent & 0x7Fu) << sh;
-    if (!lut_term(ent)) {
-      sh += 7;
-      continue;
-    }
-    if (sizeof(Z) == 4 && (acc >> 32)) wide = 1;
-    const uint32_t ki = k_lo + kk;
-    my[ki & (CH - 1)] = static_cast<Z>(acc);
-    if (((ki + 1) & (CH - 1)) == 0) flush(k + kk + 1);
-    if (kk + 1 == room && room64 <= 0xFFFFFFFFu) {  // the N-th value: exhausted_clean (codec.cpp:370-375)
-      st->end_bit = base + p;
-      const uint32_t rest = tl - p;
-      br.refill();
-      st->clean = rest < 8 && (rest == 0 || (static_cast<uint32_t>(br.buf >> 32) >> (32 - rest)) == 0);
-    }
-    ++kk;
-    acc = 0;
-    sh = 0;
-  }
-  k += kk;
-  if ((k & (CH - 1)) != 0 && k > k_first) flush(k);
-  if (err) atomicMin(first_err, ((base + err_at) << 2) | err);  // the first error in stream order
-  if (wide) atomicOr(&st->wide, 1u);
+  const bool skipping = j > 0 && seqs[j - 1].lc != 0;
+  const uint64_t k_first = toff[j] + (skipping ? 1 : 0);
+  if (k_first >= N) return;  // every value that starts here is past the N-th (never read, codec.cpp:475-481)
+  // values that start here: the terminators in [entry, exit), less the one
+  // closing a value begun earlier, plus the value left open at the exit
+  const uint64_t nstart = cnt[j] - (skipping ? 1 : 0) + q.lc;
+  const bool has_last = k_first + nstart >= N;
+  const uint32_t nv = static_cast<uint32_t>(umin64(nstart, N - k_first));
+  if (ex + 256 >= tl)
+    tfd_emit_values<true>(sm, lut, maxlen, S + q.entry, tl, skipping, k_first, nv, has_last, base, zz,
+                          slot[threadIdx.x], st, first_err);
+  else
+    tfd_emit_values<false>(sm, lut, maxlen, S + q.entry, tl, skipping, k_first, nv, has_last, base, zz,
+                           slot[threadIdx.x], st, first_err);
 }
 
 }  // namespace dev

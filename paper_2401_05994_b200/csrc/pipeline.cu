@@ -1270,10 +1270,10 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
             auto launch = [&](auto* zz) {
               using Z = std::remove_pointer_t<decltype(zz)>;
               if (glut)
-                k_tfd_emit<Z, true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, toff, zz,
+                k_tfd_emit<Z, true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, cnt, toff, zz,
                                                                      &sd->dstat, first_err);
               else
-                k_tfd_emit<Z, false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, toff, zz,
+                k_tfd_emit<Z, false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, cnt, toff, zz,
                                                                       &sd->dstat, first_err);
               check_launch("k_tfd_emit");
             };
