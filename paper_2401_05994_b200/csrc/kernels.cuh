@@ -878,30 +878,13 @@ static __global__ void __launch_bounds__(kCrcThreads) k_crc_fold(const uint32_t*
 }
 
 // ---------------------------------------------------------------------------
-// Self-synchronising parallel Huffman decode of the varint byte stream.
-// The format has no sync points (codec.cpp:399-418), so the stream is cut
-// into fixed subsequences of kSeqBits bits; each subsequence is decoded from
-// a guessed start, and the start of subsequence j+1 is corrected to the exit
-// (first codeword boundary past its end) of subsequence j until every
-// boundary agrees (prefix codes resynchronise within a few codewords).
+// Huffman decode (huff.cuh, huff_tf.cuh): the coded stream is cut into
+// subsequences of kSeqBits bits (the unit of the transfer-function scan).
 
 #ifndef MGRC_SEQ_BITS
 #define MGRC_SEQ_BITS 1024
 #endif
 constexpr int kSeqBits = MGRC_SEQ_BITS;
-constexpr int kDecThreads = 128;
-
-struct SeqInfo {
-  unsigned long long start, exit;
-  uint32_t nsym, nterm;
-  uint32_t last_cont;  // last decoded symbol has the continuation bit
-  uint32_t pad;
-};
-
-static __global__ void k_seq_counts(const SeqInfo* __restrict__ seq, uint64_t nseq, unsigned long long* __restrict__ nterm) {
-  const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (j < nseq) nterm[j] = seq[j].nterm;
-}
 
 struct DecodeStatus {
   unsigned long long end_bit;  // bit position after the N-th varint (ULLONG_MAX: not reached)

@@ -11,8 +11,8 @@
 //    K5  k_pack_lb + k_pack_edges               single-pass look-back bit packing
 //    K5b k_crc_coal / k_crc_fold / k_crc_finish CRC-32 of the payload
 //  decompress (container.cpp:210-261)
-//    K5b CRC (auxiliary stream) → K6 k_huff_sync_s / k_huff_fix_s / k_tf_* (self-
-//    synchronising decode) → k_seq_counts + k_scan_lb → k_huff_emit_s → K7
+//    K5b CRC (auxiliary stream) → K6 transfer-function decode (huff_tf.cuh:
+//    k_tfd_maps → k_tfd_tiles → k_tfd_count → k_scan_lb → k_tfd_emit) → K7
 //    k_recon_coarse + k_inverse_box + k_inv_warp (coarse box) → k_recon_warp (+narrow)
 #include <cuda_runtime.h>
 
@@ -987,18 +987,12 @@ ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len) {
   }
 }
 
-static size_t tf_smem_base() { return static_cast<size_t>(stage_idx(kTfStage) + 2 + 4 * kTfThreads * kTfMapStride) * 4; }
 static bool lut_global(int maxlen) { return maxlen > kSmemLutMaxLen; }
 static size_t lut_smem(int maxlen) { return lut_global(maxlen) ? 0 : (sizeof(uint16_t) << maxlen); }
-static size_t huff_smem(int maxlen) { return static_cast<size_t>(kStageSmemWords) * 4 + lut_smem(maxlen); }
-static size_t sync_smem(int maxlen) { return static_cast<size_t>(kSyncSmemWords) * 4 + lut_smem(maxlen); }
-static size_t tf_smem(int maxlen) { return tf_smem_base() + lut_smem(maxlen); }
 
 static size_t tfd_smem(int maxlen) {
   return static_cast<size_t>((kTfdThreads / 32) * kTfdWarpSmem) * 4 + lut_smem(maxlen);
 }
-
-static size_t fix_smem(int maxlen) { return static_cast<size_t>(stage_idx(kFixWords) + 2) * 4 + (sizeof(uint16_t) << maxlen); }
 
 static void huff_smem_optin() {
   // the attribute is per device: track the opt-in per (thread, device)
@@ -1007,20 +1001,6 @@ static void huff_smem_optin() {
   CK(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
   if (done_mask & bit) return;
-  const int mx = static_cast<int>(huff_smem(kSmemLutMaxLen));
-  const int ms = static_cast<int>(sync_smem(kSmemLutMaxLen));
-  CK(cudaFuncSetAttribute(k_huff_sync_s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ms));
-  CK(cudaFuncSetAttribute(k_huff_sync_s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ms));
-  CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(k_huff_emit_s<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(k_huff_emit_s<unsigned long long, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  CK(cudaFuncSetAttribute(k_tf_tables<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(tf_smem(kSmemLutMaxLen))));
-  CK(cudaFuncSetAttribute(k_tf_tables<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(tf_smem(kSmemLutMaxLen))));
-  CK(cudaFuncSetAttribute(k_huff_fix_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(fix_smem(kMaxCodeLen))));
   const int mt = static_cast<int>(tfd_smem(kSmemLutMaxLen));
   CK(cudaFuncSetAttribute(k_tfd_maps<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   CK(cudaFuncSetAttribute(k_tfd_maps<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
@@ -1031,20 +1011,6 @@ static void huff_smem_optin() {
   CK(cudaFuncSetAttribute(k_tfd_emit<unsigned long long, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   CK(cudaFuncSetAttribute(k_tfd_emit<unsigned long long, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   done_mask |= bit;
-}
-
-template <typename Z>
-static void decode_emit(Context& ctx, const uint32_t* w, uint64_t nw, uint64_t T, const uint16_t* lut, int maxlen,
-                        uint64_t nseq, const SeqInfo* seq, const unsigned long long* toff, uint64_t N, Z* zz,
-                        DecodeStatus* st) {
-  const unsigned grid = static_cast<unsigned>((nseq + kEmitThreads - 1) / kEmitThreads);
-  if (lut_global(maxlen))
-    k_huff_emit_s<Z, true><<<grid, kEmitThreads, huff_smem(maxlen), ctx.stream>>>(w, nw, T, lut, maxlen, nseq, seq,
-                                                                                 toff, N, zz, st);
-  else
-    k_huff_emit_s<Z, false><<<grid, kEmitThreads, huff_smem(maxlen), ctx.stream>>>(w, nw, T, lut, maxlen, nseq, seq,
-                                                                                  toff, N, zz, st);
-  check_launch("k_huff_emit_s");
 }
 
 template <typename Z>
@@ -1216,16 +1182,10 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         const int maxlen = table.max_len;
         const uint64_t T = body_len * 8;
         const uint64_t nseq = std::max<uint64_t>(1, (T + kSeqBits - 1) / kSeqBits);
-        auto* seq = ctx.seq.get<SeqInfo>(nseq * sizeof(SeqInfo));
         const uint32_t* w = reinterpret_cast<const uint32_t*>(body);
         const uint64_t nw = (body_len + 64) / 4;
         huff_smem_optin();
-        static const bool old_decoder = [] {
-          const char* e = std::getenv("MGRC_DECODER");
-          return e && std::strcmp(e, "sync") == 0;
-        }();
-        if (!old_decoder) {
-          // one-pass transfer-function decoder (huff_tf.cuh)
+          // transfer-function decoder (huff_tf.cuh)
           int minlen = 99;
           for (int b = 0; b < 256; ++b)
             if (table.lengths[b]) minlen = std::min<int>(minlen, table.lengths[b]);
@@ -1297,127 +1257,6 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
             }
             break;
           }
-        } else {
-        prof.begin("huff_sync", static_cast<double>(body_len));
-        const uint64_t nblk = (nseq + kSyncReal - 1) / kSyncReal;
-        CK(cudaMemsetAsync(&sd->raw_wide, 0, 4, s));  // reused as the "rounds capped" flag
-        if (lut_global(maxlen))
-          k_huff_sync_s<true><<<static_cast<unsigned>(nblk), kSyncThreads, sync_smem(maxlen), s>>>(
-              w, nw, T, lut, maxlen, nseq, seq, &sd->raw_wide);
-        else
-          k_huff_sync_s<false><<<static_cast<unsigned>(nblk), kSyncThreads, sync_smem(maxlen), s>>>(
-              w, nw, T, lut, maxlen, nseq, seq, &sd->raw_wide);
-        check_launch("k_huff_sync_s");
-        // CTA edges: short chains are re-walked serially (two rounds at most) ...
-        static const int fix_rounds = [] {
-          const char* e = std::getenv("MGRC_FIX_ROUNDS");
-          return e ? std::atoi(e) : 2;
-        }();
-        bool pending = fix_rounds == 0 && nblk > 1;  // no serial edge walks: every bad edge goes to the tables
-        for (int it = 0; nblk > 1 && it < fix_rounds; ++it) {
-          CK(cudaMemsetAsync(&sd->fix_changed, 0, 4, s));
-          k_huff_fix_s<<<static_cast<unsigned>(nblk - 1), 32, fix_smem(maxlen), s>>>(w, nw, T, lut, maxlen, nseq, seq,
-                                                                                  &sd->fix_changed);
-          check_launch("k_huff_fix_s");
-          CK(cudaMemcpyAsync(&sh->fix_changed, &sd->fix_changed, 4, cudaMemcpyDeviceToHost, s));
-          CK(cudaStreamSynchronize(s));
-          pending = sh->fix_changed != 0;
-          if (sh->fix_changed & 2u) break;  // a walk hit its cap: the tables resolve the rest
-          if (!pending) break;
-        }
-        // ... long ones (periodic stretches that stay out of phase for megabits) are resolved a window
-        // at a time by transfer tables composed with a parallel scan.
-        int tf_windows = 0;
-        CK(cudaMemcpyAsync(&sh->raw_wide, &sd->raw_wide, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        pending = pending || sh->raw_wide != 0;  // some CTA left an in-CTA chain open
-        for (uint64_t guard = 0; pending; ++guard) {
-          if (guard > nseq / 512 + 16) raise(Errc::invalid_state, "internal: Huffman resynchronisation did not converge");
-          constexpr unsigned kCap = 4096;
-          auto* lst = ctx.lbws.get<unsigned long long>(kCap * 8 + 16);
-          auto* nl = reinterpret_cast<unsigned int*>(lst + kCap);
-          CK(cudaMemsetAsync(nl, 0, 4, s));
-          k_seq_mismatch<<<static_cast<unsigned>((nseq + 255) / 256), 256, 0, s>>>(seq, nseq, lst, nl, kCap);
-          check_launch("k_seq_mismatch");
-          unsigned int nmis = 0;
-          CK(cudaMemcpyAsync(&nmis, nl, 4, cudaMemcpyDeviceToHost, s));
-          CK(cudaStreamSynchronize(s));
-          if (nmis == 0) break;
-          std::vector<unsigned long long> js(std::min<unsigned>(nmis, kCap));
-          CK(cudaMemcpyAsync(js.data(), lst, js.size() * 8, cudaMemcpyDeviceToHost, s));
-          CK(cudaStreamSynchronize(s));
-          std::sort(js.begin(), js.end());
-          if (const char* dbg = std::getenv("MGRC_DEBUG"); dbg && dbg[0] == '2' && guard < 40) {
-            std::fprintf(stderr, "[mgrc] iter %llu: %u mismatches, first:", static_cast<unsigned long long>(guard), nmis);
-            for (size_t q = 0; q < js.size() && q < 6; ++q) std::fprintf(stderr, " %llu", js[q]);
-            std::fprintf(stderr, "\n");
-          }
-          // non-overlapping windows from every mismatch, all resolved in one pair of launches; windows
-          // whose entry is not yet true get rewritten by a later round (the earliest one always is)
-          // a chain still open after a round is long: the windows grow ×4 per round (512 … 32768
-          // subsequences), so a megabit stretch takes a few rounds instead of one per 512 kbit
-          const uint32_t wlen = static_cast<uint32_t>(kTfWin) << (2 * std::min<uint64_t>(guard, 3));
-          std::vector<unsigned long long> starts;
-          uint64_t covered = 0;
-          for (const unsigned long long j : js) {
-            if (j < covered) continue;
-            starts.push_back(j);
-            covered = j + wlen;
-          }
-          const uint64_t nwin = starts.size();
-          auto* st_d = ctx.tfst.get<unsigned long long>(nwin * 8);
-          CK(cudaMemcpyAsync(st_d, starts.data(), nwin * 8, cudaMemcpyHostToDevice, s));
-          auto* tabs = ctx.tftab.get<TfTab>(nwin * wlen * sizeof(TfTab));
-          const unsigned tgrid = static_cast<unsigned>(nwin * (wlen / kTfThreads));
-          if (lut_global(maxlen))
-            k_tf_tables<true><<<tgrid, kTfThreads, tf_smem(maxlen), s>>>(w, nw, T, lut, maxlen, st_d, nseq, tabs, wlen);
-          else
-            k_tf_tables<false><<<tgrid, kTfThreads, tf_smem(maxlen), s>>>(w, nw, T, lut, maxlen, st_d, nseq, tabs,
-                                                                           wlen);
-          check_launch("k_tf_tables");
-          k_tf_resolve<<<static_cast<unsigned>(nwin), kTfResolveThreads, 0, s>>>(tabs, st_d, nseq, T, seq, wlen);
-          check_launch("k_tf_resolve");
-          tf_windows += static_cast<int>(nwin);
-        }
-        if (std::getenv("MGRC_DEBUG")) std::fprintf(stderr, "[mgrc] huffman long-chain windows: %d\n", tf_windows);
-        prof.end();
-        auto* cnt = ctx.tiles.get<unsigned long long>(nseq * 8);
-        auto* toff = ctx.scan.get<unsigned long long>((nseq + 1) * 8);
-        k_seq_counts<<<static_cast<unsigned>((nseq + 255) / 256), 256, 0, s>>>(seq, nseq, cnt);
-        check_launch("k_seq_counts");
-        {
-          const uint64_t nt = (nseq + kScanTile - 1) / kScanTile;
-          auto* st = ctx.lbws.get<unsigned long long>(nt * 8 + 16);
-          auto* ticket = reinterpret_cast<unsigned int*>(st + nt);
-          CK(cudaMemsetAsync(st, 0, nt * 8 + 16, s));
-          k_scan_lb<<<static_cast<unsigned>(nt), kScanThreads, 0, s>>>(cnt, toff, nseq, st, ticket);
-          check_launch("k_scan_lb");
-        }
-        for (;;) {
-          DecodeStatus init{~0ull, 0u, 0u, 0u};
-          CK(cudaMemcpyAsync(&sd->dstat, &init, sizeof init, cudaMemcpyHostToDevice, s));
-          prof.begin("huff_emit", static_cast<double>(body_len) + static_cast<double>(N) * (wide ? 8 : 4));
-          if (wide)
-            decode_emit(ctx, w, nw, T, lut, maxlen, nseq, seq, toff, N, ctx.zz.get<unsigned long long>(N * 8),
-                        &sd->dstat);
-          else
-            decode_emit(ctx, w, nw, T, lut, maxlen, nseq, seq, toff, N, ctx.zz.get<uint32_t>(N * 4), &sd->dstat);
-          prof.end();
-          CK(cudaMemcpyAsync(&sh->dstat, &sd->dstat, sizeof(DecodeStatus), cudaMemcpyDeviceToHost, s));
-          CK(cudaStreamSynchronize(s));
-          if (sh->dstat.error == 1) raise(Errc::corrupt_stream, "varint overflows 64 bits");
-          if (sh->dstat.error == 2 || sh->dstat.end_bit == ~0ull)
-            raise(Errc::corrupt_stream, info.codec_id == 2 ? "Huffman stream truncated" : "truncated varint stream");
-          if (!sh->dstat.clean)
-            raise(Errc::corrupt_stream, info.codec_id == 2 ? "trailing bits after Huffman stream"
-                                                           : "trailing bytes after varint stream");
-          if (sh->dstat.wide && !wide) {
-            wide = true;
-            continue;
-          }
-          break;
-        }
-        }  // old decoder
       }
     }
     prof.begin("recon", static_cast<double>(N) * ((wide ? 8 : 4) + dtype_size(info.dtype)));
