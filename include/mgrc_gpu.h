@@ -114,6 +114,20 @@ MGRC_GPU_API int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndim
 MGRC_GPU_API int mgrc_gpu_decompress_chunked(const uint8_t* in, uint64_t len, void** out, int* dtype, int* ndims,
                                              uint64_t* shape);
 
+/* The same two on `ngpus` GPUs of one process: one host thread
+ * per rank, rank g on device g % device_count, slab b on rank floor(b*G/B)
+ * (contiguous rows and stream ranges); the per-block compressed sizes are
+ * all-gathered with NCCL (ncclCommInitAll + ncclAllGather, loaded at run
+ * time) when the ranks sit on distinct devices.  Host inputs (a device input
+ * is compressed on its own device); the output stream is byte-identical for
+ * every ngpus. */
+MGRC_GPU_API int mgrc_gpu_compress_chunked_multi(const void* data, int dtype, int ndims, const uint64_t* shape,
+                                                 const double* const* coords, double tol, int norm, double smoothness,
+                                                 int mode, int codec, uint64_t chunk_mem, int ngpus, uint8_t** out,
+                                                 uint64_t* out_len);
+MGRC_GPU_API int mgrc_gpu_decompress_chunked_multi(const uint8_t* in, uint64_t len, int ngpus, void** out, int* dtype,
+                                                   int* ndims, uint64_t* shape);
+
 /* ---- the decomposition and the quantiser as entry points of their own ----
  * f64 arrays, row-major over the grid (shape, coords as in mgrc_gpu_compress);
  * host or device pointers.  Bit-identical to the reference library. */

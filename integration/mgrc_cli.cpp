@@ -7,8 +7,8 @@
 //
 //   mgrc-gpu compress   --input F --output F --shape 513x513x513 --tol 1e-4
 //                       [--dtype f32|f64] [--s inf|<s>] [--mode abs|rel]
-//                       [--codec 0..2] [--chunk-mem 4GiB] [--coords F] [--device N]
-//   mgrc-gpu decompress --input F --output F [--device N]
+//                       [--codec 0..2] [--chunk-mem 4GiB] [--coords F] [--device N] [--gpus N]
+//   mgrc-gpu decompress --input F --output F [--device N] [--gpus N]
 //   mgrc-gpu inspect    PATH
 //
 // refactor / recompose (MDR stores, refactor.cpp) are SURVEY §8(f) row f2 and
@@ -18,6 +18,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cctype>
 #include <cerrno>
 #include <cinttypes>
@@ -212,6 +213,9 @@ void select_device(const Args& a) {
   if (a.has("--device")) check(mgrc_gpu_set_device(std::atoi(a.get("--device").c_str())));
 }
 
+// --gpus N: the blocks are spread over N GPUs of this process (mgrc_gpu_*_chunked_multi)
+int gpus(const Args& a) { return a.has("--gpus") ? std::max(1, std::atoi(a.get("--gpus").c_str())) : 1; }
+
 // run_compress (mgrc.cpp:363-484)
 int run_compress(const Args& a) {
   if (!a.pos.empty()) throw Usage("unexpected argument " + a.pos[0]);
@@ -269,9 +273,9 @@ int run_compress(const Args& a) {
   read_exact(input, in.data(), expect);
   uint8_t* out = nullptr;
   uint64_t out_len = 0;
-  check(mgrc_gpu_compress_chunked(in.data(), dtype, static_cast<int>(shape.size()), shape.data(),
-                                  cptr.empty() ? nullptr : cptr.data(), tol, norm, s, mode, codec, chunk_mem, &out,
-                                  &out_len));
+  check(mgrc_gpu_compress_chunked_multi(in.data(), dtype, static_cast<int>(shape.size()), shape.data(),
+                                        cptr.empty() ? nullptr : cptr.data(), tol, norm, s, mode, codec, chunk_mem,
+                                        gpus(a), &out, &out_len));
   const uint32_t nblocks = out_len >= 4 ? (uint32_t(out[0]) | uint32_t(out[1]) << 8 | uint32_t(out[2]) << 16 |
                                            uint32_t(out[3]) << 24)
                                         : 0;
@@ -300,7 +304,7 @@ int run_decompress(const Args& a) {
   void* out = nullptr;
   int dtype = 0, nd = 0;
   uint64_t shape[4] = {0, 0, 0, 0};
-  check(mgrc_gpu_decompress_chunked(in.data(), n, &out, &dtype, &nd, shape));
+  check(mgrc_gpu_decompress_chunked_multi(in.data(), n, gpus(a), &out, &dtype, &nd, shape));
   uint64_t count = 1;
   for (int k = 0; k < nd; ++k) count *= shape[k];
   try {
@@ -358,8 +362,8 @@ void usage(FILE* f) {
       "mgrc-gpu: error-bounded compression of raw floating-point arrays on the B200 path\n"
       "usage:\n"
       "  mgrc-gpu compress --input F --output F --shape AxBxC --tol T [--dtype f32|f64] [--s inf|S]\n"
-      "                    [--mode abs|rel] [--codec 0..2] [--chunk-mem SIZE] [--coords F] [--device N]\n"
-      "  mgrc-gpu decompress --input F --output F [--device N]\n"
+      "                    [--mode abs|rel] [--codec 0..2] [--chunk-mem SIZE] [--coords F] [--device N] [--gpus N]\n"
+      "  mgrc-gpu decompress --input F --output F [--device N] [--gpus N]\n"
       "  mgrc-gpu inspect PATH\n",
       f);
 }
@@ -380,8 +384,8 @@ int main(int argc, char** argv) {
     if (sub == "compress")
       return run_compress(parse_args(argc, argv, 2,
                                      {"--input", "--output", "--shape", "--dtype", "--tol", "--s", "--mode", "--codec",
-                                      "--chunk-mem", "--coords", "--device"}));
-    if (sub == "decompress") return run_decompress(parse_args(argc, argv, 2, {"--input", "--output", "--device"}));
+                                      "--chunk-mem", "--coords", "--device", "--gpus"}));
+    if (sub == "decompress") return run_decompress(parse_args(argc, argv, 2, {"--input", "--output", "--device", "--gpus"}));
     if (sub == "inspect") return run_inspect(parse_args(argc, argv, 2, {}));
     if (sub == "refactor" || sub == "recompose")
       raise(MGRC_E_INVALID_STATE, sub + " (MDR stores, refactor.cpp) is not part of the B200 path");

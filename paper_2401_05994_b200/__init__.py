@@ -302,30 +302,31 @@ def plan_chunks(shape: Sequence[int], dtype: DType, budget: int) -> np.ndarray:
 
 
 def compress_chunked(u, spec: ErrorSpec, codec: Codec = Codec.huffman, chunk_mem: int = 0,
-                     coords=None) -> bytes:
-    """The CLI's multiblock compress (tools/mgrc.cpp:363-484) on one GPU."""
+                     coords=None, ngpus: int = 1) -> bytes:
+    """The CLI's multiblock compress (tools/mgrc.cpp:363-484) on ``ngpus`` GPUs of this process
+    (mgrc_gpu_compress_chunked_multi: one host thread per GPU, NCCL all-gather of the sizes)."""
     ptr, dt, shape, keep = _array_ptr(u)
     grid = make_grid(shape, coords)
     gshape, cs, ckeep = _grid_args(grid)
     out = P()
     n = C.c_uint64()
-    _check(_lib.lib().mgrc_gpu_compress_chunked(ptr, int(dt), len(gshape), gshape.ctypes.data, cs, spec.tol,
-                                                int(spec.norm), spec.smoothness, int(spec.mode), int(codec),
-                                                chunk_mem, C.byref(out), C.byref(n)))
+    _check(_lib.lib().mgrc_gpu_compress_chunked_multi(ptr, int(dt), len(gshape), gshape.ctypes.data, cs, spec.tol,
+                                                      int(spec.norm), spec.smoothness, int(spec.mode), int(codec),
+                                                      chunk_mem, int(ngpus), C.byref(out), C.byref(n)))
     b = bytes(_take(out, n.value))
     _lib.lib().mgrc_gpu_free(out)
     return b
 
 
-def decompress_chunked(blob) -> np.ndarray:
-    """The CLI's multiblock decompress (tools/mgrc.cpp:490-542)."""
+def decompress_chunked(blob, ngpus: int = 1) -> np.ndarray:
+    """The CLI's multiblock decompress (tools/mgrc.cpp:490-542) on ``ngpus`` GPUs of this process."""
     ptr, n, keep = _bytes_ptr(blob)
     out = P()
     dt = C.c_int()
     nd = C.c_int()
     shape = np.zeros(4, dtype=np.uint64)
-    _check(_lib.lib().mgrc_gpu_decompress_chunked(ptr, n, C.byref(out), C.byref(dt), C.byref(nd),
-                                                  shape.ctypes.data))
+    _check(_lib.lib().mgrc_gpu_decompress_chunked_multi(ptr, n, int(ngpus), C.byref(out), C.byref(dt), C.byref(nd),
+                                                        shape.ctypes.data))
     sh = tuple(int(s) for s in shape[: nd.value])
     npdt = np.float32 if dt.value == 0 else np.float64
     cnt = int(np.prod(sh))

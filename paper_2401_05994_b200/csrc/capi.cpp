@@ -3,11 +3,16 @@
 // message in a thread-local slot, mirroring mgrc::error (error.hpp:34-47).
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/mgrc_gpu.h"
@@ -259,6 +264,349 @@ const void* host_box(const void* data, size_t unit, int d, const uint64_t* shape
     }
   }
   return tmp.data();
+}
+
+
+// ---- single-process multi-GPU chunked driver ---------------------------------
+//
+// One host thread per rank, rank g on device g % device_count (each thread has
+// its own per-device context: stream + workspace), slab b on rank floor(b*G/B)
+// (contiguous rows and stream ranges, as the torch.distributed driver).  The
+// blocks are independent containers; the only collective is the
+// all-gather of the per-block compressed sizes, done with NCCL (loaded at run
+// time: the process may already hold torch's copy) when the ranks sit on
+// distinct devices, on the host when a device carries several ranks.
+
+struct Nccl {
+  using comm_t = void*;
+  int (*init_all)(comm_t*, int, const int*) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, comm_t, cudaStream_t) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
+  int (*destroy)(comm_t) = nullptr;
+  bool ok = false;
+};
+
+const Nccl& nccl() {
+  static const Nccl n = [] {
+    Nccl r;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return r;
+    r.init_all = reinterpret_cast<decltype(r.init_all)>(dlsym(h, "ncclCommInitAll"));
+    r.all_gather = reinterpret_cast<decltype(r.all_gather)>(dlsym(h, "ncclAllGather"));
+    r.group_start = reinterpret_cast<decltype(r.group_start)>(dlsym(h, "ncclGroupStart"));
+    r.group_end = reinterpret_cast<decltype(r.group_end)>(dlsym(h, "ncclGroupEnd"));
+    r.destroy = reinterpret_cast<decltype(r.destroy)>(dlsym(h, "ncclCommDestroy"));
+    r.ok = r.init_all && r.all_gather && r.group_start && r.group_end && r.destroy;
+    return r;
+  }();
+  return n;
+}
+constexpr int kNcclUint64 = 5;  // ncclUint64 (nccl.h)
+
+uint64_t owner_of(uint64_t b, uint64_t nb, int G) { return (b * static_cast<uint64_t>(G)) / nb; }
+
+// Runs fn(rank) on G host threads, rank g on device g % ndev; rethrows the first failure.
+template <class Fn>
+void on_ranks(int G, Fn fn) {
+  if (G == 1) {  // the calling thread, its context and stream
+    fn(0);
+    return;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) raise(Errc::cuda, "no CUDA device");
+  std::vector<std::thread> th;
+  std::exception_ptr failure;
+  std::mutex mu;
+  for (int g = 0; g < G; ++g)
+    th.emplace_back([&, g] {
+      try {
+        if (cudaSetDevice(g % ndev) != cudaSuccess) raise(Errc::cuda, "cudaSetDevice failed");
+        fn(g);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!failure) failure = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  if (failure) std::rethrow_exception(failure);
+}
+
+// All-gather of the per-rank size vectors (every rank contributes nb entries,
+// zeros outside its blocks) -> the summed sizes of every block.
+std::vector<uint64_t> gather_sizes(int G, const std::vector<std::vector<uint64_t>>& local, uint64_t nb) {
+  std::vector<uint64_t> sizes(nb, 0);
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  const Nccl& n = nccl();
+  if (G > 1 && G <= ndev && n.ok) {
+    std::vector<Nccl::comm_t> comms(G, nullptr);
+    std::vector<int> devs(G);
+    for (int g = 0; g < G; ++g) devs[g] = g;
+    if (n.init_all(comms.data(), G, devs.data()) != 0) raise(Errc::cuda, "ncclCommInitAll failed");
+    std::vector<uint64_t*> send(G, nullptr), recv(G, nullptr);
+    std::vector<cudaStream_t> st(G, nullptr);
+    for (int g = 0; g < G; ++g) {
+      cudaSetDevice(g);
+      cudaStreamCreate(&st[g]);
+      cudaMalloc(&send[g], nb * 8);
+      cudaMalloc(&recv[g], nb * 8 * G);
+      cudaMemcpy(send[g], local[g].data(), nb * 8, cudaMemcpyHostToDevice);
+    }
+    n.group_start();
+    for (int g = 0; g < G; ++g) n.all_gather(send[g], recv[g], nb, kNcclUint64, comms[g], st[g]);
+    n.group_end();
+    std::vector<uint64_t> all(nb * G);
+    cudaSetDevice(0);
+    cudaStreamSynchronize(st[0]);
+    cudaMemcpy(all.data(), recv[0], nb * 8 * G, cudaMemcpyDeviceToHost);
+    for (int g = 0; g < G; ++g) {
+      cudaSetDevice(g);
+      cudaStreamSynchronize(st[g]);
+      cudaFree(send[g]);
+      cudaFree(recv[g]);
+      cudaStreamDestroy(st[g]);
+      n.destroy(comms[g]);
+    }
+    cudaSetDevice(0);
+    for (int g = 0; g < G; ++g)
+      for (uint64_t b = 0; b < nb; ++b) sizes[b] += all[g * nb + b];
+  } else {  // ranks sharing a device (or no NCCL): the vectors are already on the host
+    for (int g = 0; g < G; ++g)
+      for (uint64_t b = 0; b < nb; ++b) sizes[b] += local[g][b];
+  }
+  return sizes;
+}
+
+// Multiblock compress (tools/mgrc.cpp:363-484) on `ngpus` ranks: global REL
+// normalisation, per-block ABS compress with the block's coordinate slice,
+// the u32 count | u64 offsets | containers framing.  Blocks split only along
+// leading axes are contiguous sub-arrays and are compressed in place (device
+// inputs) or uploaded one block at a time (host inputs, read_block :91-145);
+// other blocks are gathered first.
+void compress_chunked_impl(const void* data, int dtype, int ndims, const uint64_t* shape,
+                                  const double* const* coords, double tol, int norm, double smoothness, int mode,
+                                  int codec, uint64_t chunk_mem, int ngpus, uint8_t** out, uint64_t* out_len) {
+  require(data != nullptr && out != nullptr && out_len != nullptr, "null argument");
+  const Grid whole = grid_from(ndims, shape, coords);
+  const DType dt = to_dtype(dtype);
+  const ErrorSpec spec = to_spec(tol, norm, smoothness, mode);
+  const Codec cd = to_codec(codec);
+  const ChunkPlan plan = plan_chunks(ndims, shape, dt, chunk_mem > 0 ? chunk_mem : UINT64_MAX);
+  const uint64_t nb = plan.block_count();
+  ensure_device();
+  const bool on_dev = is_device_pointer(data);
+  // ranks: at most one per block; a device-resident input stays on its device
+  const int G = on_dev ? 1 : static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ngpus > 0 ? ngpus : 1, nb)));
+  int dev0 = 0;
+  cudaGetDevice(&dev0);
+  const size_t unit = dtype_size(dt);
+  std::vector<std::vector<uint8_t>> blocks(nb);
+  ErrorSpec bspec = spec;
+  if (nb > 1) {
+    bspec.mode = Mode::abs;
+    if (spec.mode == Mode::rel) {  // global normalisation (tools/mgrc.cpp:405-418, scan_stats :197-233)
+      const uint64_t count = whole.count();
+      GlobalStats gs{0.0, 0.0, 0.0, false};
+      if (spec.norm == Norm::s || G == 1) {
+        // Σu² in file order, exactly (serial_sum.cuh) — one rank streams the whole array
+        gs = global_stats(context_for_current_device(), data, dt, count, spec.norm == Norm::s);
+      } else {  // min / max are order-free: each rank scans its own rows
+        std::vector<GlobalStats> part(G);
+        on_ranks(G, [&](int g) {
+          uint64_t lo = UINT64_MAX, hi = 0;
+          for (uint64_t b = 0; b < nb; ++b)
+            if (static_cast<int>(owner_of(b, nb, G)) == g) {
+              const auto r = plan.block(b);
+              lo = std::min<uint64_t>(lo, r[0].begin);
+              hi = std::max<uint64_t>(hi, r[0].end);
+            }
+          const uint64_t row = count / shape[0];
+          part[g] = global_stats(context_for_current_device(), static_cast<const uint8_t*>(data) + lo * row * unit,
+                                 dt, (hi - lo) * row, false);
+        });
+        gs = part[0];
+        for (int g = 1; g < G; ++g) {
+          gs.nonfinite = gs.nonfinite || part[g].nonfinite;
+          gs.min = std::min(gs.min, part[g].min);
+          gs.max = std::max(gs.max, part[g].max);
+        }
+      }
+      if (gs.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
+      const double nrm = spec.norm == Norm::s ? std::sqrt(gs.sumsq / static_cast<double>(count)) : gs.max - gs.min;
+      if (nrm == 0.0) raise(Errc::degenerate_data, "relative bound on a constant file");
+      bspec.tol = spec.tol * nrm;
+    }
+  }
+  std::vector<std::vector<uint64_t>> local(G, std::vector<uint64_t>(nb, 0));
+  on_ranks(G, [&](int g) {
+    Context& ctx = context_for_current_device();
+    cudaStream_t st = context_stream(ctx);
+    DeviceArray gather;
+    std::vector<uint8_t> hostbox;
+    for (uint64_t b = 0; b < nb; ++b) {
+      if (static_cast<int>(owner_of(b, nb, G)) != g) continue;
+      if (nb == 1) {  // single block: the user's grid and spec (mgrc.cpp:389-404)
+        const ContainerParts parts = compress(ctx, data, dt, whole, spec, cd);
+        blocks[0].resize(parts.total());
+        emit_parts(ctx, parts, blocks[0].data(), false);
+      } else {
+        const auto rng = plan.block(b);
+        uint64_t bshape[kMaxDims];
+        std::vector<double> bc[kMaxDims];
+        const double* cptr[kMaxDims];
+        for (int a = 0; a < ndims; ++a) {
+          bshape[a] = rng[a].length();
+          bc[a].assign(whole.coords[a].begin() + rng[a].begin, whole.coords[a].begin() + rng[a].end);
+          cptr[a] = bc[a].data();
+        }
+        const void* bdata = on_dev ? copy_box(st, data, unit, ndims, shape, rng, gather)
+                                   : host_box(data, unit, ndims, shape, rng, hostbox);
+        const Grid bg = make_grid(ndims, bshape, cptr);
+        const ContainerParts parts = compress(ctx, bdata, dt, bg, bspec, cd);
+        blocks[b].resize(parts.total());
+        emit_parts(ctx, parts, blocks[b].data(), false);
+      }
+      local[g][b] = blocks[b].size();
+    }
+  });
+  const std::vector<uint64_t> sizes = gather_sizes(G, local, nb);
+  cudaSetDevice(dev0);
+  uint64_t total = 4 + 8 * nb;
+  for (const uint64_t z : sizes) total += z;
+  uint8_t* buf = static_cast<uint8_t*>(std::malloc(total));
+  if (!buf) throw std::bad_alloc();
+  uint64_t at = 0;
+  auto put = [&](uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) buf[at++] = static_cast<uint8_t>(v >> (8 * i));
+  };
+  put(nb, 4);
+  uint64_t off = 4 + 8 * nb;
+  std::vector<uint64_t> offs(nb);
+  for (uint64_t b = 0; b < nb; ++b) {
+    offs[b] = off;
+    put(off, 8);
+    off += sizes[b];
+  }
+  for (uint64_t b = 0; b < nb; ++b) std::memcpy(buf + offs[b], blocks[b].data(), blocks[b].size());
+  *out = buf;
+  *out_len = total;
+}
+
+// Multiblock decompress (tools/mgrc.cpp:490-542) on `ngpus` ranks: offset
+// validation, placement from the blocks' coordinate slices, decode; a block
+// that is a contiguous slab of the output is decoded straight into place.
+void decompress_chunked_impl(const uint8_t* in, uint64_t len, int ngpus, void** out, int* dtype, int* ndims,
+                                    uint64_t* shape) {
+  require(in != nullptr && out != nullptr, "null argument");
+  ensure_device();
+  const auto blocks = split_multiblock(in, len);
+  std::vector<ContainerInfo> infos;
+  for (const auto& b : blocks) infos.push_back(parse_header(in + b.first, b.second));
+  const DType dt = infos[0].dtype;
+  for (const auto& i : infos)
+    if (i.dtype != dt) raise(Errc::corrupt_stream, "blocks disagree on dtype");
+  const int d = infos[0].ndims;
+  uint64_t gshape[kMaxDims] = {0, 0, 0, 0};
+  std::vector<std::vector<Range>> place(blocks.size());
+  if (blocks.size() == 1) {
+    for (int a = 0; a < d; ++a) {
+      gshape[a] = infos[0].shape[a];
+      place[0].push_back({0, gshape[a]});
+    }
+  } else {  // derive_placement (tools/mgrc.cpp:302-347)
+    for (int a = 0; a < d; ++a) {
+      std::vector<std::pair<double, uint64_t>> ranges;
+      for (const auto& info : infos) {
+        if (!info.coords_present || info.ndims != d)
+          raise(Errc::corrupt_stream, "multi-block container lacks placement coordinates");
+        const double start = info.coords[a][0];
+        const uint64_t l = info.shape[a];
+        bool found = false;
+        for (auto& r : ranges)
+          if (r.first == start) {
+            if (r.second != l) raise(Errc::corrupt_stream, "inconsistent block grid");
+            found = true;
+          }
+        if (!found) ranges.push_back({start, l});
+      }
+      std::sort(ranges.begin(), ranges.end());
+      uint64_t at = 0;
+      std::vector<std::pair<double, Range>> placed;
+      for (const auto& r : ranges) {
+        placed.push_back({r.first, {at, at + r.second}});
+        at += r.second;
+      }
+      gshape[a] = at;
+      for (size_t i = 0; i < infos.size(); ++i)
+        for (const auto& pr : placed)
+          if (pr.first == infos[i].coords[a][0]) {
+            place[i].push_back(pr.second);
+            break;
+          }
+      for (const auto& br : place)
+        if (static_cast<int>(br.size()) != a + 1) raise(Errc::corrupt_stream, "block placement failed");
+    }
+  }
+  uint64_t count = 1;
+  for (int a = 0; a < d; ++a) count *= gshape[a];
+  const size_t unit = dtype_size(dt);
+  uint8_t* buf = static_cast<uint8_t*>(std::malloc(count * unit + 1));
+  if (!buf) throw std::bad_alloc();
+  const uint64_t nb = blocks.size();
+  const int G = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ngpus > 0 ? ngpus : 1, nb)));
+  int dev0 = 0;
+  cudaGetDevice(&dev0);
+  try {
+    uint64_t stride[kMaxDims];
+    stride[d - 1] = 1;
+    for (int a = d - 1; a > 0; --a) stride[a - 1] = stride[a] * gshape[a];
+    on_ranks(G, [&](int g) {
+        Context& ctx = context_for_current_device();
+      std::vector<uint8_t> tmp;
+      for (uint64_t b = 0; b < nb; ++b) {
+        if (static_cast<int>(owner_of(b, nb, G)) != g) continue;
+        const auto& r = place[b];
+        uint64_t bcount = 1, origin = 0;
+        int first_partial = -1;
+        for (int a = 0; a < d; ++a) {
+          bcount *= r[a].length();
+          origin += r[a].begin * stride[a];
+          if (first_partial < 0 && r[a].length() != gshape[a]) first_partial = a;
+        }
+        bool contiguous = true;  // only leading axes split: the block is one run of the output
+        for (int a = first_partial + 1; first_partial >= 0 && a < d; ++a)
+          if (r[a].length() != gshape[a]) contiguous = false;
+        if (contiguous) {
+          decompress_into(ctx, in + blocks[b].first, blocks[b].second, buf + origin * unit, bcount * unit);
+          continue;
+        }
+        tmp.resize(bcount * unit);
+        decompress_into(ctx, in + blocks[b].first, blocks[b].second, tmp.data(), tmp.size());
+        const uint64_t run = r[d - 1].length();
+        std::vector<uint64_t> pos(d, 0);
+        for (uint64_t row = 0; row < bcount / run; ++row) {  // write_block (tools/mgrc.cpp:148-190)
+          uint64_t off = r[d - 1].begin;
+          for (int a = 0; a + 1 < d; ++a) off += (r[a].begin + pos[a]) * stride[a];
+          std::memcpy(buf + off * unit, tmp.data() + row * run * unit, run * unit);
+          for (int a = d - 2; a >= 0; --a) {
+            if (++pos[a] < r[a].length()) break;
+            pos[a] = 0;
+          }
+        }
+      }
+    });
+    cudaSetDevice(dev0);
+  } catch (...) {
+    cudaSetDevice(dev0);
+    std::free(buf);
+    throw;
+  }
+  *out = buf;
+  if (dtype) *dtype = static_cast<int>(dt);
+  if (ndims) *ndims = d;
+  if (shape)
+    for (int a = 0; a < d; ++a) shape[a] = gshape[a];
 }
 
 }  // namespace
@@ -525,178 +873,32 @@ int mgrc_gpu_dequantize(const int64_t* q, int ndims, const uint64_t* shape, cons
   });
 }
 
-// Multiblock compress on one GPU (tools/mgrc.cpp:363-484).  Blocks split only
-// along leading axes are contiguous sub-arrays and are compressed in place;
-// other blocks are gathered first.
 int mgrc_gpu_compress_chunked(const void* data, int dtype, int ndims, const uint64_t* shape,
                               const double* const* coords, double tol, int norm, double smoothness, int mode,
                               int codec, uint64_t chunk_mem, uint8_t** out, uint64_t* out_len) {
   return guarded([&] {
-    require(data != nullptr && out != nullptr && out_len != nullptr, "null argument");
-    const Grid whole = grid_from(ndims, shape, coords);
-    const DType dt = to_dtype(dtype);
-    const ErrorSpec spec = to_spec(tol, norm, smoothness, mode);
-    const Codec cd = to_codec(codec);
-    const ChunkPlan plan = plan_chunks(ndims, shape, dt, chunk_mem > 0 ? chunk_mem : UINT64_MAX);
-    const uint64_t nb = plan.block_count();
-    ensure_device();
-    Context& ctx = context_for_current_device();
-    const size_t unit = dtype_size(dt);
-    std::vector<std::vector<uint8_t>> blocks(nb);
-    if (nb == 1) {
-      const ContainerParts parts = compress(ctx, data, dt, whole, spec, cd);
-      blocks[0].resize(parts.total());
-      emit_parts(ctx, parts, blocks[0].data(), false);
-    } else {
-      ErrorSpec bspec = spec;
-      bspec.mode = Mode::abs;
-      const uint64_t count = whole.count();
-      cudaStream_t st = context_stream(ctx);
-      const bool on_dev = is_device_pointer(data);
-      if (spec.mode == Mode::rel) {  // global normalisation (tools/mgrc.cpp:405-418, scan_stats :197-233)
-        const GlobalStats gs = global_stats(ctx, data, dt, count, spec.norm == Norm::s);
-        if (gs.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
-        const double nrm = spec.norm == Norm::s ? std::sqrt(gs.sumsq / static_cast<double>(count)) : gs.max - gs.min;
-        if (nrm == 0.0) raise(Errc::degenerate_data, "relative bound on a constant file");
-        bspec.tol = spec.tol * nrm;
-      }
-      // one block at a time (read_block, tools/mgrc.cpp:91-145): device inputs are cut on the device;
-      // host inputs are uploaded block by block, so memory stays bounded by the largest block
-      DeviceArray gather;
-      std::vector<uint8_t> hostbox;
-      for (uint64_t b = 0; b < nb; ++b) {
-        const auto rng = plan.block(b);
-        uint64_t bshape[kMaxDims];
-        std::vector<double> bc[kMaxDims];
-        const double* cptr[kMaxDims];
-        for (int a = 0; a < ndims; ++a) {
-          bshape[a] = rng[a].length();
-          bc[a].assign(whole.coords[a].begin() + rng[a].begin, whole.coords[a].begin() + rng[a].end);
-          cptr[a] = bc[a].data();
-        }
-        const void* bdata = on_dev ? copy_box(st, data, unit, ndims, shape, rng, gather)
-                                   : host_box(data, unit, ndims, shape, rng, hostbox);
-        const Grid bg = make_grid(ndims, bshape, cptr);
-        const ContainerParts parts = compress(ctx, bdata, dt, bg, bspec, cd);
-        blocks[b].resize(parts.total());
-        emit_parts(ctx, parts, blocks[b].data(), false);
-      }
-    }
-    uint64_t total = 4 + 8 * nb;
-    for (const auto& b : blocks) total += b.size();
-    uint8_t* buf = static_cast<uint8_t*>(std::malloc(total));
-    uint64_t at = 0;
-    auto put = [&](uint64_t v, int bytes) {
-      for (int i = 0; i < bytes; ++i) buf[at++] = static_cast<uint8_t>(v >> (8 * i));
-    };
-    put(nb, 4);
-    uint64_t off = 4 + 8 * nb;
-    for (const auto& b : blocks) {
-      put(off, 8);
-      off += b.size();
-    }
-    for (const auto& b : blocks) {
-      std::memcpy(buf + at, b.data(), b.size());
-      at += b.size();
-    }
-    *out = buf;
-    *out_len = total;
+    compress_chunked_impl(data, dtype, ndims, shape, coords, tol, norm, smoothness, mode, codec, chunk_mem, 1, out,
+                          out_len);
   });
 }
 
-// Multiblock decompress (tools/mgrc.cpp:490-542).
+int mgrc_gpu_compress_chunked_multi(const void* data, int dtype, int ndims, const uint64_t* shape,
+                                    const double* const* coords, double tol, int norm, double smoothness, int mode,
+                                    int codec, uint64_t chunk_mem, int ngpus, uint8_t** out, uint64_t* out_len) {
+  return guarded([&] {
+    compress_chunked_impl(data, dtype, ndims, shape, coords, tol, norm, smoothness, mode, codec, chunk_mem, ngpus,
+                          out, out_len);
+  });
+}
+
 int mgrc_gpu_decompress_chunked(const uint8_t* in, uint64_t len, void** out, int* dtype, int* ndims,
                                 uint64_t* shape) {
-  return guarded([&] {
-    require(in != nullptr && out != nullptr, "null argument");
-    ensure_device();
-    Context& ctx = context_for_current_device();
-    const auto blocks = split_multiblock(in, len);
-    std::vector<ContainerInfo> infos;
-    for (const auto& b : blocks) infos.push_back(parse_header(in + b.first, b.second));
-    const DType dt = infos[0].dtype;
-    for (const auto& i : infos)
-      if (i.dtype != dt) raise(Errc::corrupt_stream, "blocks disagree on dtype");
-    const int d = infos[0].ndims;
-    uint64_t gshape[kMaxDims] = {0, 0, 0, 0};
-    std::vector<std::vector<Range>> place(blocks.size());
-    if (blocks.size() == 1) {
-      for (int a = 0; a < d; ++a) {
-        gshape[a] = infos[0].shape[a];
-        place[0].push_back({0, gshape[a]});
-      }
-    } else {  // derive_placement (tools/mgrc.cpp:302-347)
-      for (int a = 0; a < d; ++a) {
-        std::vector<std::pair<double, uint64_t>> ranges;
-        for (const auto& info : infos) {
-          if (!info.coords_present || info.ndims != d)
-            raise(Errc::corrupt_stream, "multi-block container lacks placement coordinates");
-          const double start = info.coords[a][0];
-          const uint64_t l = info.shape[a];
-          bool found = false;
-          for (auto& r : ranges)
-            if (r.first == start) {
-              if (r.second != l) raise(Errc::corrupt_stream, "inconsistent block grid");
-              found = true;
-            }
-          if (!found) ranges.push_back({start, l});
-        }
-        std::sort(ranges.begin(), ranges.end());
-        uint64_t at = 0;
-        std::vector<std::pair<double, Range>> placed;
-        for (const auto& r : ranges) {
-          placed.push_back({r.first, {at, at + r.second}});
-          at += r.second;
-        }
-        gshape[a] = at;
-        for (size_t i = 0; i < infos.size(); ++i)
-          for (const auto& pr : placed)
-            if (pr.first == infos[i].coords[a][0]) {
-              place[i].push_back(pr.second);
-              break;
-            }
-        for (const auto& br : place)
-          if (static_cast<int>(br.size()) != a + 1) raise(Errc::corrupt_stream, "block placement failed");
-      }
-    }
-    uint64_t count = 1;
-    for (int a = 0; a < d; ++a) count *= gshape[a];
-    const size_t unit = dtype_size(dt);
-    uint8_t* buf = static_cast<uint8_t*>(std::malloc(count * unit + 1));
-    if (!buf) throw std::bad_alloc();
-    try {
-      uint64_t stride[kMaxDims];
-      stride[d - 1] = 1;
-      for (int a = d - 1; a > 0; --a) stride[a - 1] = stride[a] * gshape[a];
-      std::vector<uint8_t> tmp;
-      for (size_t b = 0; b < blocks.size(); ++b) {
-        const auto& r = place[b];
-        uint64_t bcount = 1;
-        for (int a = 0; a < d; ++a) bcount *= r[a].length();
-        tmp.resize(bcount * unit);
-        decompress_into(ctx, in + blocks[b].first, blocks[b].second, tmp.data(), tmp.size());
-        const uint64_t run = r[d - 1].length();
-        std::vector<uint64_t> pos(d, 0);
-        for (uint64_t row = 0; row < bcount / run; ++row) {  // write_block (tools/mgrc.cpp:148-190)
-          uint64_t off = r[d - 1].begin;
-          for (int a = 0; a + 1 < d; ++a) off += (r[a].begin + pos[a]) * stride[a];
-          std::memcpy(buf + off * unit, tmp.data() + row * run * unit, run * unit);
-          for (int a = d - 2; a >= 0; --a) {
-            if (++pos[a] < r[a].length()) break;
-            pos[a] = 0;
-          }
-        }
-      }
-    } catch (...) {
-      std::free(buf);
-      throw;
-    }
-    *out = buf;
-    if (dtype) *dtype = static_cast<int>(dt);
-    if (ndims) *ndims = d;
-    if (shape)
-      for (int a = 0; a < d; ++a) shape[a] = gshape[a];
-  });
+  return guarded([&] { decompress_chunked_impl(in, len, 1, out, dtype, ndims, shape); });
+}
+
+int mgrc_gpu_decompress_chunked_multi(const uint8_t* in, uint64_t len, int ngpus, void** out, int* dtype, int* ndims,
+                                      uint64_t* shape) {
+  return guarded([&] { decompress_chunked_impl(in, len, ngpus, out, dtype, ndims, shape); });
 }
 
 }  // extern "C"

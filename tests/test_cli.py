@@ -111,6 +111,15 @@ def test_cli_round_trip(cli, oracle, tmp_path, case):
     offs = list(struct.unpack_from(f"<{count}Q", want, 4)) + [len(want)]
     ref = np.concatenate([oracle.decompress(want[offs[i]:offs[i + 1]]) for i in range(count)], axis=0)
     assert back.read_bytes() == ref.astype(dt).tobytes()
+    # the same stream and output from several GPU ranks of one process (--gpus; ranks share the device here)
+    out3 = tmp_path / "u3.mgrc"
+    r = run(cli, *[str(x) if x != out else out3 for x in args], "--gpus", "3")
+    assert r.returncode == 0, r.stderr
+    assert out3.read_bytes() == want
+    back3 = tmp_path / "back3.raw"
+    r = run(cli, "decompress", "--input", out3, "--output", back3, "--gpus", "2")
+    assert r.returncode == 0, r.stderr
+    assert back3.read_bytes() == back.read_bytes()
 
 
 @pytest.mark.gpu

@@ -312,3 +312,26 @@ def test_level_weighted_serial_fallback(mg, oracle, case, monkeypatch):
     assert st["achieved"] == oracle.achieved_error(r, 1, s)
     # the tree estimate is within the certified window of the serial value
     assert abs(fast["achieved"] - st["achieved"]) <= 1e-12 * st["achieved"]
+
+
+# ---------------------------------------------------------------------------
+# the single-process multi-GPU chunked driver (mgrc_gpu_compress_chunked_multi):
+# the stream is byte-identical for every rank count (ranks share the device on
+# a one-GPU box; the NCCL all-gather runs when they sit on distinct devices)
+
+
+@pytest.mark.parametrize("case", [
+    ((40, 33, 17), "multisine", "f32", 1e-4, 0, 0.0, 1, 17 * 33 * 17 * 4),
+    ((70, 65), "noisy", "f64", 1e-3, 0, 0.0, 0, 20 * 65 * 8),
+    ((60, 20, 20), "noisy", "f64", 1e-3, 1, 0.0, 1, 17 * 400 * 8),   # S-REL: the serial Σu² order
+    ((100, 70), "noisy", "f64", 1e-3, 0, 0.0, 1, 17 * 70 * 8),
+], ids=lambda c: "x".join(map(str, c[0])))
+@pytest.mark.parametrize("ngpus", [2, 3, 8])
+def test_chunked_multi_rank(mg, oracle, case, ngpus):
+    shape, kind, dt, tol, norm, s, mode, cm = case
+    u = make_field(oracle, kind, shape, dt)
+    spec = mg.ErrorSpec(tol, mg.Norm(norm), s, mg.Mode(mode))
+    want = oracle.compress_chunked(u, tol, norm, s, mode, 2, chunk_mem=cm)
+    got = mg.compress_chunked(u, spec, mg.Codec.huffman, chunk_mem=cm, ngpus=ngpus)
+    assert got == want
+    assert np.array_equal(mg.decompress_chunked(got, ngpus=ngpus), mg.decompress_chunked(got))
