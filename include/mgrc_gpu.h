@@ -160,6 +160,13 @@ MGRC_GPU_API int mgrc_gpu_dequantize(const int64_t* q, int ndims, const uint64_t
 MGRC_GPU_API int mgrc_gpu_field_stats(const void* data, int dtype, uint64_t n, double* min, double* max,
                                       int* nonfinite);
 
+/* s0 + sum of v_i*v_i, added serially in index order with one rounding per
+ * addition (exactly the CLI's scan_stats accumulation, tools/mgrc.cpp:227),
+ * reproduced bit for bit on the device; host or device array.  Ranks holding
+ * consecutive row ranges chain it (s0 = the previous rank's result) so the
+ * multi-GPU S-REL tolerance equals the single-scan one. */
+MGRC_GPU_API int mgrc_gpu_serial_sumsq(const void* data, int dtype, uint64_t n, double s0, double* out);
+
 /* Page-locked host buffers for fast host<->device staging (the CLI's raw-file
  * reads land in one; any host pointer is accepted by the calls above). */
 MGRC_GPU_API int mgrc_gpu_host_alloc(uint64_t bytes, void** p);

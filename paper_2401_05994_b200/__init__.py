@@ -30,7 +30,7 @@ from ._lib import ContainerInfoC, P
 __all__ = [
     "Norm", "Mode", "Codec", "DType", "ErrorSpec", "TensorGrid", "ContainerInfo", "MgrcError", "make_grid",
     "compress", "compress_to", "decompress", "decompress_into", "inspect", "describe", "plan_chunks",
-    "compress_chunked", "decompress_chunked", "field_stats", "set_device", "set_stream", "set_profiling",
+    "compress_chunked", "decompress_chunked", "field_stats", "serial_sumsq", "set_device", "set_stream", "set_profiling",
     "last_profile", "launch_count", "last_compress_stats", "nlevels", "initial_bin_widths", "forward_transform",
     "inverse_transform", "quantize", "dequantize", "ERRC_NAMES",
 ]
@@ -344,6 +344,15 @@ def field_stats(u) -> tuple:
     _check(_lib.lib().mgrc_gpu_field_stats(ptr, int(dt), int(np.prod(shape)), C.byref(mn), C.byref(mx),
                                            C.byref(nf)))
     return mn.value, mx.value, bool(nf.value)
+
+
+def serial_sumsq(u, s0: float = 0.0) -> float:
+    """s0 + Σ u_i² added serially in index order (the CLI's scan_stats sum, tools/mgrc.cpp:227), bit-exact,
+    computed on the GPU (serial_sum.cuh)."""
+    ptr, dt, shape, keep = _array_ptr(u)
+    out = C.c_double()
+    _check(_lib.lib().mgrc_gpu_serial_sumsq(ptr, int(dt), int(np.prod(shape)), float(s0), C.byref(out)))
+    return out.value
 
 
 def set_device(device: int) -> None:

@@ -47,6 +47,7 @@ SIGNATURES = {
                                                   C.c_int, C.c_uint64, C.c_int, C.POINTER(P), U64P]),
     "mgrc_gpu_decompress_chunked_multi": (C.c_int, [P, C.c_uint64, C.c_int, C.POINTER(P), IP, IP, P]),
     "mgrc_gpu_field_stats": (C.c_int, [P, C.c_int, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double), IP]),
+    "mgrc_gpu_serial_sumsq": (C.c_int, [P, C.c_int, C.c_uint64, C.c_double, C.POINTER(C.c_double)]),
     "mgrc_gpu_last_error": (C.c_char_p, []),
     "mgrc_gpu_free": (None, [P]),
     "mgrc_gpu_set_device": (C.c_int, [C.c_int]),

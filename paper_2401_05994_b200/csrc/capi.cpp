@@ -804,6 +804,14 @@ int mgrc_gpu_plan_chunks(int ndims, const uint64_t* shape, int dtype, uint64_t b
   });
 }
 
+int mgrc_gpu_serial_sumsq(const void* data, int dtype, uint64_t n, double s0, double* out) {
+  return guarded([&] {
+    require(data != nullptr && out != nullptr, "null argument");
+    ensure_device();
+    *out = serial_sumsq(context_for_current_device(), data, to_dtype(dtype), n, s0);
+  });
+}
+
 int mgrc_gpu_field_stats(const void* data, int dtype, uint64_t n, double* mn, double* mx, int* nonfinite) {
   return guarded([&] {
     require(data != nullptr && n > 0, "null argument");

@@ -562,6 +562,21 @@ FieldStats field_stats(Context& ctx, const void* data, DType dtype, uint64_t n) 
   return {key_to_double(sh->stats.min_key), key_to_double(sh->stats.max_key), sh->stats.nonfinite != 0};
 }
 
+double serial_sumsq(Context& ctx, const void* data, DType dtype, uint64_t n, double s0) {
+  const size_t unit = dtype_size(dtype);
+  if (is_device_pointer(data)) return exact_serial_sum(ctx, data, dtype, n, true, s0);
+  const uint64_t chunk = std::max<uint64_t>(1, (uint64_t{256} << 20) / unit);  // bounded staging, file order
+  double s = s0;
+  for (uint64_t at = 0; at < n; at += chunk) {
+    const uint64_t cnt = std::min(chunk, n - at);
+    void* d = ctx.in.get<uint8_t>(cnt * unit);
+    CK(cudaMemcpyAsync(d, static_cast<const uint8_t*>(data) + at * unit, cnt * unit, cudaMemcpyHostToDevice,
+                       ctx.stream));
+    s = exact_serial_sum(ctx, d, dtype, cnt, true, s);
+  }
+  return s;
+}
+
 GlobalStats global_stats(Context& ctx, const void* data, DType dtype, uint64_t n, bool want_sumsq) {
   GlobalStats g{0.0, 0.0, 0.0, false};
   const size_t unit = dtype_size(dtype);

@@ -87,5 +87,8 @@ GlobalStats global_stats(Context& ctx, const void* data, DType dtype, uint64_t n
 // s0 + Σ p_i in index order with one rounding per addition (p_i = v_i² when
 // `square`), reproduced exactly on the device (serial_sum.cuh).  Terms ≥ 0.
 double exact_serial_sum(Context& ctx, const void* v, DType dtype, uint64_t n, bool square, double s0);
+// s0 + Σ v_i² serially in index order over a host or device array (the
+// continuation of the CLI's scan_stats sum, tools/mgrc.cpp:227).
+double serial_sumsq(Context& ctx, const void* data, DType dtype, uint64_t n, double s0);
 
 }  // namespace mgrc_gpu

@@ -7,18 +7,18 @@ rank ``floor(b * G / B)``, so every rank owns a contiguous range of the input
 rows and of the output stream.  The blocks are independent containers
 (SPEC.md:478), so the only collectives are tiny:
 
-  1. REL mode: all-gather of the per-rank ``[min, max]`` (INF) or of the
-     per-rank sums of squares (S) to form the global absolute tolerance
-     (``mgrc.cpp:405-418``);
+  1. REL mode: all-gather of the per-rank ``[min, max]`` (INF); for S norms
+     the file-order serial sum of squares of the CLI (``mgrc.cpp:197-233``)
+     is chained rank to rank (one double each, exact) and all-gathered, so
+     the global absolute tolerance is bit-identical (``mgrc.cpp:405-418``);
   2. all-gather of the per-block compressed sizes, from which every rank
      computes the absolute offsets ``4 + 8 B + sum(sizes before)`` of the
      multiblock stream ``u32 count | u64 offsets[count] | containers``
      (``mgrc.cpp:258-275``).
 
 The resulting stream is byte-identical for any number of ranks and identical
-to the CLI's (INF norms; for S-REL the global sum of squares is combined per
-rank in rank order instead of the CLI's single serial scan, an ulp-level
-difference in tau).
+to the CLI's (for S-REL with plans that split inner axes the per-rank sums
+are combined in rank order instead — an ulp-level difference in tau).
 
 ``block_compress`` / ``block_stats`` default to the sm_100a library; the CPU
 tests inject the oracle to exercise the host logic under ``gloo``.
@@ -92,11 +92,10 @@ def _default_stats(block):
     return mn, mx, nonfinite
 
 
-def _default_sumsq(block) -> float:
-    import torch
+def _default_sumsq(block, s0: float) -> float:
+    from . import serial_sumsq
 
-    t = block if isinstance(block, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(block))
-    return float((t.double() ** 2).sum().item())
+    return serial_sumsq(block, s0)
 
 
 def compress_sharded(read_block: Callable[[int, list], object], shape: Sequence[int], dtype: DType,
@@ -137,8 +136,19 @@ def compress_sharded(read_block: Callable[[int, list], object], shape: Sequence[
         for b in mine:
             a, c, nf = block_stats(data[b])
             mn, mx, bad = min(mn, a), max(mx, c), bad | int(nf)
-            if spec.norm == Norm.s:
-                ss = ss + block_sumsq(data[b])
+        if spec.norm == Norm.s:
+            # Σu² in file order, added serially like the CLI's scan_stats (mgrc.cpp:197-233): with a
+            # slowest-axis slab plan every rank holds consecutive rows, so the exact serial sum is a chain
+            # (rank r continues from rank r-1's running value; one double passed per rank)
+            slabs = all(int(r[1] - r[0]) == shape[a] for blk in plan for a, r in enumerate(blk) if a > 0)
+            if slabs:
+                ss = _chain_recv(rank, group)
+                for b in mine:
+                    ss = block_sumsq(data[b], ss)
+                _chain_send(ss, rank, world, group)
+            else:  # blocks split inner axes: per-rank partials combined in rank order (ulp-level difference)
+                for b in mine:
+                    ss = ss + block_sumsq(data[b], 0.0)
         st = _allgather_floats([mn, mx, float(bad), ss], group)
         if any(row[2] for row in st):
             raise MgrcError(5, "NonFiniteInput: input contains NaN or Inf")
@@ -147,9 +157,12 @@ def compress_sharded(read_block: Callable[[int, list], object], shape: Sequence[
         if spec.norm == Norm.inf:
             nrm = gmax - gmin
         else:
-            tot = 0.0
-            for row in st:  # rank order
-                tot = tot + row[3]
+            if slabs:  # the last rank holds the whole serial sum
+                tot = st[-1][3]
+            else:
+                tot = 0.0
+                for row in st:  # rank order
+                    tot = tot + row[3]
             nrm = float(np.sqrt(tot / float(np.prod(shape))))
         if nrm == 0.0:
             raise MgrcError(6, "DegenerateData: relative bound on a constant file")
@@ -228,6 +241,27 @@ def _allgather_floats(vals: List[float], group) -> List[List[float]]:
     parts = [torch.zeros_like(t) for _ in range(dist.get_world_size(group))]
     dist.all_gather(parts, t, group=group)
     return [p.cpu().tolist() for p in parts]
+
+
+def _chain_recv(rank: int, group) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if rank == 0 or not dist.is_initialized():
+        return 0.0
+    t = torch.zeros(1, dtype=torch.float64, device=_coll_device(group))
+    dist.recv(t, src=dist.get_global_rank(group, rank - 1) if group is not None else rank - 1, group=group)
+    return float(t.item())
+
+
+def _chain_send(v: float, rank: int, world: int, group) -> None:
+    import torch
+    import torch.distributed as dist
+
+    if rank + 1 >= world or not dist.is_initialized():
+        return
+    t = torch.tensor([v], dtype=torch.float64, device=_coll_device(group))
+    dist.send(t, dst=dist.get_global_rank(group, rank + 1) if group is not None else rank + 1, group=group)
 
 
 def _coll_device(group):

@@ -207,18 +207,32 @@ def test_chunked_parity(mg, oracle, case):
     got = mg.compress_chunked(u, mg.ErrorSpec(tol, mg.Norm(norm), s, mg.Mode(mode)), mg.Codec.huffman, chunk_mem=cm)
     assert got == want
     assert np.array_equal(mg.decompress_chunked(got), oracle_decompress_chunked(oracle, want, shape))
-    if not (norm == 1 and mode == 1):
-        from paper_2401_05994_b200 import sharded
+    from paper_2401_05994_b200 import sharded  # the multi-rank driver (world size 1 here), S-REL included
 
-        def read_block(b, ranges):
-            return np.ascontiguousarray(u[tuple(slice(int(r[0]), int(r[1])) for r in ranges)])
+    def read_block(b, ranges):
+        return np.ascontiguousarray(u[tuple(slice(int(r[0]), int(r[1])) for r in ranges)])
 
-        st = sharded.compress_sharded(read_block, shape, mg.DType.f32 if dt == np.float32 else mg.DType.f64,
-                                      mg.ErrorSpec(tol, mg.Norm(norm), s, mg.Mode(mode)), mg.Codec.huffman,
-                                      chunk_mem=cm)
-        buf = bytearray(st.total_len)
-        st.write_into(buf)
-        assert bytes(buf) == want
+    st = sharded.compress_sharded(read_block, shape, mg.DType.f32 if dt == np.float32 else mg.DType.f64,
+                                  mg.ErrorSpec(tol, mg.Norm(norm), s, mg.Mode(mode)), mg.Codec.huffman, chunk_mem=cm)
+    buf = bytearray(st.total_len)
+    st.write_into(buf)
+    assert bytes(buf) == want
+
+
+def test_serial_sumsq_matches_cli_scan(mg, oracle):
+    """The CLI's scan_stats accumulation (mgrc.cpp:227: sumsq += v*v in file order), bit-exact, host and device
+    arrays, and continued across a split (the multi-rank chain)."""
+    import torch
+
+    for dt in (np.float32, np.float64):
+        u = oracle.multisine_noisy((37, 41, 13), 42, 0.05).astype(dt)
+        want = 0.0
+        for v in u.astype(np.float64).ravel().tolist():
+            want = want + v * v
+        assert mg.serial_sumsq(u) == want
+        assert mg.serial_sumsq(torch.from_numpy(u).cuda()) == want
+        a = mg.serial_sumsq(np.ascontiguousarray(u[:20]))
+        assert mg.serial_sumsq(np.ascontiguousarray(u[20:]), a) == want
 
 
 def oracle_decompress_chunked(oracle, stream, shape):

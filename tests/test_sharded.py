@@ -28,6 +28,8 @@ CASES = {
     "inf_rel_f32": dict(shape=(40, 33, 17), dtype="f32", tol=1e-4, norm=0, s=0.0, mode=1, chunk=17 * 33 * 17 * 4),
     "inf_abs_f64_2d": dict(shape=(70, 65), dtype="f64", tol=1e-3, norm=0, s=0.0, mode=0, chunk=20 * 65 * 8),
     "s0_abs_f64": dict(shape=(60, 20, 20), dtype="f64", tol=1e-3, norm=1, s=0.0, mode=0, chunk=17 * 400 * 8),
+    "s0_rel_f64": dict(shape=(60, 20, 20), dtype="f64", tol=1e-3, norm=1, s=0.0, mode=1, chunk=17 * 400 * 8),
+    "s1_rel_f32": dict(shape=(50, 24, 20), dtype="f32", tol=1e-3, norm=1, s=1.0, mode=1, chunk=17 * 24 * 20 * 4),
     "single_block": dict(shape=(33, 17), dtype="f64", tol=1e-3, norm=0, s=0.0, mode=1, chunk=0),
 }
 
@@ -55,6 +57,12 @@ def _worker(rank, world, port, case_name, out_q):
             return orc.compress(block, spec.tol, int(spec.norm), spec.smoothness, int(spec.mode), int(codec),
                                 coords=coords, shape=bshape)
 
+        def block_sumsq(block, s0):  # the CLI's serial accumulation (mgrc.cpp:227), continued from s0
+            acc = float(s0)
+            for v in np.asarray(block, dtype=np.float64).ravel().tolist():
+                acc = acc + v * v
+            return acc
+
         def block_stats(block):
             b = np.asarray(block, dtype=np.float64)
             return float(b.min()), float(b.max()), bool(~np.isfinite(b).all())
@@ -62,7 +70,7 @@ def _worker(rank, world, port, case_name, out_q):
         spec = mg.ErrorSpec(c["tol"], mg.Norm(c["norm"]), c["s"], mg.Mode(c["mode"]))
         st = sharded.compress_sharded(read_block, c["shape"], mg.DType.f32 if c["dtype"] == "f32" else mg.DType.f64,
                                       spec, mg.Codec.huffman, chunk_mem=c["chunk"], block_compress=block_compress,
-                                      block_stats=block_stats)
+                                      block_stats=block_stats, block_sumsq=block_sumsq)
         # assemble on every rank through an all-gather of the parts (test only)
         parts = [None] * world
         dist.all_gather_object(parts, (st.my_offset, st.my_bytes))
@@ -98,10 +106,7 @@ def test_sharded_stream_matches_cli(case_name, world):
         assert p.exitcode == 0
     blocks_seen = []
     for rank, stream, dec in res:
-        if c["norm"] == 1 and c["mode"] == 1:
-            pass  # S-REL: per-rank sums combined in rank order (ulp-level tau difference)
-        else:
-            assert stream == want, (rank, world)
+        assert stream == want, (rank, world)  # S-REL too: the serial Σu² is chained rank to rank
         blocks_seen += [b for b, _ in dec]
     nb = int.from_bytes(want[:4], "little")
     assert sorted(blocks_seen) == list(range(nb))
