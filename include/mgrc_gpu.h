@@ -144,6 +144,16 @@ MGRC_GPU_API int mgrc_gpu_forward_transform(const double* u, int ndims, const ui
 /* Replaces inverse_transform (transform.hpp:28-30, transform.cpp:180-191). */
 MGRC_GPU_API int mgrc_gpu_inverse_transform(const double* c, int ndims, const uint64_t* shape,
                                             const double* const* coords, double* u);
+/* The decomposition / recomposition with MGARD's L2-projection correction
+ * (opt-in; the reference is interpolation-only): after the
+ * level-l coefficients are formed the coarse values receive
+ * z = M_{l-1}^{-1} R M_l c (mass-matrix multiply, restriction, tridiagonal
+ * solve, axis by axis), so each coarse level is the L2 projection of the
+ * finer one.  Same arguments as mgrc_gpu_forward/inverse_transform. */
+MGRC_GPU_API int mgrc_gpu_forward_transform_l2(const double* u, int ndims, const uint64_t* shape,
+                                               const double* const* coords, double* c);
+MGRC_GPU_API int mgrc_gpu_inverse_transform_l2(const double* c, int ndims, const uint64_t* shape,
+                                               const double* const* coords, double* u);
 /* Replaces quantize (quantize.hpp:32-36, quantize.cpp:72-132): q = rne(c/delta_tag)
  * and (if residuals != NULL) r = c - q*delta_tag; nwidths must be nlevels+1
  * (ShapeMismatch), widths > 0 (InvalidState); Overflow when |c/delta| >= 2^63;

@@ -1,0 +1,200 @@
+"""TEST INFRASTRUCTURE ONLY — CPU oracle of the L²-projection correction
+(SURVEY §8(f) row f3), restated in numpy float64.
+
+The reference decomposition is interpolation-only: its coarse levels hold the
+nodal values of u (transform.cpp:12-23).  The production
+MGARD decomposition (Ainsworth, Tugluk, Whitney, Klasky, "Multilevel
+techniques for compression and reduction of scientific data", and the MGARD
+software paper, PAPER.md) instead makes each coarse level the L² projection
+of the finer one: after the level-l coefficients c_l = u_l − I_{l-1} u_l are
+formed, the coarse values receive the correction
+
+    z_l = M_{l-1}^{-1} R_l M_l c_l,      u_{l-1} = u_l|_{coarse} + z_l,
+
+with M the mass matrix of the multilinear hat basis and R_l = I_l^T the
+restriction.  On a tensor grid every operator is a tensor product of 1-D
+operators, so z_l is computed axis by axis (ascending axis order; axes that
+do not refine at level l are skipped: M^{-1} I M = I):
+
+  1-D mass matrix on the level set x_0 < ... < x_{n-1}, h_k = x_{k+1} - x_k:
+      (M v)_k = (h_{k-1}/6) v_{k-1} + ((h_{k-1} + h_k)/3) v_k + (h_k/6) v_{k+1}
+  1-D restriction to the coarse subset (the new node between coarse q and q'
+  interpolates with weights wl, wr — transform.cpp:57-60):
+      (R f)_q = f_q + wr(new left of q) f_{left} + wl(new right of q) f_{right}
+  1-D solve M_{l-1} z = r by the Thomas algorithm (cp, denom precomputed).
+
+The hierarchy (level sets, stencils and their weights) is the reference's
+(grid.cpp:100-153, transform.cpp:27-63), so for the correction off this is
+exactly the reference decomposition.  The GPU (paper_2401_05994_b200/csrc/
+l2proj.cu) follows the same operation order with round-to-nearest
+intrinsics and no FMA, so its coefficients are expected to agree bit for bit;
+the north_star gate is 1e-12 relative.
+
+Parity: this restatement has no counterpart in the reference (SPEC.md:12
+excludes the correction), so it is pinned instead by the properties the
+projection has by construction (tests/test_l2proj.py): exact inverse up to
+rounding; with the correction off it reproduces the reference transform bit
+for bit; the corrected coarse level is the L² projection (the Galerkin
+orthogonality M_{l-1} z = R M c holds to rounding, and for a field in the
+coarse space the coefficients vanish).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import binding
+
+
+def _level_tables(shape, coords):
+    """Per axis and level: the level set, fresh flags, neighbour positions (within the level set) and
+    interpolation weights of the fresh nodes (transform.cpp:27-63), mass/Thomas coefficients."""
+    o = binding.get("restatement")
+    shape = tuple(int(s) for s in shape)
+    d = len(shape)
+    L = o.hierarchy(shape)["nlevels"]
+    xs = [np.arange(n, dtype=np.float64) if coords is None else np.asarray(coords[a], dtype=np.float64)
+          for a, n in enumerate(shape)]
+    tab = {}
+    for a in range(d):
+        for l in range(L + 1):
+            idx = o.level_set(shape, l, a).astype(np.int64)
+            coarse = o.level_set(shape, l - 1, a).astype(np.int64) if l > 0 else idx
+            fresh = ~np.isin(idx, coarse) if l > 0 else np.zeros(len(idx), bool)
+            x = xs[a][idx]
+            n = len(idx)
+            wl = np.zeros(n)
+            wr = np.zeros(n)
+            for p in np.nonzero(fresh)[0]:
+                xl, xr = x[p - 1], x[p + 1]  # a fresh node sits between two coarse ones
+                wl[p] = (xr - x[p]) / (xr - xl)
+                wr[p] = (x[p] - xl) / (xr - xl)
+            h = np.diff(x)
+            lo = np.zeros(n)
+            di = np.zeros(n)
+            up = np.zeros(n)
+            for k in range(n):
+                hp = h[k - 1] if k > 0 else 0.0
+                hn = h[k] if k < n - 1 else 0.0
+                lo[k] = hp / 6.0
+                di[k] = (hp + hn) / 3.0
+                up[k] = hn / 6.0
+            cp = np.zeros(n)
+            den = np.zeros(n)
+            den[0] = di[0]
+            cp[0] = up[0] / den[0]
+            for k in range(1, n):
+                den[k] = di[k] - lo[k] * cp[k - 1]
+                cp[k] = up[k] / den[k]
+            tab[a, l] = dict(idx=idx, fresh=fresh, wl=wl, wr=wr, lo=lo, di=di, up=up, cp=cp, den=den)
+    return L, tab
+
+
+def _interp_level(v, tab, d, l, sign):
+    """v[node] += sign * I_{l-1}(node) for the nodes new at level l (transform.cpp:68-143), vectorised over
+    the sub-boxes of nodes sharing one set of fresh axes; corner order and weight products as the reference."""
+    sets = [tab[a, l] for a in range(d)]
+    for F in range(1, 1 << d):
+        parts = []
+        ok = True
+        for a in range(d):
+            sel = np.nonzero(sets[a]["fresh"] if (F >> a) & 1 else ~sets[a]["fresh"])[0]
+            if len(sel) == 0:
+                ok = False
+                break
+            parts.append(sel)
+        if not ok:
+            continue
+        shape = tuple(len(p) for p in parts)
+        acc = np.zeros(shape)
+        s = 0
+        while True:  # submasks of F in increasing order; bit a selects the right neighbour on axis a
+            w = 1.0
+            ix = []
+            for a in range(d):
+                t, p = sets[a], parts[a]
+                if (F >> a) & 1:
+                    right = (s >> a) & 1
+                    bshape = [1] * d
+                    bshape[a] = len(p)
+                    w = w * (t["wr"] if right else t["wl"])[p].reshape(bshape)  # ascending axis order
+                    ix.append(t["idx"][p + (1 if right else -1)])
+                else:
+                    ix.append(t["idx"][p])
+            acc = acc + np.broadcast_to(w, shape) * v[np.ix_(*ix)]
+            s = (s - F) & F
+            if s == 0:
+                break
+        tgt = np.ix_(*[sets[a]["idx"][parts[a]] for a in range(d)])
+        v[tgt] = v[tgt] + sign * acc
+
+
+def _axis_correction(C, tl, tc, axis):
+    """One axis of z = M_{l-1}^{-1} R M_l c: mass multiply on the level-l line, restriction to the coarse
+    positions, Thomas solve on the coarse line.  C: dense array whose `axis` runs over the level-l set."""
+    v = np.moveaxis(C, axis, -1)
+    n = v.shape[-1]
+    lo, di, up = tl["lo"], tl["di"], tl["up"]
+    f = di * v
+    if n > 1:
+        f[..., 1:] = lo[1:] * v[..., :-1] + f[..., 1:]
+        f[..., :-1] = f[..., :-1] + up[:-1] * v[..., 1:]
+    fresh = tl["fresh"]
+    kq = np.nonzero(~fresh)[0]  # coarse positions within the level-l line
+    r = f[..., kq].copy()
+    for q, k in enumerate(kq):
+        if k - 1 >= 0 and fresh[k - 1]:
+            r[..., q] = r[..., q] + tl["wr"][k - 1] * f[..., k - 1]
+        if k + 1 < n and fresh[k + 1]:
+            r[..., q] = r[..., q] + tl["wl"][k + 1] * f[..., k + 1]
+    m = r.shape[-1]
+    lo, cp, den = tc["lo"], tc["cp"], tc["den"]
+    dp = np.empty_like(r)
+    dp[..., 0] = r[..., 0] / den[0]
+    for k in range(1, m):
+        dp[..., k] = (r[..., k] - lo[k] * dp[..., k - 1]) / den[k]
+    x = np.empty_like(r)
+    x[..., m - 1] = dp[..., m - 1]
+    for k in range(m - 2, -1, -1):
+        x[..., k] = dp[..., k] - cp[k] * x[..., k + 1]
+    return np.moveaxis(x, -1, axis)
+
+
+def _correction(v, tab, d, l):
+    """z_l on the level-(l-1) box from the coefficients of the nodes new at level l."""
+    box = np.ix_(*[tab[a, l]["idx"] for a in range(d)])
+    new = np.zeros(tuple(len(tab[a, l]["idx"]) for a in range(d)), bool)
+    for a in range(d):
+        shp = [1] * d
+        shp[a] = -1
+        new = new | tab[a, l]["fresh"].reshape(shp)
+    C = np.where(new, v[box], 0.0)
+    for a in range(d):
+        if tab[a, l]["fresh"].any():
+            C = _axis_correction(C, tab[a, l], tab[a, l - 1], a)
+    return C
+
+
+def forward_l2(u, coords=None):
+    """Multilevel coefficients with the L² correction (levels L..1)."""
+    v = np.array(u, dtype=np.float64, copy=True)
+    d = v.ndim
+    L, tab = _level_tables(v.shape, coords)
+    for l in range(L, 0, -1):
+        _interp_level(v, tab, d, l, -1.0)
+        z = _correction(v, tab, d, l)
+        cb = np.ix_(*[tab[a, l - 1]["idx"] for a in range(d)])
+        v[cb] = v[cb] + z
+    return v
+
+
+def inverse_l2(c, coords=None):
+    """Exact inverse of forward_l2 up to rounding (levels 1..L)."""
+    v = np.array(c, dtype=np.float64, copy=True)
+    d = v.ndim
+    L, tab = _level_tables(v.shape, coords)
+    for l in range(1, L + 1):
+        z = _correction(v, tab, d, l)
+        cb = np.ix_(*[tab[a, l - 1]["idx"] for a in range(d)])
+        v[cb] = v[cb] - z
+        _interp_level(v, tab, d, l, +1.0)
+    return v

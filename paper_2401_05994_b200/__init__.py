@@ -445,25 +445,28 @@ def initial_bin_widths(tau_abs: float, spec: ErrorSpec, ndims: int, nlev: int) -
     return out
 
 
-def forward_transform(u, grid: Optional[TensorGrid] = None):
-    """forward_transform (transform.cpp:163-178) on the GPU: the multilevel coefficients of ``u``."""
+def forward_transform(u, grid: Optional[TensorGrid] = None, l2: bool = False):
+    """forward_transform (transform.cpp:163-178) on the GPU: the multilevel coefficients of ``u``.
+    ``l2=True``: with MGARD's L²-projection correction of the coarse levels (not in the reference)."""
     ptr, shape, keep = _f64_ptr(u, "u")
     grid = grid or make_grid(shape)
     _check_grid(grid, shape)
     gshape, coords, ck = _grid_args(grid)
     c, cp = _empty_like(keep, np.float64)
-    _check(_lib.lib().mgrc_gpu_forward_transform(ptr, len(gshape), gshape.ctypes.data, coords, cp))
+    fn = _lib.lib().mgrc_gpu_forward_transform_l2 if l2 else _lib.lib().mgrc_gpu_forward_transform
+    _check(fn(ptr, len(gshape), gshape.ctypes.data, coords, cp))
     return c
 
 
-def inverse_transform(c, grid: Optional[TensorGrid] = None):
-    """inverse_transform (transform.cpp:180-191) on the GPU."""
+def inverse_transform(c, grid: Optional[TensorGrid] = None, l2: bool = False):
+    """inverse_transform (transform.cpp:180-191) on the GPU (``l2=True``: of the corrected decomposition)."""
     ptr, shape, keep = _f64_ptr(c, "c")
     grid = grid or make_grid(shape)
     _check_grid(grid, shape)
     gshape, coords, ck = _grid_args(grid)
     u, up = _empty_like(keep, np.float64)
-    _check(_lib.lib().mgrc_gpu_inverse_transform(ptr, len(gshape), gshape.ctypes.data, coords, up))
+    fn = _lib.lib().mgrc_gpu_inverse_transform_l2 if l2 else _lib.lib().mgrc_gpu_inverse_transform
+    _check(fn(ptr, len(gshape), gshape.ctypes.data, coords, up))
     return u
 
 

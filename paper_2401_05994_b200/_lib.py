@@ -62,6 +62,8 @@ SIGNATURES = {
     "mgrc_gpu_initial_bin_widths": (C.c_int, [C.c_double, C.c_int, C.c_double, C.c_int, C.c_int, P]),
     "mgrc_gpu_forward_transform": (C.c_int, [P, C.c_int, P, P, P]),
     "mgrc_gpu_inverse_transform": (C.c_int, [P, C.c_int, P, P, P]),
+    "mgrc_gpu_forward_transform_l2": (C.c_int, [P, C.c_int, P, P, P]),
+    "mgrc_gpu_inverse_transform_l2": (C.c_int, [P, C.c_int, P, P, P]),
     "mgrc_gpu_quantize": (C.c_int, [P, C.c_int, P, P, P, C.c_int, P, P, U64P]),
     "mgrc_gpu_dequantize": (C.c_int, [P, C.c_int, P, P, P, C.c_int, P]),
     "mgrc_gpu_last_compress_stats": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), IP, IP]),

@@ -860,6 +860,26 @@ int mgrc_gpu_inverse_transform(const double* c, int ndims, const uint64_t* shape
   });
 }
 
+int mgrc_gpu_forward_transform_l2(const double* u, int ndims, const uint64_t* shape, const double* const* coords,
+                                  double* c) {
+  return guarded([&] {
+    require(u != nullptr && c != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    ensure_device();
+    forward_transform_l2(context_for_current_device(), u, c, g);
+  });
+}
+
+int mgrc_gpu_inverse_transform_l2(const double* c, int ndims, const uint64_t* shape, const double* const* coords,
+                                  double* u) {
+  return guarded([&] {
+    require(u != nullptr && c != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    ensure_device();
+    inverse_transform_l2(context_for_current_device(), c, u, g);
+  });
+}
+
 int mgrc_gpu_quantize(const double* c, int ndims, const uint64_t* shape, const double* const* coords,
                       const double* widths, int nwidths, int64_t* q, double* residuals, uint64_t* outliers) {
   return guarded([&] {

@@ -95,6 +95,10 @@ struct DevHier {
   std::vector<BoxDev> boxes;   // per level, finest-grid indices
   GridDev gc{};                // coarse box (valid when h.L >= 1)
   std::vector<BoxDev> cboxes;  // per level 0..L-1, compact indices
+  // L²-projection correction tables (transform.cu), built on first use
+  DevBuf l2buf;
+  std::vector<L2Axis> l2;      // [l * 4 + a], l = 1..L
+  bool l2_ready = false;
 };
 
 struct Scratch {  // small device-side results read back at sync points
@@ -120,6 +124,7 @@ class Context {
   DevBuf ssmaps;
   PinnedBuf ssmaps_h;
   DevBuf in, zz, zc, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws, tfst, tftab;
+  DevBuf l2a, l2b;  // dense level arrays of the L²-projection correction
   DevBuf scratch_d;
   PinnedBuf scratch_h, partial_h;
   std::vector<std::unique_ptr<DevHier>> hiers;  // most recently used first (chunked slabs alternate shapes)

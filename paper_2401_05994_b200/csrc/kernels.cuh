@@ -57,6 +57,19 @@ struct Widths {
   double w[kMaxL];
 };
 
+// One axis of the L²-projection correction at level l (transform.cu): the
+// level-l line (nl nodes: mass matrix rows lo/di/up, fresh flags, the fresh
+// nodes' interpolation weights) and the level-(l-1) line (nc nodes: their
+// positions kq in the level-l line, Thomas coefficients lo/cp/den).
+struct L2Axis {
+  const double *lo, *di, *up, *wl, *wr;
+  const uint8_t* fresh;
+  const uint32_t* kq;
+  const double *clo, *cp, *den;
+  uint32_t nl, nc;
+  int refines;
+};
+
 __device__ __forceinline__ uint64_t zigzag(long long q) {
   return (static_cast<uint64_t>(q) << 1) ^ static_cast<uint64_t>(q >> 63);
 }

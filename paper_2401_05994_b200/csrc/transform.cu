@@ -134,6 +134,95 @@ __global__ void __launch_bounds__(kTfmThreads) k_dequantize(GridDev g, BoxDev bo
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// L²-projection correction (opt-in; MGARD's decomposition):
+// after the level-l coefficients are formed, the coarse values receive
+// z = M_{l-1}^{-1} R M_l c, axis by axis (oracle/l2proj.py states the
+// algorithm and the operation order this follows).
+
+// v[node] = v[node] ± I(v)(node) in place for the nodes tagged l.
+template <int D>
+__global__ void __launch_bounds__(kTfmThreads) k_interp_level(GridDev g, BoxDev box, int l, int sub, double* v) {
+  const BoxWalk<D> w{g, box};
+  auto ld = [v](uint64_t off) { return v[off]; };
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < box.count; p += step) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    const uint64_t n = w.locate(p, i);
+    if (node_tag<D>(g, i) != l) continue;
+    const double acc = interp<D>(g, i, l, ld);
+    v[n] = sub ? __dsub_rn(v[n], acc) : __dadd_rn(v[n], acc);
+  }
+}
+
+// Dense level-l array (row-major over the level sets): the coefficients of
+// the nodes tagged l, zero at the coarse nodes.
+template <int D>
+__global__ void __launch_bounds__(kTfmThreads) k_l2_gather(GridDev g, BoxDev box, int l, const double* __restrict__ v,
+                                                            double* __restrict__ out) {
+  const BoxWalk<D> w{g, box};
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < box.count; p += step) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    const uint64_t n = w.locate(p, i);
+    out[p] = node_tag<D>(g, i) == l ? v[n] : 0.0;
+  }
+}
+
+// v[node] = v[node] ± z for the nodes of the level-(l-1) box (z dense over it).
+template <int D>
+__global__ void __launch_bounds__(kTfmThreads) k_l2_scatter(GridDev g, BoxDev box, int sub,
+                                                             const double* __restrict__ z, double* v) {
+  const BoxWalk<D> w{g, box};
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < box.count; p += step) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    const uint64_t n = w.locate(p, i);
+    v[n] = sub ? __dsub_rn(v[n], z[p]) : __dadd_rn(v[n], z[p]);
+  }
+}
+
+// One axis of the correction, one thread per line: mass-matrix row, the
+// restriction onto the coarse positions, the Thomas sweeps of the coarse mass
+// matrix.  A: dense with `nl` along the axis, B: dense with `nc` along it;
+// `inner` = product of the later dimensions (the axis stride in both), so
+// consecutive threads touch consecutive addresses (coalesced unless the axis
+// is the last one, where L1 serves the reuse along the line).
+__device__ __forceinline__ double l2_mass(const L2Axis& t, const double* __restrict__ a, uint64_t inner, uint32_t k) {
+  // ((lo_k v_{k-1} + di_k v_k) + up_k v_{k+1}), end terms absent (oracle/l2proj.py _axis_correction)
+  double f = __dmul_rn(__ldg(t.di + k), a[k * inner]);
+  if (k > 0) f = __dadd_rn(__dmul_rn(__ldg(t.lo + k), a[(k - 1) * inner]), f);
+  if (k + 1 < t.nl) f = __dadd_rn(f, __dmul_rn(__ldg(t.up + k), a[(k + 1) * inner]));
+  return f;
+}
+
+__global__ void __launch_bounds__(256) k_l2_line(L2Axis t, const double* __restrict__ A, double* __restrict__ B,
+                                                 uint64_t nlines, uint64_t inner) {
+  const uint64_t line = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (line >= nlines) return;
+  const uint64_t o = line / inner, ii = line - o * inner;
+  const double* a = A + o * t.nl * inner + ii;
+  double* b = B + o * t.nc * inner + ii;
+  // restriction + Thomas forward sweep: dp_q = (r_q - lo_q dp_{q-1}) / den_q
+  double dp = 0.0;
+  for (uint32_t q = 0; q < t.nc; ++q) {
+    const uint32_t k = __ldg(t.kq + q);
+    double r = l2_mass(t, a, inner, k);
+    if (k > 0 && __ldg(t.fresh + k - 1)) r = __dadd_rn(r, __dmul_rn(__ldg(t.wr + k - 1), l2_mass(t, a, inner, k - 1)));
+    if (k + 1 < t.nl && __ldg(t.fresh + k + 1))
+      r = __dadd_rn(r, __dmul_rn(__ldg(t.wl + k + 1), l2_mass(t, a, inner, k + 1)));
+    dp = q == 0 ? __ddiv_rn(r, __ldg(t.den)) : __ddiv_rn(__dsub_rn(r, __dmul_rn(__ldg(t.clo + q), dp)), __ldg(t.den + q));
+    b[q * inner] = dp;
+  }
+  // back substitution: x_q = dp_q - cp_q x_{q+1}
+  double x = dp;
+  for (int q = static_cast<int>(t.nc) - 2; q >= 0; --q) {
+    x = __dsub_rn(b[q * inner], __dmul_rn(__ldg(t.cp + q), x));
+    b[q * inner] = x;
+  }
+}
+
 }  // namespace dev
 
 namespace {
@@ -178,6 +267,154 @@ struct Dequant {
     }
   };
 };
+
+
+struct InterpLevel {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const BoxDev& b, int l, int sub, double* v) {
+      k_interp_level<D><<<blocks_for(b.count), kTfmThreads, 0, s>>>(g, b, l, sub, v);
+      check_launch("k_interp_level");
+    }
+  };
+};
+struct L2Gather {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const BoxDev& b, int l, const double* v, double* out) {
+      k_l2_gather<D><<<blocks_for(b.count), kTfmThreads, 0, s>>>(g, b, l, v, out);
+      check_launch("k_l2_gather");
+    }
+  };
+};
+struct L2Scatter {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const BoxDev& b, int sub, const double* z, double* v) {
+      k_l2_scatter<D><<<blocks_for(b.count), kTfmThreads, 0, s>>>(g, b, sub, z, v);
+      check_launch("k_l2_scatter");
+    }
+  };
+};
+
+// Device tables of the correction for every level and axis (oracle/l2proj.py
+// _level_tables, the same double expressions).
+void l2_tables(Context& ctx, DevHier& dh) {
+  if (dh.l2_ready) return;
+  const Hierarchy& h = dh.h;
+  const int d = h.grid.d, L = h.L;
+  std::vector<uint8_t> host;
+  auto align = [](size_t x) { return (x + 15) & ~size_t{15}; };
+  auto put = [&](const void* p, size_t n) {
+    const size_t off = host.size();
+    host.resize(align(off + n), 0);
+    if (n) std::memcpy(&host[off], p, n);
+    return off;
+  };
+  struct Off {
+    size_t lo, di, up, wl, wr, fresh, kq, clo, cp, den;
+    uint32_t nl, nc;
+    int refines;
+  };
+  std::vector<Off> offs(static_cast<size_t>(L + 1) * 4);
+  auto mass = [](const std::vector<double>& x, std::vector<double>& lo, std::vector<double>& di,
+                 std::vector<double>& up) {
+    const size_t n = x.size();
+    lo.assign(n, 0.0), di.assign(n, 0.0), up.assign(n, 0.0);
+    for (size_t k = 0; k < n; ++k) {
+      const double hp = k > 0 ? x[k] - x[k - 1] : 0.0;
+      const double hn = k + 1 < n ? x[k + 1] - x[k] : 0.0;
+      lo[k] = hp / 6.0;
+      di[k] = (hp + hn) / 3.0;
+      up[k] = hn / 6.0;
+    }
+  };
+  for (int l = 1; l <= L; ++l)
+    for (int a = 0; a < d; ++a) {
+      const auto& S = h.sets[a][l];
+      const auto& Sc = h.sets[a][l - 1];
+      Off& o = offs[static_cast<size_t>(l) * 4 + a];
+      o.nl = static_cast<uint32_t>(S.size());
+      o.nc = static_cast<uint32_t>(Sc.size());
+      o.refines = S.size() > Sc.size();
+      std::vector<double> x(S.size()), xc(Sc.size());
+      for (size_t k = 0; k < S.size(); ++k) x[k] = h.grid.coords[a][S[k]];
+      for (size_t k = 0; k < Sc.size(); ++k) xc[k] = h.grid.coords[a][Sc[k]];
+      std::vector<double> lo, di, up, clo, cdi, cup;
+      mass(x, lo, di, up);
+      mass(xc, clo, cdi, cup);
+      std::vector<uint8_t> fresh(S.size(), 0);
+      std::vector<double> wl(S.size(), 0.0), wr(S.size(), 0.0);
+      std::vector<uint32_t> kq;
+      for (size_t k = 0; k < S.size(); ++k) {
+        if (h.lvl[a][S[k]] == l) {
+          fresh[k] = 1;
+          wl[k] = h.wl[a][S[k]];
+          wr[k] = h.wr[a][S[k]];
+        } else {
+          kq.push_back(static_cast<uint32_t>(k));
+        }
+      }
+      std::vector<double> cp(Sc.size()), den(Sc.size());
+      den[0] = cdi[0];
+      cp[0] = cup[0] / den[0];
+      for (size_t k = 1; k < Sc.size(); ++k) {
+        den[k] = cdi[k] - clo[k] * cp[k - 1];
+        cp[k] = cup[k] / den[k];
+      }
+      o.lo = put(lo.data(), 8 * lo.size());
+      o.di = put(di.data(), 8 * di.size());
+      o.up = put(up.data(), 8 * up.size());
+      o.wl = put(wl.data(), 8 * wl.size());
+      o.wr = put(wr.data(), 8 * wr.size());
+      o.fresh = put(fresh.data(), fresh.size());
+      o.kq = put(kq.data(), 4 * kq.size());
+      o.clo = put(clo.data(), 8 * clo.size());
+      o.cp = put(cp.data(), 8 * cp.size());
+      o.den = put(den.data(), 8 * den.size());
+    }
+  uint8_t* dp = dh.l2buf.get<uint8_t>(std::max<size_t>(host.size(), 16));
+  CK(cudaMemcpyAsync(dp, host.data(), host.size(), cudaMemcpyHostToDevice, ctx.stream));
+  CK(cudaStreamSynchronize(ctx.stream));
+  dh.l2.assign(static_cast<size_t>(L + 1) * 4, L2Axis{});
+  for (int l = 1; l <= L; ++l)
+    for (int a = 0; a < d; ++a) {
+      const Off& o = offs[static_cast<size_t>(l) * 4 + a];
+      L2Axis& t = dh.l2[static_cast<size_t>(l) * 4 + a];
+      auto P64 = [&](size_t x) { return reinterpret_cast<const double*>(dp + x); };
+      t.lo = P64(o.lo), t.di = P64(o.di), t.up = P64(o.up), t.wl = P64(o.wl), t.wr = P64(o.wr);
+      t.fresh = dp + o.fresh;
+      t.kq = reinterpret_cast<const uint32_t*>(dp + o.kq);
+      t.clo = P64(o.clo), t.cp = P64(o.cp), t.den = P64(o.den);
+      t.nl = o.nl, t.nc = o.nc, t.refines = o.refines;
+    }
+  dh.l2_ready = true;
+}
+
+// z_l (dense over the level-(l-1) box) from the coefficients of the nodes tagged l; returns its buffer.
+const double* l2_correction(Context& ctx, DevHier& dh, int l, const double* v) {
+  cudaStream_t s = ctx.stream;
+  const int d = dh.h.grid.d;
+  uint64_t dims[kMaxDims] = {1, 1, 1, 1};
+  for (int a = 0; a < d; ++a) dims[a] = dh.h.sets[a][l].size();
+  const uint64_t n = dh.boxes[l].count;
+  double* A = ctx.l2a.get<double>(n * 8);
+  double* B = ctx.l2b.get<double>(n * 8);
+  by_dim<L2Gather::L>(d, s, dh.g, dh.boxes[l], l, v, A);
+  for (int a = 0; a < d; ++a) {
+    const L2Axis& t = dh.l2[static_cast<size_t>(l) * 4 + a];
+    if (!t.refines) continue;
+    uint64_t inner = 1, lines = 1;
+    for (int b = 0; b < d; ++b)
+      if (b != a) lines *= dims[b];
+    for (int b = a + 1; b < d; ++b) inner *= dims[b];
+    k_l2_line<<<static_cast<unsigned>((lines + 255) / 256), 256, 0, s>>>(t, A, B, lines, inner);
+    check_launch("k_l2_line");
+    dims[a] = t.nc;
+    std::swap(A, B);
+  }
+  return A;
+}
 
 // A caller array as a device pointer: device arrays are used in place, host
 // arrays are staged through the context buffer `buf` (uploaded when `in`).
@@ -283,6 +520,56 @@ void dequantize_coefficients(Context& ctx, const int64_t* q, const Grid& grid, c
   by_dim<Dequant::L>(grid.d, s, dh.g, dh.boxes[dh.h.L], W, dq, dc);
   prof.end();
   download(ctx, c, dc, N * 8);
+  CK(cudaStreamSynchronize(s));
+}
+
+
+void forward_transform_l2(Context& ctx, const double* u, double* c, const Grid& grid) {
+  Prof prof(ctx);
+  cudaStream_t s = ctx.stream;
+  const uint64_t N = grid.count();
+  const double* du = staged<double>(ctx, ctx.in, u, N, true);
+  Scratch* sd = ctx.sd();
+  Scratch* sh = ctx.sh();
+  launch_stats(ctx, du, N, &sd->stats);
+  CK(cudaMemcpyAsync(&sh->stats, &sd->stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (sh->stats.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
+  DevHier& dh = device_hierarchy(ctx, grid);
+  l2_tables(ctx, dh);
+  double* v = staged<double>(ctx, ctx.v, c, N, false);
+  if (static_cast<const void*>(v) == static_cast<const void*>(du))
+    raise(Errc::invalid_argument, "forward_transform: output aliases the input");
+  prof.begin("forward_l2", static_cast<double>(N) * 16);
+  CK(cudaMemcpyAsync(v, du, N * 8, cudaMemcpyDeviceToDevice, s));
+  for (int l = dh.h.L; l >= 1; --l) {  // oracle/l2proj.py forward_l2
+    by_dim<InterpLevel::L>(grid.d, s, dh.g, dh.boxes[l], l, 1, v);
+    const double* z = l2_correction(ctx, dh, l, v);
+    by_dim<L2Scatter::L>(grid.d, s, dh.g, dh.boxes[l - 1], 0, z, v);
+  }
+  prof.end();
+  download(ctx, c, v, N * 8);
+  CK(cudaStreamSynchronize(s));
+}
+
+void inverse_transform_l2(Context& ctx, const double* c, double* u, const Grid& grid) {
+  Prof prof(ctx);
+  cudaStream_t s = ctx.stream;
+  const uint64_t N = grid.count();
+  const double* dc = staged<double>(ctx, ctx.in, c, N, true);
+  DevHier& dh = device_hierarchy(ctx, grid);
+  l2_tables(ctx, dh);
+  double* v = staged<double>(ctx, ctx.v, u, N, false);
+  if (v == dc) raise(Errc::invalid_argument, "inverse_transform: output aliases the coefficients");
+  prof.begin("inverse_l2", static_cast<double>(N) * 16);
+  CK(cudaMemcpyAsync(v, dc, N * 8, cudaMemcpyDeviceToDevice, s));
+  for (int l = 1; l <= dh.h.L; ++l) {  // oracle/l2proj.py inverse_l2
+    const double* z = l2_correction(ctx, dh, l, v);
+    by_dim<L2Scatter::L>(grid.d, s, dh.g, dh.boxes[l - 1], 1, z, v);
+    by_dim<InterpLevel::L>(grid.d, s, dh.g, dh.boxes[l], l, 0, v);
+  }
+  prof.end();
+  download(ctx, u, v, N * 8);
   CK(cudaStreamSynchronize(s));
 }
 

@@ -16,6 +16,10 @@ class Context;
 void forward_transform(Context& ctx, const double* u, double* c, const Grid& grid);
 // inverse_transform (transform.cpp:180-191).
 void inverse_transform(Context& ctx, const double* c, double* u, const Grid& grid);
+// The decomposition / recomposition with MGARD's L²-projection correction
+// (opt-in, not in the reference: SPEC.md:12; oracle/l2proj.py).
+void forward_transform_l2(Context& ctx, const double* u, double* c, const Grid& grid);
+void inverse_transform_l2(Context& ctx, const double* c, double* u, const Grid& grid);
 // quantize (quantize.cpp:72-132): Overflow when |c/δ| ≥ 2^63; returns the
 // outlier count (|q| > 2^31 − 1).  r may be null.
 uint64_t quantize_coefficients(Context& ctx, const double* c, const Grid& grid, const double* widths, int nwidths,
