@@ -66,6 +66,7 @@ typedef struct {
   uint64_t payload_len;
   uint32_t checksum;
   uint64_t header_size;
+  uint8_t l2_projection; /* header flag 0x04: the L2-corrected decomposition (not readable by the reference) */
 } mgrc_container_info;
 
 /* Replaces mgrc::compress(span<const float|double>, TensorGrid, ErrorSpec,
@@ -82,6 +83,19 @@ MGRC_GPU_API int mgrc_gpu_compress(const void* data, int dtype, int ndims, const
 MGRC_GPU_API int mgrc_gpu_compress_to(const void* data, int dtype, int ndims, const uint64_t* shape,
                                       const double* const* coords, double tol, int norm, double smoothness, int mode,
                                       int codec, void* dst, uint64_t dst_capacity, uint64_t* out_len);
+
+/* The same two on the decomposition with MGARD's L2-projection correction
+ * (mgrc_gpu_forward_transform_l2): the reference's quantiser, accept loop and
+ * lossless stage on the corrected coefficients, the a-posteriori error taken
+ * through the corrected recomposition.  The container carries header flag
+ * 0x04 (the reference rejects it as unknown, container.cpp:143); the
+ * decompress entry points below read it. */
+MGRC_GPU_API int mgrc_gpu_compress_l2(const void* data, int dtype, int ndims, const uint64_t* shape,
+                                      const double* const* coords, double tol, int norm, double smoothness, int mode,
+                                      int codec, uint8_t** out, uint64_t* out_len);
+MGRC_GPU_API int mgrc_gpu_compress_l2_to(const void* data, int dtype, int ndims, const uint64_t* shape,
+                                         const double* const* coords, double tol, int norm, double smoothness,
+                                         int mode, int codec, void* dst, uint64_t dst_capacity, uint64_t* out_len);
 
 /* Replaces mgrc::decompress(span<const uint8_t>, exec) — container.hpp:76-77.
  * *out is a host buffer of prod(shape) floats (dtype f32) or doubles. */

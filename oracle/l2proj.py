@@ -198,3 +198,82 @@ def inverse_l2(c, coords=None):
         v[cb] = v[cb] - z
         _interp_level(v, tab, d, l, +1.0)
     return v
+
+
+# ---------------------------------------------------------------------------
+# Containers of the corrected decomposition: the reference's tolerance, bin
+# widths, quantiser, accept loop and lossless stage (container.cpp:71-131,
+# via the restatement) on the corrected coefficients; the a-posteriori error
+# through inverse_l2; header flag 0x04 (our extension — the reference's own
+# parser rejects it, container.cpp:143).
+
+FLAG_L2 = 0x04
+
+
+def append_header(shape, coords, dtype, constant, tol, norm, s, mode, widths, codec, payload_len, crc, flags=0):
+    """container.cpp:28-55 (little endian)."""
+    import struct
+
+    out = bytearray(b"MGRC")
+    out += struct.pack("<H", 1)
+    fl = (1 if constant else 0) | (2 if coords is not None else 0) | flags
+    out += struct.pack("<BBB", fl, 0 if dtype == np.float32 else 1, len(shape))
+    for n in shape:
+        out += struct.pack("<Q", n)
+    if coords is not None:
+        for c in coords:
+            out += struct.pack("<Q", len(c)) + np.asarray(c, dtype="<f8").tobytes()
+    out += struct.pack("<BBdd", mode, norm, s if norm == 1 else 0.0, tol)
+    out += struct.pack("<B", len(widths) - 1) + np.asarray(widths, dtype="<f8").tobytes()
+    out += struct.pack("<BQI", codec, payload_len, crc)
+    return bytes(out)
+
+
+def compress_l2(u, tol, norm=0, s=0.0, mode=0, codec=2, coords=None):
+    o = binding.get("restatement")
+    src = np.ascontiguousarray(u)
+    u64 = src.astype(np.float64)
+    shape = src.shape
+    N = u64.size
+    if u64.max() == u64.min():  # constant field: the reference's header-only container
+        return o.compress(src, tol, norm, s, mode, codec, coords=coords)
+    tau = o.absolute_tolerance(u64, tol, norm, s, mode)
+    L = o.hierarchy(shape)["nlevels"]
+    widths = o.bin_widths(tau, norm, s, len(shape), L)
+    c = forward_l2(u64, coords)
+    for _ in range(10):
+        q, r, _ = o.quantize(c, widths, coords)
+        if norm == 1 and s != 0.0:
+            achieved = o.achieved_error(r, 1, s, coords)
+        else:
+            e = inverse_l2(r, coords)
+            if src.dtype == np.float32:  # container.cpp:96-110
+                e = u64 - (u64 - e).astype(np.float32).astype(np.float64)
+            achieved = float(np.max(np.abs(e))) if norm == 0 else float(np.sqrt(o.sum_squares(e) / N))
+        if achieved <= tau * (1 - 1e-9):
+            break
+        widths = widths * 0.5
+    else:
+        raise binding.OracleError(13, "ToleranceUnreachable: bin shrink loop exhausted after 10 passes")
+    payload = o.lossless_encode(q, codec)
+    hdr = append_header(shape, coords, src.dtype, False, tol, norm, s, mode, widths, codec, len(payload),
+                        o.crc32(payload), FLAG_L2)
+    return hdr + payload
+
+
+def decompress_l2(blob, coords=None):
+    import struct
+
+    o = binding.get("restatement")
+    fl = blob[6]
+    if not fl & FLAG_L2:
+        return o.decompress(blob)
+    plain = blob[:6] + bytes([fl & ~FLAG_L2]) + blob[7:]
+    info = o.inspect(plain)
+    shape = tuple(int(info.shape[a]) for a in range(info.ndims))
+    hs = info.header_size
+    payload = blob[hs: hs + info.payload_len]
+    q = o.lossless_decode(payload, int(np.prod(shape)), info.codec_id).reshape(shape)
+    widths = np.array([info.bin_widths[l] for l in range(info.nlevels + 1)])
+    v = inverse_l2(o.dequantize(q, widths, coords), coords)
+    return v.astype(np.float32) if info.dtype == 0 else v

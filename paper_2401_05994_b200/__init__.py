@@ -116,6 +116,7 @@ class ContainerInfo:  # container.hpp:37-51
     checksum: int
     header_size: int
     raw: bytes = field(default=b"", repr=False)
+    l2_projection: bool = False  # header flag 0x04 (the L²-corrected decomposition)
 
 
 def make_grid(shape: Sequence[int], coords: Optional[Sequence[Sequence[float]]] = None) -> TensorGrid:
@@ -197,8 +198,9 @@ def _check_grid(grid: TensorGrid, shape) -> None:
 
 
 def compress(u, grid: Optional[TensorGrid] = None, spec: Optional[ErrorSpec] = None,
-             codec: Codec = Codec.huffman) -> bytes:
-    """mgrc::compress (container.hpp:69-74) on the GPU; returns the container bytes."""
+             codec: Codec = Codec.huffman, l2: bool = False) -> bytes:
+    """mgrc::compress (container.hpp:69-74) on the GPU; returns the container bytes.
+    ``l2=True``: on the decomposition with MGARD's L²-projection correction (header flag 0x04)."""
     ptr, dt, shape, keep = _array_ptr(u)
     grid = grid or make_grid(shape)
     _check_grid(grid, shape)
@@ -206,16 +208,16 @@ def compress(u, grid: Optional[TensorGrid] = None, spec: Optional[ErrorSpec] = N
     gshape, coords, ckeep = _grid_args(grid)
     out = P()
     n = C.c_uint64()
-    _check(_lib.lib().mgrc_gpu_compress(ptr, int(dt), len(gshape), gshape.ctypes.data, coords, spec.tol,
-                                        int(spec.norm), spec.smoothness, int(spec.mode), int(codec), C.byref(out),
-                                        C.byref(n)))
+    fn = _lib.lib().mgrc_gpu_compress_l2 if l2 else _lib.lib().mgrc_gpu_compress
+    _check(fn(ptr, int(dt), len(gshape), gshape.ctypes.data, coords, spec.tol, int(spec.norm), spec.smoothness,
+              int(spec.mode), int(codec), C.byref(out), C.byref(n)))
     b = bytes(_take(out, n.value))
     _lib.lib().mgrc_gpu_free(out)
     return b
 
 
 def compress_to(u, dst, grid: Optional[TensorGrid] = None, spec: Optional[ErrorSpec] = None,
-                codec: Codec = Codec.huffman) -> int:
+                codec: Codec = Codec.huffman, l2: bool = False) -> int:
     """Compress into a caller buffer (host numpy / torch, or a CUDA torch uint8 tensor); returns the length.
 
     With ``dst=None`` only the length is computed (the container stays staged on the device)."""
@@ -229,9 +231,9 @@ def compress_to(u, dst, grid: Optional[TensorGrid] = None, spec: Optional[ErrorS
     else:
         dptr, cap, dkeep = _bytes_ptr(dst)
     n = C.c_uint64()
-    _check(_lib.lib().mgrc_gpu_compress_to(ptr, int(dt), len(gshape), gshape.ctypes.data, coords, spec.tol,
-                                           int(spec.norm), spec.smoothness, int(spec.mode), int(codec), dptr, cap,
-                                           C.byref(n)))
+    fn = _lib.lib().mgrc_gpu_compress_l2_to if l2 else _lib.lib().mgrc_gpu_compress_to
+    _check(fn(ptr, int(dt), len(gshape), gshape.ctypes.data, coords, spec.tol, int(spec.norm), spec.smoothness,
+              int(spec.mode), int(codec), dptr, cap, C.byref(n)))
     return n.value
 
 
@@ -276,7 +278,8 @@ def inspect(blob) -> ContainerInfo:
         dtype=DType(ci.dtype), shape=tuple(int(ci.shape[a]) for a in range(ci.ndims)),
         spec=ErrorSpec(ci.tol, Norm(ci.norm), ci.smoothness, Mode(ci.mode)), nlevels=ci.nlevels,
         bin_widths=[ci.bin_widths[l] for l in range(ci.nlevels + 1)], codec_id=ci.codec_id,
-        payload_len=ci.payload_len, checksum=ci.checksum, header_size=ci.header_size, raw=b[: ci.header_size])
+        payload_len=ci.payload_len, checksum=ci.checksum, header_size=ci.header_size, raw=b[: ci.header_size],
+        l2_projection=bool(ci.l2_projection))
 
 
 def describe(info_or_blob) -> str:

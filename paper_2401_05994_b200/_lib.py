@@ -24,6 +24,7 @@ class ContainerInfoC(C.Structure):
         ("shape", C.c_uint64 * 4), ("mode", C.c_uint8), ("norm", C.c_uint8),
         ("smoothness", C.c_double), ("tol", C.c_double), ("bin_widths", C.c_double * 65),
         ("payload_len", C.c_uint64), ("checksum", C.c_uint32), ("header_size", C.c_uint64),
+        ("l2_projection", C.c_uint8),
     ]
 
 
@@ -34,6 +35,10 @@ SIGNATURES = {
     "mgrc_gpu_compress_to": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_double, C.c_int, C.c_double, C.c_int,
                                        C.c_int, P, C.c_uint64, U64P]),
     "mgrc_gpu_decompress": (C.c_int, [P, C.c_uint64, C.POINTER(P), IP, IP, P]),
+    "mgrc_gpu_compress_l2": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_double, C.c_int, C.c_double, C.c_int, C.c_int,
+                                       C.POINTER(P), U64P]),
+    "mgrc_gpu_compress_l2_to": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_double, C.c_int, C.c_double, C.c_int,
+                                          C.c_int, P, C.c_uint64, U64P]),
     "mgrc_gpu_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(P)]),
     "mgrc_gpu_host_free": (None, [P]),
     "mgrc_gpu_decompress_into": (C.c_int, [P, C.c_uint64, P, C.c_uint64, IP, IP, P]),

@@ -112,6 +112,7 @@ void fill_info(const ContainerInfo& ci, mgrc_container_info* info) {
   std::memset(info, 0, sizeof *info);
   info->version = ci.version;
   info->constant_field = ci.constant_field;
+  info->l2_projection = ci.l2_projection;
   info->coords_present = ci.coords_present;
   info->dtype = static_cast<uint8_t>(ci.dtype);
   info->ndims = static_cast<uint8_t>(ci.ndims);
@@ -687,7 +688,7 @@ int mgrc_gpu_profile_entry(int i, const char** name, double* ms, double* bytes) 
   });
 }
 
-int mgrc_gpu_compress_to(const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
+static int compress_to_impl(bool l2, const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
                          double tol, int norm, double smoothness, int mode, int codec, void* dst,
                          uint64_t dst_capacity, uint64_t* out_len) {
   return guarded([&] {
@@ -698,7 +699,7 @@ int mgrc_gpu_compress_to(const void* data, int dtype, int ndims, const uint64_t*
     const DType dt = to_dtype(dtype);
     ensure_device();
     Context& ctx = context_for_current_device();
-    const ContainerParts parts = compress(ctx, data, dt, g, sp, cd);
+    const ContainerParts parts = l2 ? compress_l2(ctx, data, dt, g, sp, cd) : compress(ctx, data, dt, g, sp, cd);
     *out_len = parts.total();
     if (!dst) return;
     if (dst_capacity < parts.total()) raise(Errc::invalid_argument, "destination buffer too small");
@@ -706,7 +707,7 @@ int mgrc_gpu_compress_to(const void* data, int dtype, int ndims, const uint64_t*
   });
 }
 
-int mgrc_gpu_compress(const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
+static int compress_impl(bool l2, const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
                       double tol, int norm, double smoothness, int mode, int codec, uint8_t** out,
                       uint64_t* out_len) {
   return guarded([&] {
@@ -717,7 +718,7 @@ int mgrc_gpu_compress(const void* data, int dtype, int ndims, const uint64_t* sh
     const DType dt = to_dtype(dtype);
     ensure_device();
     Context& ctx = context_for_current_device();
-    const ContainerParts parts = compress(ctx, data, dt, g, sp, cd);
+    const ContainerParts parts = l2 ? compress_l2(ctx, data, dt, g, sp, cd) : compress(ctx, data, dt, g, sp, cd);
     uint8_t* buf = static_cast<uint8_t*>(std::malloc(parts.total() + 1));
     if (!buf) throw std::bad_alloc();
     try {
@@ -729,6 +730,32 @@ int mgrc_gpu_compress(const void* data, int dtype, int ndims, const uint64_t* sh
     *out = buf;
     *out_len = parts.total();
   });
+}
+
+int mgrc_gpu_compress_to(const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
+                         double tol, int norm, double smoothness, int mode, int codec, void* dst,
+                         uint64_t dst_capacity, uint64_t* out_len) {
+  return compress_to_impl(false, data, dtype, ndims, shape, coords, tol, norm, smoothness, mode, codec, dst,
+                          dst_capacity, out_len);
+}
+
+int mgrc_gpu_compress_l2_to(const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
+                            double tol, int norm, double smoothness, int mode, int codec, void* dst,
+                            uint64_t dst_capacity, uint64_t* out_len) {
+  return compress_to_impl(true, data, dtype, ndims, shape, coords, tol, norm, smoothness, mode, codec, dst,
+                          dst_capacity, out_len);
+}
+
+int mgrc_gpu_compress(const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
+                      double tol, int norm, double smoothness, int mode, int codec, uint8_t** out,
+                      uint64_t* out_len) {
+  return compress_impl(false, data, dtype, ndims, shape, coords, tol, norm, smoothness, mode, codec, out, out_len);
+}
+
+int mgrc_gpu_compress_l2(const void* data, int dtype, int ndims, const uint64_t* shape, const double* const* coords,
+                         double tol, int norm, double smoothness, int mode, int codec, uint8_t** out,
+                         uint64_t* out_len) {
+  return compress_impl(true, data, dtype, ndims, shape, coords, tol, norm, smoothness, mode, codec, out, out_len);
 }
 
 int mgrc_gpu_decompress_into(const uint8_t* in, uint64_t len, void* dst, uint64_t dst_capacity, int* dtype,

@@ -231,9 +231,10 @@ ContainerInfo parse_header(const uint8_t* p, uint64_t n) {
   info.version = r.u16();
   if (info.version != 1) raise(Errc::unsupported_version, "container version " + std::to_string(info.version));
   const uint8_t flags = r.u8();
-  if (flags & ~0x03u) raise(Errc::corrupt_stream, "unknown header flags");
+  if (flags & ~(0x03u | kFlagL2Projection)) raise(Errc::corrupt_stream, "unknown header flags");
   info.constant_field = flags & 1u;
   info.coords_present = (flags & 2u) != 0;
+  info.l2_projection = (flags & kFlagL2Projection) != 0;
   const uint8_t dt = r.u8();
   if (dt > 1) raise(Errc::corrupt_stream, "unknown element type");
   info.dtype = static_cast<DType>(dt);
@@ -293,6 +294,7 @@ std::string describe(const ContainerInfo& info) {
   line("version", std::to_string(info.version));
   line("constant_field", info.constant_field ? "1" : "0");
   line("coords_present", info.coords_present ? "1" : "0");
+  if (info.l2_projection) line("l2_projection", "1");
   line("dtype", info.dtype == DType::f32 ? "f32" : "f64");
   line("ndims", std::to_string(info.ndims));
   std::string sh;

@@ -97,10 +97,15 @@ Hierarchy build_hierarchy(const Grid& g);
 std::vector<double> initial_bin_widths(double tau_abs, const ErrorSpec& spec, int d, int L);
 
 // ---- container header (container.cpp:28-55, :133-188) --------------------
+// Header flag of containers of the L²-corrected decomposition (our extension;
+// the reference rejects unknown flags, container.cpp:143).
+constexpr uint8_t kFlagL2Projection = 0x04;
+
 struct ContainerInfo {  // container.hpp:37-51
   uint16_t version = 1;
   bool constant_field = false;
   bool coords_present = false;
+  bool l2_projection = false;  // flag 0x04
   DType dtype = DType::f64;
   int ndims = 0;
   uint64_t shape[kMaxDims] = {0, 0, 0, 0};

@@ -31,6 +31,7 @@
 #include "rows.cuh"
 #include "huff.cuh"
 #include "huff_tf.cuh"
+#include "transform.hpp"
 #include "serial_sum.cuh"
 #include "pipeline.hpp"
 #include "context.hpp"
@@ -608,6 +609,121 @@ GlobalStats global_stats(Context& ctx, const void* data, DType dtype, uint64_t n
 // ---------------------------------------------------------------------------
 // compress
 
+// Lossless stage of a container (codec.cpp:431-453) from the zigzag codes on
+// the device and their varint histogram (sh->hist): codebook (K4, host),
+// packing (K5), CRC, header.
+static void lossless_stage(Context& ctx, Prof& prof, void* zzp, bool wide, uint64_t N, const Grid& grid,
+                           DType dtype, const ErrorSpec& spec, const std::vector<double>& widths, Codec codec,
+                           ContainerParts& out) {
+  cudaStream_t s = ctx.stream;
+  Scratch* sh = ctx.sh();
+  // lossless stage (codec.cpp:431-453)
+  std::vector<uint8_t> table_bytes;
+  const uint8_t* dev_payload = nullptr;
+  uint64_t dev_len = 0;
+  if (codec == Codec::raw) {
+    auto* raw = ctx.bits.get<long long>(N * 8 + 16);
+    prof.begin("raw_encode", static_cast<double>(N) * ((wide ? 8 : 4) + 8));
+    if (wide)
+      k_raw_encode<<<grid_blocks(N, 256), 256, 0, s>>>(static_cast<unsigned long long*>(zzp), N, raw);
+    else
+      k_raw_encode<<<grid_blocks(N, 256), 256, 0, s>>>(static_cast<uint32_t*>(zzp), N, raw);
+    check_launch("k_raw_encode");
+    prof.end();
+    dev_payload = reinterpret_cast<const uint8_t*>(raw);
+    dev_len = N * 8;
+  } else {
+    CodeTable table;
+    if (codec == Codec::huffman) {
+      table = build_code_table(reinterpret_cast<const uint64_t*>(sh->hist));  // K4 on host: 256 symbols
+      write_table_header(table_bytes, table);
+    } else {
+      for (int b = 0; b < 256; ++b) {
+        table.lengths[b] = 8;
+        table.codes[b] = static_cast<uint32_t>(b);
+      }
+      table.nsym = 256;
+      table.max_len = 8;
+    }
+    if (codec == Codec::varint || table.nsym >= 2) {
+      // total bits = Σ_sym count·len, known before packing
+      unsigned long long total_bits = 0;
+      for (int b = 0; b < 256; ++b) total_bits += sh->hist[b] * table.lengths[b];
+      struct {
+        uint32_t codes[256];
+        uint8_t lens[256];
+      } tab;
+      for (int b = 0; b < 256; ++b) {
+        tab.codes[b] = table.codes[b];
+        tab.lens[b] = table.lengths[b];
+      }
+      auto* dtab = ctx.codes.get<uint8_t>(sizeof tab);
+      CK(cudaMemcpyAsync(dtab, &tab, sizeof tab, cudaMemcpyHostToDevice, s));
+      const uint32_t* dcodes = reinterpret_cast<const uint32_t*>(dtab);
+      const uint8_t* dlens = dtab + 1024;
+      const uint64_t ntiles = (N + kPackTile - 1) / kPackTile;
+      // workspace: status[ntiles] | tile_start[ntiles+1] | edge_first | edge_last | ticket
+      const size_t ws = ntiles * 8 + (ntiles + 1) * 8 + ntiles * 4 * 2 + 16;
+      auto* wsp = ctx.tiles.get<uint8_t>(ws);
+      auto* status = reinterpret_cast<unsigned long long*>(wsp);
+      auto* tstart = status + ntiles;
+      auto* efirst = reinterpret_cast<uint32_t*>(tstart + ntiles + 1);
+      auto* elast = efirst + ntiles;
+      auto* ticket = elast + ntiles;
+      CK(cudaMemsetAsync(status, 0, ntiles * 8, s));
+      CK(cudaMemsetAsync(ticket, 0, 4, s));
+      CK(cudaMemcpyAsync(tstart + ntiles, &total_bits, 8, cudaMemcpyHostToDevice, s));
+      const uint64_t nbytes = (total_bits + 7) / 8;
+      const uint64_t nwords = (total_bits + 31) / 32 + 2;
+      auto* words = ctx.bits.get<uint32_t>(nwords * 4 + 16);
+      prof.begin("pack", static_cast<double>(N) * (wide ? 8 : 4) + static_cast<double>(nbytes));
+      // shared-memory image of one tile: bounded by the longest varint × the longest code
+      const int maxl = codec == Codec::varint ? 8 : table.max_len;
+      const uint32_t cap_words = static_cast<uint32_t>(
+          (static_cast<uint64_t>(kPackTile) * (wide ? 10 : 5) * static_cast<uint64_t>(maxl) + 31) / 32 + 1);
+      const size_t smem = static_cast<size_t>(cap_words + 1) * 4;
+      if (smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_pack_lb<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CK(cudaFuncSetAttribute(k_pack_lb<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                200 * 1024));
+      }
+      if (wide)
+        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<unsigned long long*>(zzp), N,
+                                                                            dcodes, dlens, status, ticket, tstart,
+                                                                            efirst, elast, words, cap_words);
+      else
+        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<uint32_t*>(zzp), N, dcodes,
+                                                                            dlens, status, ticket, tstart, efirst,
+                                                                            elast, words, cap_words);
+      check_launch("k_pack_lb");
+      k_pack_edges<<<static_cast<unsigned>((ntiles + 255) / 256), 256, 0, s>>>(tstart, ntiles, efirst, elast,
+                                                                              words);
+      check_launch("k_pack_edges");
+      prof.end();
+      dev_payload = reinterpret_cast<const uint8_t*>(words);
+      dev_len = nbytes;
+    }
+  }
+
+  // CRC-32 of the payload = crc(table header) ⊕-combined with the device part
+  uint32_t crc = crc32_host(table_bytes.data(), table_bytes.size());
+  if (dev_len) {
+    prof.begin("crc", static_cast<double>(dev_len));
+    CrcSlot slot = device_crc_launch(ctx, dev_payload, dev_len);
+    prof.end();
+    uint32_t dcrc = 0;
+    CK(cudaMemcpyAsync(&sh->fix_changed, slot.crc, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dcrc = sh->fix_changed;
+    crc = table_bytes.empty() ? dcrc : crc32_combine(crc, dcrc, dev_len);
+  }
+  const uint64_t payload_len = table_bytes.size() + dev_len;
+  append_header(out.head, grid, dtype, false, spec, widths, codec, payload_len, crc);
+  out.head.insert(out.head.end(), table_bytes.begin(), table_bytes.end());
+  out.dev = dev_payload;
+  out.dev_len = dev_len;
+}
+
 template <typename T>
 static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DType dtype, const Grid& grid,
                                  const ErrorSpec& spec, Codec codec) {
@@ -865,112 +981,274 @@ static ContainerParts compress_t(Context& ctx, const T* u_in, bool on_device, DT
   }
   if (!accepted) raise(Errc::tolerance_unreachable, "bin shrink loop exhausted after 10 passes");
 
-  // lossless stage (codec.cpp:431-453)
-  std::vector<uint8_t> table_bytes;
-  const uint8_t* dev_payload = nullptr;
-  uint64_t dev_len = 0;
-  if (codec == Codec::raw) {
-    auto* raw = ctx.bits.get<long long>(N * 8 + 16);
-    prof.begin("raw_encode", static_cast<double>(N) * ((wide ? 8 : 4) + 8));
-    if (wide)
-      k_raw_encode<<<grid_blocks(N, 256), 256, 0, s>>>(static_cast<unsigned long long*>(zzp), N, raw);
-    else
-      k_raw_encode<<<grid_blocks(N, 256), 256, 0, s>>>(static_cast<uint32_t*>(zzp), N, raw);
-    check_launch("k_raw_encode");
-    prof.end();
-    dev_payload = reinterpret_cast<const uint8_t*>(raw);
-    dev_len = N * 8;
-  } else {
-    CodeTable table;
-    if (codec == Codec::huffman) {
-      table = build_code_table(reinterpret_cast<const uint64_t*>(sh->hist));  // K4 on host: 256 symbols
-      write_table_header(table_bytes, table);
-    } else {
-      for (int b = 0; b < 256; ++b) {
-        table.lengths[b] = 8;
-        table.codes[b] = static_cast<uint32_t>(b);
-      }
-      table.nsym = 256;
-      table.max_len = 8;
-    }
-    if (codec == Codec::varint || table.nsym >= 2) {
-      // total bits = Σ_sym count·len, known before packing
-      unsigned long long total_bits = 0;
-      for (int b = 0; b < 256; ++b) total_bits += sh->hist[b] * table.lengths[b];
-      struct {
-        uint32_t codes[256];
-        uint8_t lens[256];
-      } tab;
-      for (int b = 0; b < 256; ++b) {
-        tab.codes[b] = table.codes[b];
-        tab.lens[b] = table.lengths[b];
-      }
-      auto* dtab = ctx.codes.get<uint8_t>(sizeof tab);
-      CK(cudaMemcpyAsync(dtab, &tab, sizeof tab, cudaMemcpyHostToDevice, s));
-      const uint32_t* dcodes = reinterpret_cast<const uint32_t*>(dtab);
-      const uint8_t* dlens = dtab + 1024;
-      const uint64_t ntiles = (N + kPackTile - 1) / kPackTile;
-      // workspace: status[ntiles] | tile_start[ntiles+1] | edge_first | edge_last | ticket
-      const size_t ws = ntiles * 8 + (ntiles + 1) * 8 + ntiles * 4 * 2 + 16;
-      auto* wsp = ctx.tiles.get<uint8_t>(ws);
-      auto* status = reinterpret_cast<unsigned long long*>(wsp);
-      auto* tstart = status + ntiles;
-      auto* efirst = reinterpret_cast<uint32_t*>(tstart + ntiles + 1);
-      auto* elast = efirst + ntiles;
-      auto* ticket = elast + ntiles;
-      CK(cudaMemsetAsync(status, 0, ntiles * 8, s));
-      CK(cudaMemsetAsync(ticket, 0, 4, s));
-      CK(cudaMemcpyAsync(tstart + ntiles, &total_bits, 8, cudaMemcpyHostToDevice, s));
-      const uint64_t nbytes = (total_bits + 7) / 8;
-      const uint64_t nwords = (total_bits + 31) / 32 + 2;
-      auto* words = ctx.bits.get<uint32_t>(nwords * 4 + 16);
-      prof.begin("pack", static_cast<double>(N) * (wide ? 8 : 4) + static_cast<double>(nbytes));
-      // shared-memory image of one tile: bounded by the longest varint × the longest code
-      const int maxl = codec == Codec::varint ? 8 : table.max_len;
-      const uint32_t cap_words = static_cast<uint32_t>(
-          (static_cast<uint64_t>(kPackTile) * (wide ? 10 : 5) * static_cast<uint64_t>(maxl) + 31) / 32 + 1);
-      const size_t smem = static_cast<size_t>(cap_words + 1) * 4;
-      if (smem > 48 * 1024) {
-        CK(cudaFuncSetAttribute(k_pack_lb<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CK(cudaFuncSetAttribute(k_pack_lb<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                200 * 1024));
-      }
-      if (wide)
-        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<unsigned long long*>(zzp), N,
-                                                                            dcodes, dlens, status, ticket, tstart,
-                                                                            efirst, elast, words, cap_words);
-      else
-        k_pack_lb<<<static_cast<unsigned>(ntiles), kPackThreads, smem, s>>>(static_cast<uint32_t*>(zzp), N, dcodes,
-                                                                            dlens, status, ticket, tstart, efirst,
-                                                                            elast, words, cap_words);
-      check_launch("k_pack_lb");
-      k_pack_edges<<<static_cast<unsigned>((ntiles + 255) / 256), 256, 0, s>>>(tstart, ntiles, efirst, elast,
-                                                                              words);
-      check_launch("k_pack_edges");
-      prof.end();
-      dev_payload = reinterpret_cast<const uint8_t*>(words);
-      dev_len = nbytes;
-    }
-  }
-
-  // CRC-32 of the payload = crc(table header) ⊕-combined with the device part
-  uint32_t crc = crc32_host(table_bytes.data(), table_bytes.size());
-  if (dev_len) {
-    prof.begin("crc", static_cast<double>(dev_len));
-    CrcSlot slot = device_crc_launch(ctx, dev_payload, dev_len);
-    prof.end();
-    uint32_t dcrc = 0;
-    CK(cudaMemcpyAsync(&sh->fix_changed, slot.crc, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    dcrc = sh->fix_changed;
-    crc = table_bytes.empty() ? dcrc : crc32_combine(crc, dcrc, dev_len);
-  }
-  const uint64_t payload_len = table_bytes.size() + dev_len;
-  append_header(out.head, grid, dtype, false, spec, widths, codec, payload_len, crc);
-  out.head.insert(out.head.end(), table_bytes.begin(), table_bytes.end());
-  out.dev = dev_payload;
-  out.dev_len = dev_len;
+  lossless_stage(ctx, prof, zzp, wide, N, grid, dtype, spec, widths, codec, out);
   return out;
+}
+
+
+// ---------------------------------------------------------------------------
+// Containers of the L²-corrected decomposition (opt-in, header flag 0x04; the
+// reference rejects the flag, container.cpp:143): coefficients from
+// forward_transform_l2, the reference's quantiser / lossless stage / accept
+// loop on top (quantize.cpp:72-132, container.cpp:93-123); the a-posteriori
+// error is the corrected inverse of the residuals.
+
+namespace dev {
+
+template <typename T>
+__global__ void k_widen(const T* __restrict__ u, uint64_t n, double* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<double>(u[i]);
+}
+
+// q = rne(c/δ_tag), r = c − q·δ, zz = zigzag(q), varint-byte histogram, row-major node order.
+template <int D, typename Z>
+__global__ void __launch_bounds__(256) k_quant_zz(GridDev g, Widths W, const double* __restrict__ c, Z* __restrict__ zz,
+                                                  double* __restrict__ r, unsigned long long* hist, QuantFlags* fl) {
+  __shared__ uint32_t sh[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
+  __syncthreads();
+  uint32_t hsym = 0, hcnt = 0;
+  unsigned long long ovf = 0;
+  unsigned wide = 0;
+  for (uint64_t n = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; n < g.N;
+       n += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    decompose<D>(g, n, i);
+    const double delta = W.w[node_tag<D>(g, i)];
+    const double cv = c[n];
+    const double scaled = __ddiv_rn(cv, delta);
+    if (!(fabs(scaled) < 9223372036854775808.0)) {  // quantize.cpp:113-116
+      ++ovf;
+      continue;
+    }
+    const long long q = __double2ll_rn(scaled);
+    r[n] = __dsub_rn(cv, __dmul_rn(__ll2double_rn(q), delta));
+    const uint64_t z = zigzag(q);
+    if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
+    zz[n] = static_cast<Z>(z);
+    hist_varint(sh, z, hsym, hcnt);
+  }
+  hist_flush(sh, hsym, hcnt);
+  if (ovf) atomicAdd(&fl->overflow, ovf);
+  if (wide) atomicOr(&fl->wide, 1u);
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x)
+    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
+}
+
+// max |e| (f64 data) or max |src − (double)(float)(src − e)| (f32 data, container.cpp:96-107); or, with
+// `store`, the per-node error for the ordered RMS.
+template <typename T>
+__global__ void k_l2_check(const T* __restrict__ src, const double* __restrict__ e, uint64_t n, int cast,
+                           double* store, unsigned long long* red) {
+  double m = 0.0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double x = e[i];
+    if (cast) {
+      const double sv = static_cast<double>(src[i]);
+      x = __dsub_rn(sv, static_cast<double>(__double2float_rn(__dsub_rn(sv, x))));
+    }
+    if (store) store[i] = x;
+    else m = fmax(m, fabs(x));
+  }
+  if (!store) {
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(red, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+// c = (double)unzigzag(zz)·δ_tag (quantize.cpp:134-158)
+template <int D, typename Z>
+__global__ void __launch_bounds__(256) k_dequant_zz(GridDev g, Widths W, const Z* __restrict__ zz,
+                                                    double* __restrict__ c) {
+  for (uint64_t n = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; n < g.N;
+       n += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t i[4] = {0, 0, 0, 0};
+    decompose<D>(g, n, i);
+    c[n] = __dmul_rn(__ll2double_rn(unzigzag(static_cast<uint64_t>(zz[n]))), W.w[node_tag<D>(g, i)]);
+  }
+}
+
+template <typename T>
+__global__ void k_narrow(const double* __restrict__ v, uint64_t n, T* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<T>(v[i]);
+}
+
+}  // namespace dev
+
+template <typename Z>
+struct QuantZZ {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const double* c, Z* zz, double* r,
+                    unsigned long long* hist, QuantFlags* fl) {
+      k_quant_zz<D, Z><<<grid_blocks(g.N, 256), 256, 0, s>>>(g, W, c, zz, r, hist, fl);
+      check_launch("k_quant_zz");
+    }
+  };
+};
+template <typename Z>
+struct DequantZZ {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const Widths& W, const Z* zz, double* c) {
+      k_dequant_zz<D, Z><<<grid_blocks(g.N, 256), 256, 0, s>>>(g, W, zz, c);
+      check_launch("k_dequant_zz");
+    }
+  };
+};
+
+// the reference's level-weighted estimator (error_control.cpp:72-101) from the residuals, exactly
+static double level_weighted_serial(Context& ctx, DevHier& dh, const double* r, const Widths& lw, uint64_t N) {
+  double* masked = ctx.l2b.get<double>(N * 8);
+  double acc = 0.0;
+  for (int l = 0; l <= dh.h.L; ++l) {
+    by_dim<LevelMask::L>(dh.g.d, ctx.stream, dh.g, r, l, masked);
+    acc += lw.w[l] * exact_serial_sum(ctx, masked, DType::f64, N, true, 0.0);
+  }
+  return std::sqrt(acc / static_cast<double>(N));
+}
+
+template <typename T>
+static ContainerParts compress_l2_t(Context& ctx, const T* u_in, bool on_device, DType dtype, const Grid& grid,
+                                    const ErrorSpec& spec, Codec codec) {
+  Prof prof(ctx);
+  cudaStream_t s = ctx.stream;
+  const uint64_t N = grid.count();
+  g_cstats = CompressStats{0.0, -1.0, 0, 0};
+  const T* u = u_in;
+  if (!on_device) {
+    T* d = ctx.in.get<T>(N * sizeof(T));
+    CK(cudaMemcpyAsync(d, u_in, N * sizeof(T), cudaMemcpyHostToDevice, s));
+    u = d;
+  }
+  Scratch* sd = ctx.sd();
+  Scratch* sh = ctx.sh();
+  launch_stats(ctx, u, N, &sd->stats);
+  CK(cudaMemcpyAsync(&sh->stats, &sd->stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (sh->stats.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
+  if (!(spec.tol > 0.0)) raise(Errc::invalid_state, "tolerance must be > 0");
+  const double mn = key_to_double(sh->stats.min_key), mx = key_to_double(sh->stats.max_key);
+  ContainerParts out;
+  if (mx == mn) {  // constant field: the same header-only container as the reference (container.cpp:57-69)
+    T val;
+    CK(cudaMemcpyAsync(&val, u + 4096 * ((N - 1) / 4096), sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double v = static_cast<double>(val);
+    std::vector<uint8_t> payload(8);
+    std::memcpy(payload.data(), &v, 8);
+    append_header(out.head, grid, dtype, true, spec, {0.0}, codec, 8, crc32_host(payload.data(), 8));
+    out.host_tail = payload;
+    return out;
+  }
+  double tau;
+  if (spec.mode == Mode::abs) tau = spec.tol;
+  else if (spec.norm == Norm::inf) tau = spec.tol * (mx - mn);
+  else {
+    const double rms = std::sqrt(blocked_sumsq(ctx, u, N) / static_cast<double>(N));
+    if (rms == 0.0) raise(Errc::degenerate_data, "relative bound on a zero field");
+    tau = spec.tol * rms;
+  }
+  DevHier& dh = device_hierarchy(ctx, grid);
+  const int L = dh.h.L;
+  std::vector<double> widths = initial_bin_widths(tau, spec, grid.d, L);
+  g_cstats = CompressStats{tau, -1.0, 0, 0};
+  // f64 values, the corrected coefficients
+  double* u64 = ctx.r.get<double>(N * 8);
+  if (std::is_same<T, double>::value) {
+    CK(cudaMemcpyAsync(u64, u, N * 8, cudaMemcpyDeviceToDevice, s));
+  } else {
+    k_widen<<<grid_blocks(N, 256), 256, 0, s>>>(u, N, u64);
+    check_launch("k_widen");
+  }
+  double* c = ctx.e.get<double>(N * 8);
+  prof.begin("forward_l2", static_cast<double>(N) * (sizeof(T) + 8));
+  forward_transform_l2(ctx, u64, c, grid);
+  prof.end();
+  const bool level_weighted = spec.norm == Norm::s && spec.smoothness != 0.0;
+  Widths lw{};
+  for (int l = 0; l <= L; ++l)
+    lw.w[l] = std::exp2(2.0 * spec.smoothness * (static_cast<double>(l) - static_cast<double>(L)));
+  double* r = ctx.tftab.get<double>(N * 8);
+  bool wide = false, accepted = false;
+  void* zzp = nullptr;
+  for (int pass = 0; pass < 10; ++pass) {
+    const Widths W = to_widths(widths);
+    for (;;) {  // u32 codes first, u64 when some |q| >= 2^31
+      CK(cudaMemsetAsync(&sd->qflags, 0, sizeof(QuantFlags), s));
+      CK(cudaMemsetAsync(sd->hist, 0, sizeof sd->hist, s));
+      prof.begin("quantize", static_cast<double>(N) * (8 + (wide ? 8 : 4) + 8));
+      if (wide) {
+        auto* zz = ctx.zz.get<unsigned long long>(N * 8);
+        zzp = zz;
+        by_dim<QuantZZ<unsigned long long>::template L>(grid.d, s, dh.g, W, c, zz, r, sd->hist, &sd->qflags);
+      } else {
+        auto* zz = ctx.zz.get<uint32_t>(N * 4);
+        zzp = zz;
+        by_dim<QuantZZ<uint32_t>::template L>(grid.d, s, dh.g, W, c, zz, r, sd->hist, &sd->qflags);
+      }
+      prof.end();
+      CK(cudaMemcpyAsync(&sh->qflags, &sd->qflags, sizeof(QuantFlags), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(sh->hist, sd->hist, sizeof sh->hist, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (sh->qflags.overflow)
+        raise(Errc::overflow, std::to_string(sh->qflags.overflow) + " coefficients exceed the 63-bit symbol range");
+      if (sh->qflags.wide && !wide) {
+        wide = true;
+        continue;
+      }
+      break;
+    }
+    double achieved;
+    prof.begin("check_l2", static_cast<double>(N) * 24);
+    if (level_weighted) {
+      achieved = level_weighted_serial(ctx, dh, r, lw, N);
+    } else {
+      double* e = ctx.bits.get<double>(N * 8 + 16);
+      inverse_transform_l2(ctx, r, e, grid);  // the error of the reconstruction (linear in the coefficients)
+      const int cast = dtype == DType::f32;
+      if (spec.norm == Norm::inf) {
+        CK(cudaMemsetAsync(&sd->red_bits, 0, 8, s));
+        k_l2_check<<<grid_blocks(N, 256), 256, 0, s>>>(u, e, N, cast, nullptr, &sd->red_bits);
+        check_launch("k_l2_check");
+        CK(cudaMemcpyAsync(&sh->red_bits, &sd->red_bits, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::memcpy(&achieved, &sh->red_bits, 8);
+      } else {  // S(0): ordered RMS (exec.cpp:47-71) of e / of the f32 cast error
+        if (cast) {
+          k_l2_check<<<grid_blocks(N, 256), 256, 0, s>>>(u, e, N, 1, e, nullptr);
+          check_launch("k_l2_check");
+        }
+        achieved = std::sqrt(blocked_sumsq(ctx, static_cast<const double*>(e), N) / static_cast<double>(N));
+      }
+    }
+    prof.end();
+    g_cstats.achieved = achieved;
+    g_cstats.passes = pass + 1;
+    g_cstats.decided_by = 2;
+    if (achieved <= tau * (1.0 - 1e-9)) {
+      accepted = true;
+      break;
+    }
+    for (double& w : widths) w *= 0.5;
+  }
+  if (!accepted) raise(Errc::tolerance_unreachable, "bin shrink loop exhausted after 10 passes");
+  lossless_stage(ctx, prof, zzp, wide, N, grid, dtype, spec, widths, codec, out);
+  out.head[6] |= kFlagL2Projection;
+  return out;
+}
+
+ContainerParts compress_l2(Context& ctx, const void* data, DType dtype, const Grid& grid, const ErrorSpec& spec,
+                           Codec codec) {
+  const bool dev = is_device_pointer(data);
+  if (dtype == DType::f32) return compress_l2_t(ctx, static_cast<const float*>(data), dev, dtype, grid, spec, codec);
+  return compress_l2_t(ctx, static_cast<const double*>(data), dev, dtype, grid, spec, codec);
 }
 
 ContainerParts compress(Context& ctx, const void* data, DType dtype, const Grid& grid, const ErrorSpec& spec,
@@ -1275,10 +1553,24 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
       }
     }
     prof.begin("recon", static_cast<double>(N) * ((wide ? 8 : 4) + dtype_size(info.dtype)));
-    if (wide)
+    if (info.l2_projection) {  // dequantise, corrected recomposition, narrow (container.cpp:210-261)
+      double* c = ctx.r.get<double>(N * 8);
+      if (wide)
+        by_dim<DequantZZ<unsigned long long>::template L>(info.ndims, s, dh.g, W,
+                                                          ctx.zz.get<unsigned long long>(N * 8), c);
+      else
+        by_dim<DequantZZ<uint32_t>::template L>(info.ndims, s, dh.g, W, ctx.zz.get<uint32_t>(N * 4), c);
+      double* v = info.dtype == DType::f64 ? static_cast<double*>(dout) : ctx.tftab.get<double>(N * 8);
+      inverse_transform_l2(ctx, c, v, grid);
+      if (info.dtype == DType::f32) {
+        k_narrow<<<grid_blocks(N, 256), 256, 0, s>>>(v, N, static_cast<float*>(dout));
+        check_launch("k_narrow");
+      }
+    } else if (wide) {
       run_recon(ctx, dh, ctx.zz.get<unsigned long long>(N * 8), W, info.dtype, dout, N);
-    else
+    } else {
       run_recon(ctx, dh, ctx.zz.get<uint32_t>(N * 4), W, info.dtype, dout, N);
+    }
     prof.end();
   }
   } catch (const Error&) {

@@ -48,6 +48,10 @@ const std::vector<PhaseTime>& context_profile(Context& c);
 ContainerParts compress(Context& ctx, const void* data, DType dtype, const Grid& grid, const ErrorSpec& spec,
                         Codec codec);
 
+// The same on the L²-corrected decomposition (header flag 0x04; transform.cu).
+ContainerParts compress_l2(Context& ctx, const void* data, DType dtype, const Grid& grid, const ErrorSpec& spec,
+                           Codec codec);
+
 // Parses and validates; decodes into `out` (host or device, capacity checked).
 DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void* out, uint64_t out_capacity_bytes);
 ContainerInfo inspect_any(Context& ctx, const uint8_t* in, uint64_t len);

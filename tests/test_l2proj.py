@@ -150,3 +150,73 @@ def test_gpu_l2_transform_coords_and_device(mg, oracle):
     assert np.array_equal(c.cpu().numpy().view(np.uint64), want.view(np.uint64))
     back = mg.inverse_transform(c, mg.make_grid(shape, cs), l2=True)
     assert np.max(np.abs(back.cpu().numpy() - u)) <= 1e-14
+
+
+# ---------------------------------------------------------------------------
+# containers of the corrected decomposition (header flag 0x04)
+
+L2_CASES = [  # (shape, dtype, tol, norm, s, mode, codec, coords seed)
+    ((33, 17, 9), np.float32, 1e-4, 0, 0.0, 1, 2, None),
+    ((65, 65, 65), np.float64, 1e-3, 0, 0.0, 1, 2, None),
+    ((129, 130), np.float64, 1e-3, 1, 1.0, 1, 2, None),
+    ((129, 130), np.float64, 1e-3, 1, 0.0, 1, 2, None),
+    ((40, 33, 17), np.float32, 1e-3, 1, 0.0, 1, 2, None),
+    ((6, 5, 4, 3), np.float64, 1e-2, 0, 0.0, 0, 2, None),
+    ((17, 12, 9), np.float64, 1e-3, 0, 0.0, 0, 2, 3),
+    ((33, 20), np.float64, 1e-3, 0, 0.0, 1, 1, None),
+    ((33, 20), np.float32, 1e-3, 0, 0.0, 1, 0, None),
+    ((2, 9), np.float64, 1e-3, 0, 0.0, 0, 2, None),
+]
+
+
+def test_l2_container_rejected_by_reference_parser(oracle):
+    u = field(oracle, (33, 17)).astype(np.float64)
+    blob = l2proj.compress_l2(u, 1e-3, 0, 0.0, 1, 2)
+    with pytest.raises(binding.OracleError) as e:
+        oracle.decompress(blob)
+    assert e.value.name == "CorruptStream"  # unknown header flags (container.cpp:143)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", L2_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"-{c[1].__name__}-n{c[3]}s{c[4]}c{c[6]}")
+def test_gpu_l2_container_matches_oracle(mg, oracle, case):
+    shape, dt, tol, norm, s, mode, codec, seed = case
+    coords = None
+    if seed is not None:
+        rng = np.random.default_rng(seed)
+        coords = [np.cumsum(rng.uniform(0.05, 1.0, n)) - 1.0 for n in shape]
+    u = field(oracle, shape).astype(dt)
+    want = l2proj.compress_l2(u, tol, norm, s, mode, codec, coords)
+    spec = mg.ErrorSpec(tol, mg.Norm(norm), s, mg.Mode(mode))
+    got = mg.compress(u, mg.make_grid(shape, coords), spec, mg.Codec(codec), l2=True)
+    assert got == want
+    info = mg.inspect(got)
+    assert info.l2_projection and "l2_projection: 1" in mg.describe(got)
+    back = mg.decompress(got)
+    ref = l2proj.decompress_l2(want, coords)
+    assert np.array_equal(back.view(np.uint8), ref.view(np.uint8))
+    err = back.astype(np.float64) - u.astype(np.float64)
+    tau = oracle.absolute_tolerance(u, tol, norm, s, mode)
+    if norm == 0:
+        assert np.max(np.abs(err)) <= tau
+    elif s == 0.0:
+        assert np.sqrt(np.mean(err * err)) <= tau
+
+
+@pytest.mark.gpu
+def test_gpu_l2_constant_and_device_buffers(mg, oracle):
+    import torch
+
+    u = np.full((9, 33), 2.5)
+    assert mg.compress(u, l2=True) == oracle.compress(u, 1e-3, 0, 0.0, 0, 2)  # constant: the reference container
+    v = field(oracle, (40, 21, 9))
+    du = torch.from_numpy(v).cuda()
+    spec = mg.ErrorSpec(1e-4, mg.Norm.inf, 0.0, mg.Mode.rel)
+    n = mg.compress_to(du, None, mg.make_grid(v.shape), spec, l2=True)
+    dst = torch.empty(n, dtype=torch.uint8, device="cuda")
+    mg.compress_to(du, dst, mg.make_grid(v.shape), spec, l2=True)
+    blob = bytes(dst.cpu().numpy())
+    assert blob == l2proj.compress_l2(v, 1e-4, 0, 0.0, 1, 2)
+    out = torch.empty_like(du)
+    mg.decompress_into(dst, out)
+    assert np.array_equal(out.cpu().numpy(), l2proj.decompress_l2(blob))
