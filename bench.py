@@ -68,6 +68,15 @@ DEFAULT_WORKLOAD = "cfg2_513cubed_f32_inf_rel1e-4"
 CHUNKED_WORKLOAD = "cfg5_2049cubed_f32_chunked_rel1e-4"
 WORKLOADS[CHUNKED_WORKLOAD] = ((2049, 2049, 2049), "f32", 1e-4, 0, 0.0, 1)
 CHUNK_MEM = 257 * 2049 * 2049 * 4
+# configs[3] as stated: "1025^3 fp64 decompose+recompose round trip" — one step = forward_transform +
+# inverse_transform on the device (transform.hpp:24-30), metric = 2·N·8 bytes / step time
+TRANSFORM_WORKLOADS = {
+    "cfg4_1025cubed_f64_roundtrip": ((1025, 1025, 1025), False),
+    "cfg4_1025cubed_f64_roundtrip_l2proj": ((1025, 1025, 1025), True),
+}
+# the opt-in L2-projection correction (row f3) on configs[1]'s field
+L2_WORKLOADS = {"cfg2_513cubed_f32_inf_rel1e-4_l2proj": ((513, 513, 513), "f32", 1e-4, 0, 0.0, 1)}
+WORKLOADS.update(L2_WORKLOADS)
 
 
 def peaks():
@@ -105,7 +114,8 @@ def multisine_torch(shape, device):
 
 
 # dominant phase -> its main kernel (for the ncu DRAM traffic lookup)
-PHASE_KERNEL = {"fine": "k_fine_warp", "huff_maps": "k_tfd_maps", "huff_count": "k_tfd_count", "huff_emit": "k_tfd_emit",
+PHASE_KERNEL = {"forward": "k_forward", "inverse": "k_inverse_level", "forward_l2": "k_l2_line",
+                "inverse_l2": "k_l2_line", "quantize": "k_quant_zz", "check_l2": "k_l2_line", "fine": "k_fine_warp", "huff_maps": "k_tfd_maps", "huff_count": "k_tfd_count", "huff_emit": "k_tfd_emit",
                 "recon": "k_recon_warp", "pack": "k_pack_lb", "coarse_check": "k_cq_warp", "crc": "k_crc_coal",
                 "stats": "k_stats"}
 
@@ -577,6 +587,76 @@ def run_chunked(args, world, rank, local, coll_dev):
     return 0
 
 
+def run_transform(args, world, rank, local, coll_dev):
+    """configs[3]: decompose + recompose round trip of the 1025^3 fp64 multisine field on the device
+    (forward_transform then inverse_transform, transform.hpp:24-30; ``_l2proj``: with the L2-projection
+    correction).  Metric: 2·N·8 bytes per step (the field is read once and written once per direction) / time;
+    the reconstruction is checked against the input every run.  One field per rank (weak)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_05994_b200 as mg
+
+    mg.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    mg.set_stream(stream.cuda_stream)
+    shape, l2 = TRANSFORM_WORKLOADS[args.workload]
+    N = int(np.prod(shape))
+    u = multisine_torch(shape, "cuda")
+    grid = mg.make_grid(shape)
+    c = mg.forward_transform(u, grid, l2=l2)
+    back = mg.inverse_transform(c, grid, l2=l2)
+    rel_err = float((back - u).abs().max()) / float(u.max() - u.min())
+    for _ in range(args.warmup - 1):
+        c = mg.forward_transform(u, grid, l2=l2)
+        back = mg.inverse_transform(c, grid, l2=l2)
+    acc = PhaseAcc()
+    mg.set_profiling(True)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = mg.launch_count()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for _ in range(args.steps):
+        c = mg.forward_transform(u, grid, l2=l2)
+        acc.add(mg)
+        back = mg.inverse_transform(c, grid, l2=l2)
+        acc.add(mg)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    launches = mg.launch_count() - l0
+    clk = clocks.stop()
+    mg.set_profiling(False)
+    ms = g0.elapsed_time(g1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    roof, phases = acc.roofline(args.steps, args.workload)
+    if rank == 0:
+        line = {
+            "metric": "decompose+recompose round trip GB/s (2 x N x 8 bytes per step)",
+            "value": 2.0 * N * 8 * world / (ms_step * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic multisine field (test_support.hpp:43-62), generated on the GPU",
+            "config": {"workload": args.workload, "shape": list(shape), "l2_projection": l2,
+                       "l2": "inputs/outputs exceed the 126 MB L2; no flush"},
+            "max_rel_roundtrip_err": rel_err, "roofline": roof, "phases_ms_per_step": phases,
+            "gpu_launches": int(launches), "clocks": clk, "host": host_info(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 
@@ -674,7 +754,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+    ap.add_argument("--workload", default=None, choices=sorted(list(WORKLOADS) + list(TRANSFORM_WORKLOADS)),
                     help="default: configs[1] (513^3 f32) at N=1, configs[4] (2049^3 f32 chunked) at N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -709,6 +789,8 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.workload == CHUNKED_WORKLOAD:
         return run_chunked(args, world, rank, local, coll_dev)
+    if args.workload in TRANSFORM_WORKLOADS:
+        return run_transform(args, world, rank, local, coll_dev)
 
     import paper_2401_05994_b200 as mg
 
@@ -739,8 +821,10 @@ def main():
         dist.all_gather(allt, t)
         return [int(x.item()) for x in allt]
 
+    l2 = args.workload in L2_WORKLOADS
+
     def step_device():
-        n = mg.compress_to(u, dst, grid, spec, mg.Codec.huffman)
+        n = mg.compress_to(u, dst, grid, spec, mg.Codec.huffman, l2=l2)
         sizes = gather_sizes(n)
         mg.decompress_into(dst[:n], out)
         return n, sizes
@@ -749,7 +833,7 @@ def main():
     for _ in range(args.warmup):
         clen, sizes = step_device()
     torch.cuda.synchronize()
-    mg.compress_to(u, dst, grid, spec, mg.Codec.huffman)
+    mg.compress_to(u, dst, grid, spec, mg.Codec.huffman, l2=l2)
     cstats = mg.last_compress_stats()  # the accept decision (tau_abs, achieved error, passes)
 
     # correctness of the measured path: the error bound on the reconstruction, in the reference's own
@@ -792,7 +876,7 @@ def main():
     for k in range(args.steps):
         a, b, c = ev[k]
         a.record(stream)
-        n = mg.compress_to(u, dst, grid, spec, mg.Codec.huffman)
+        n = mg.compress_to(u, dst, grid, spec, mg.Codec.huffman, l2=l2)
         for name, ms, by in mg.last_profile():
             phase_ms[name] = phase_ms.get(name, 0.0) + ms
             phase_bytes[name] = phase_bytes.get(name, 0.0) + by
