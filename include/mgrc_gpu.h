@@ -179,6 +179,54 @@ MGRC_GPU_API int mgrc_gpu_quantize(const double* c, int ndims, const uint64_t* s
 MGRC_GPU_API int mgrc_gpu_dequantize(const int64_t* q, int ndims, const uint64_t* shape, const double* const* coords,
                                      const double* widths, int nwidths, double* c);
 
+/* ---- MDR refactor / recompose (refactor.hpp:81-117) ----------------------
+ * refactor: multilevel coefficients per level in node scan order, B-bit
+ * fixed point against the level exponent, split into B bit planes (plane 0
+ * interleaves the sign with the top magnitude bit), each (level, plane)
+ * segment canonical-Huffman coded with its CRC-32 — byte-identical to the
+ * reference's segments.  request: the reference's greedy planner.
+ * reconstruct: applies segments in per-level prefix order to a
+ * device-resident state and synthesises the field (inverse transform). */
+typedef struct {
+  int ndims;
+  uint64_t shape[4];
+  int nlevels;
+  uint32_t planes;
+  int32_t level_exponents[65]; /* INT32_MIN: the level is empty (all coefficients 0) */
+  uint64_t level_counts[65];
+  double value_min, value_max, value_rms;
+} mgrc_mdr_manifest;
+typedef struct {
+  uint64_t bytes, raw_bits;
+  uint32_t crc32;
+} mgrc_mdr_segment;
+
+/* refactor (refactor.cpp:144-218): f64 input (host or device); *store is an
+ * opaque handle (mgrc_gpu_mdr_store_free). */
+MGRC_GPU_API int mgrc_gpu_mdr_refactor(const double* u, int ndims, const uint64_t* shape,
+                                       const double* const* coords, uint32_t planes, void** store);
+/* The store's manifest and its (nlevels+1)*planes segment table (level-major; segs nullable). */
+MGRC_GPU_API int mgrc_gpu_mdr_store_manifest(const void* store, mgrc_mdr_manifest* m, mgrc_mdr_segment* segs);
+/* A segment payload (owned by the store). */
+MGRC_GPU_API int mgrc_gpu_mdr_store_segment(const void* store, uint32_t level, uint32_t plane, const uint8_t** data,
+                                            uint64_t* len);
+MGRC_GPU_API void mgrc_gpu_mdr_store_free(void* store);
+/* request (refactor.cpp:226-272) from a state with fetched[l] planes (NULL: none). */
+MGRC_GPU_API int mgrc_gpu_mdr_request(const mgrc_mdr_manifest* m, const mgrc_mdr_segment* segs, double tol_abs,
+                                      int norm, double smoothness, const uint32_t* fetched, uint32_t* levels,
+                                      uint32_t* planes, uint64_t cap, uint64_t* n, uint64_t* total_bytes,
+                                      double* predicted, int* satisfiable);
+/* A retrieval session (make_initial_state, refactor.cpp:210-221) on the current device. */
+MGRC_GPU_API int mgrc_gpu_mdr_session_new(const mgrc_mdr_manifest* m, const mgrc_mdr_segment* segs,
+                                          const double* const* coords, void** session);
+/* reconstruct (refactor.cpp:274-357): applies the n segments (their payloads in
+ * request order; checksum and per-level prefix order enforced) and writes the
+ * refined field to out (host or device, prod(shape) doubles). */
+MGRC_GPU_API int mgrc_gpu_mdr_reconstruct(void* session, const uint32_t* levels, const uint32_t* planes, uint64_t n,
+                                          const uint8_t* const* payloads, const uint64_t* lens, int norm,
+                                          double smoothness, double* out, double* accrued, uint32_t* fetched_out);
+MGRC_GPU_API void mgrc_gpu_mdr_session_free(void* session);
+
 /* Non-finite flag, min and max of an array (host or device) — the per-rank
  * statistics of the multi-GPU driver's global REL normalisation. */
 MGRC_GPU_API int mgrc_gpu_field_stats(const void* data, int dtype, uint64_t n, double* min, double* max,

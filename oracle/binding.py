@@ -344,3 +344,107 @@ def get(kind: str = "restatement") -> Oracle:
 
 def available(kind: str) -> bool:
     return LIBS[kind].exists()
+
+
+# ---------------------------------------------------------------------------
+# MDR refactor / request / reconstruct of the reference library (refactor.hpp:81-117);
+# only the compiled reference provides them (the C restatement does not).
+
+
+class RefStore:
+    """A reference RefactoredStore (opaque handle) with its manifest JSON and segment payloads."""
+
+    def __init__(self, lib, handle):
+        self.lib, self.h = lib, handle
+        p = C.c_char_p()
+        rc = lib.oc_mdr_manifest_json(self.h, C.byref(p))
+        if rc:
+            raise OracleError(rc, lib.oc_last_error().decode())
+        self.manifest_json = C.string_at(p).decode()
+        lib.oc_free(p)
+
+    def segment(self, level: int, plane: int) -> bytes:
+        out = P()
+        n = C.c_uint64()
+        rc = self.lib.oc_mdr_segment(self.h, level, plane, C.byref(out), C.byref(n))
+        if rc:
+            raise OracleError(rc, self.lib.oc_last_error().decode())
+        b = bytes((C.c_uint8 * n.value).from_address(out.value)) if n.value else b""
+        self.lib.oc_free(out)
+        return b
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.oc_mdr_free(self.h)
+            self.h = None
+
+
+def mdr_lib():
+    o = get("reference")
+    L = o.lib
+    L.oc_mdr_refactor.restype = P
+    L.oc_mdr_refactor.argtypes = [P, C.c_int, P, P, C.c_uint32]
+    L.oc_mdr_manifest_json.argtypes = [P, C.POINTER(C.c_char_p)]
+    L.oc_mdr_segment.argtypes = [P, C.c_uint32, C.c_uint32, C.POINTER(P), U64P]
+    L.oc_mdr_free.argtypes = [P]
+    L.oc_mdr_request.argtypes = [C.c_char_p, C.c_double, C.c_int, C.c_double, P, P, P, C.c_uint64, U64P, U64P,
+                                 C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    L.oc_mdr_session.restype = P
+    L.oc_mdr_session.argtypes = [C.c_char_p, P]
+    L.oc_mdr_reconstruct.argtypes = [P, P, P, C.c_uint64, C.c_int, C.c_double, P, C.POINTER(C.c_double)]
+    L.oc_mdr_session_free.argtypes = [P]
+    L.oc_free.argtypes = [P]
+    return L
+
+
+def mdr_refactor(u, planes=32, coords=None) -> RefStore:
+    L = mdr_lib()
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    shape = _shape_arr(u.shape)
+    h = L.oc_mdr_refactor(_ptr(u), len(shape), _ptr(shape), _ptr(_coords_arr(coords)), planes)
+    if not h:
+        raise OracleError(1, L.oc_last_error().decode())
+    return RefStore(L, h)
+
+
+def mdr_request(manifest_json: str, tol_abs: float, norm=0, s=0.0, fetched=None):
+    """-> (segments [(level, plane)], total_bytes, predicted, satisfiable) from a state with `fetched` planes."""
+    L = mdr_lib()
+    cap = 4096
+    lv = np.zeros(cap, dtype=np.uint32)
+    pl = np.zeros(cap, dtype=np.uint32)
+    f = None if fetched is None else np.ascontiguousarray(fetched, dtype=np.uint32)
+    n, by = C.c_uint64(), C.c_uint64()
+    pred, sat = C.c_double(), C.c_int()
+    rc = L.oc_mdr_request(manifest_json.encode(), tol_abs, norm, s, _ptr(f), _ptr(lv), _ptr(pl), cap, C.byref(n),
+                          C.byref(by), C.byref(pred), C.byref(sat))
+    if rc:
+        raise OracleError(rc, L.oc_last_error().decode())
+    return [(int(lv[i]), int(pl[i])) for i in range(n.value)], by.value, pred.value, bool(sat.value)
+
+
+class RefSession:
+    """A reference retrieval session over a RefStore (RetrievalState kept between reconstructs)."""
+
+    def __init__(self, store: RefStore, count: int):
+        self.L = mdr_lib()
+        self.store = store
+        self.count = count
+        self.h = self.L.oc_mdr_session(store.manifest_json.encode(), store.h)
+        if not self.h:
+            raise OracleError(1, self.L.oc_last_error().decode())
+
+    def reconstruct(self, segments, norm=0, s=0.0):
+        lv = np.ascontiguousarray([a for a, _ in segments] or [0], dtype=np.uint32)
+        pl = np.ascontiguousarray([b for _, b in segments] or [0], dtype=np.uint32)
+        out = np.zeros(self.count, dtype=np.float64)
+        acc = C.c_double()
+        rc = self.L.oc_mdr_reconstruct(self.h, _ptr(lv), _ptr(pl), len(segments), norm, s, _ptr(out), C.byref(acc))
+        if rc:
+            raise OracleError(rc, self.L.oc_last_error().decode())
+        return out, acc.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.oc_mdr_session_free(self.h)
+            self.h = None

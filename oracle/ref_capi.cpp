@@ -30,6 +30,7 @@
 #include "mgrc/exec.hpp"
 #include "mgrc/grid.hpp"
 #include "mgrc/quantize.hpp"
+#include "mgrc/refactor.hpp"
 #include "mgrc/transform.hpp"
 #include "support/test_support.hpp"
 
@@ -448,6 +449,97 @@ int oc_compress_chunked(const void* data, int dtype, int ndims, const uint64_t* 
     *out_len = file.size();
   });
 }
+
+
+// ---- MDR refactor / request / reconstruct (refactor.hpp:81-117) -----------
+// The reference's own functions; a store and a retrieval session are opaque
+// handles (test infrastructure for the GPU refactor's parity).
+
+struct OcSession {
+  mgrc::StoreManifest manifest;
+  const mgrc::RefactoredStore* store;
+  mgrc::RetrievalState state;
+};
+
+void* oc_mdr_refactor(const double* u, int ndims, const uint64_t* shape, const double* coords, uint32_t planes) {
+  void* out = nullptr;
+  if (guard([&] {
+        const auto g = grid_of(ndims, shape, coords);
+        auto* st = new mgrc::RefactoredStore(
+            mgrc::refactor(std::span<const double>(u, count_of(ndims, shape)), g, planes));
+        out = st;
+      }) != 0)
+    return nullptr;
+  return out;
+}
+
+int oc_mdr_manifest_json(void* store, char** out) {
+  return guard([&] {
+    const std::string j = mgrc::manifest_to_json(static_cast<mgrc::RefactoredStore*>(store)->manifest);
+    *out = static_cast<char*>(std::malloc(j.size() + 1));
+    std::memcpy(*out, j.c_str(), j.size() + 1);
+  });
+}
+
+int oc_mdr_segment(void* store, uint32_t l, uint32_t p, uint8_t** out, uint64_t* n) {
+  return guard([&] {
+    const auto& seg = static_cast<mgrc::RefactoredStore*>(store)->segments.at(l).at(p);
+    *out = dup(seg);
+    *n = seg.size();
+  });
+}
+
+void oc_mdr_free(void* store) { delete static_cast<mgrc::RefactoredStore*>(store); }
+
+int oc_mdr_request(const char* manifest_json, double tol_abs, int norm, double s, const uint32_t* fetched,
+                   uint32_t* levels, uint32_t* planes, uint64_t cap, uint64_t* nseg, uint64_t* bytes,
+                   double* predicted, int* satisfiable) {
+  return guard([&] {
+    const mgrc::StoreManifest m = mgrc::manifest_from_json(manifest_json);
+    mgrc::RetrievalState st = mgrc::make_initial_state(m);
+    for (std::size_t l = 0; l < st.planes_fetched.size(); ++l) st.planes_fetched[l] = fetched ? fetched[l] : 0;
+    const mgrc::SegmentRequest r = mgrc::request(m, tol_abs, static_cast<mgrc::Norm>(norm), s, st);
+    *nseg = r.segments.size();
+    for (std::size_t i = 0; i < r.segments.size() && i < cap; ++i) {
+      levels[i] = r.segments[i].level;
+      planes[i] = r.segments[i].plane;
+    }
+    *bytes = r.total_bytes;
+    *predicted = r.predicted.value;
+    *satisfiable = r.satisfiable ? 1 : 0;
+  });
+}
+
+void* oc_mdr_session(const char* manifest_json, void* store) {
+  void* out = nullptr;
+  if (guard([&] {
+        auto* ss = new OcSession;
+        ss->manifest = mgrc::manifest_from_json(manifest_json);
+        ss->store = static_cast<mgrc::RefactoredStore*>(store);
+        ss->state = mgrc::make_initial_state(ss->manifest);
+        out = ss;
+      }) != 0)
+    return nullptr;
+  return out;
+}
+
+int oc_mdr_reconstruct(void* sess, const uint32_t* levels, const uint32_t* planes, uint64_t nseg, int norm, double s,
+                       double* out, double* accrued) {
+  return guard([&] {
+    auto* ss = static_cast<OcSession*>(sess);
+    mgrc::SegmentRequest req;
+    for (uint64_t i = 0; i < nseg; ++i) req.segments.push_back({levels[i], planes[i]});
+    req.predicted.norm = static_cast<mgrc::Norm>(norm);
+    req.predicted.smoothness = s;
+    const auto* store = ss->store;
+    const mgrc::SegmentSource src = [store](std::uint32_t l, std::uint32_t p) { return store->segments.at(l).at(p); };
+    const std::vector<double> v = mgrc::reconstruct(ss->manifest, src, req, ss->state);
+    std::memcpy(out, v.data(), v.size() * sizeof(double));
+    *accrued = ss->state.accrued.value;
+  });
+}
+
+void oc_mdr_session_free(void* sess) { delete static_cast<OcSession*>(sess); }
 
 void oc_multisine(int ndims, const uint64_t* shape, double* out) {
   std::vector<std::size_t> s(shape, shape + ndims);

@@ -53,6 +53,17 @@ SIGNATURES = {
     "mgrc_gpu_decompress_chunked_multi": (C.c_int, [P, C.c_uint64, C.c_int, C.POINTER(P), IP, IP, P]),
     "mgrc_gpu_field_stats": (C.c_int, [P, C.c_int, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double), IP]),
     "mgrc_gpu_serial_sumsq": (C.c_int, [P, C.c_int, C.c_uint64, C.c_double, C.POINTER(C.c_double)]),
+    # MDR (struct arguments as void*; paper_2401_05994_b200/mdr.py binds the structs)
+    "mgrc_gpu_mdr_refactor": (C.c_int, [P, C.c_int, P, P, C.c_uint32, C.POINTER(P)]),
+    "mgrc_gpu_mdr_store_manifest": (C.c_int, [P, P, P]),
+    "mgrc_gpu_mdr_store_segment": (C.c_int, [P, C.c_uint32, C.c_uint32, C.POINTER(P), U64P]),
+    "mgrc_gpu_mdr_store_free": (None, [P]),
+    "mgrc_gpu_mdr_request": (C.c_int, [P, P, C.c_double, C.c_int, C.c_double, P, P, P, C.c_uint64, U64P, U64P,
+                                       C.POINTER(C.c_double), IP]),
+    "mgrc_gpu_mdr_session_new": (C.c_int, [P, P, P, C.POINTER(P)]),
+    "mgrc_gpu_mdr_reconstruct": (C.c_int, [P, P, P, C.c_uint64, P, P, C.c_int, C.c_double, P,
+                                           C.POINTER(C.c_double), P]),
+    "mgrc_gpu_mdr_session_free": (None, [P]),
     "mgrc_gpu_last_error": (C.c_char_p, []),
     "mgrc_gpu_free": (None, [P]),
     "mgrc_gpu_set_device": (C.c_int, [C.c_int]),

@@ -379,6 +379,31 @@ std::vector<uint64_t> gather_sizes(int G, const std::vector<std::vector<uint64_t
   return sizes;
 }
 
+MdrManifest manifest_from(const mgrc_mdr_manifest* m, const mgrc_mdr_segment* segs, const double* const* coords) {
+  require(m != nullptr && segs != nullptr, "null argument");
+  MdrManifest r;
+  r.grid = grid_from(m->ndims, m->shape, coords);
+  r.nlevels = m->nlevels;
+  r.planes = m->planes;
+  if (m->nlevels < 0 || m->nlevels > 64) raise(Errc::corrupt_stream, "manifest level count out of range");
+  for (int l = 0; l <= m->nlevels; ++l) {
+    r.exps.push_back(m->level_exponents[l]);
+    r.counts.push_back(m->level_counts[l]);
+    std::vector<MdrSegment> row(m->planes);
+    for (uint32_t p = 0; p < m->planes; ++p) {
+      const mgrc_mdr_segment& sg = segs[static_cast<size_t>(l) * m->planes + p];
+      row[p].bytes = sg.bytes;
+      row[p].raw_bits = sg.raw_bits;
+      row[p].crc = sg.crc32;
+    }
+    r.seg.push_back(row);
+  }
+  r.vmin = m->value_min;
+  r.vmax = m->value_max;
+  r.vrms = m->value_rms;
+  return r;
+}
+
 // Multiblock compress (tools/mgrc.cpp:363-484) on `ngpus` ranks: global REL
 // normalisation, per-block ABS compress with the block's coordinate slice,
 // the u32 count | u64 offsets | containers framing.  Blocks split only along
@@ -955,5 +980,107 @@ int mgrc_gpu_decompress_chunked_multi(const uint8_t* in, uint64_t len, int ngpus
                                       uint64_t* shape) {
   return guarded([&] { decompress_chunked_impl(in, len, ngpus, out, dtype, ndims, shape); });
 }
+
+int mgrc_gpu_mdr_refactor(const double* u, int ndims, const uint64_t* shape, const double* const* coords,
+                          uint32_t planes, void** store) {
+  return guarded([&] {
+    require(u != nullptr && store != nullptr, "null argument");
+    const Grid g = grid_from(ndims, shape, coords);
+    ensure_device();
+    *store = new MdrStore(mdr_refactor(context_for_current_device(), u, g, planes));
+  });
+}
+
+int mgrc_gpu_mdr_store_manifest(const void* store, mgrc_mdr_manifest* m, mgrc_mdr_segment* segs) {
+  return guarded([&] {
+    require(store != nullptr && m != nullptr, "null argument");
+    const MdrManifest& s = static_cast<const MdrStore*>(store)->m;
+    std::memset(m, 0, sizeof *m);
+    m->ndims = s.grid.d;
+    for (int a = 0; a < s.grid.d; ++a) m->shape[a] = s.grid.shape[a];
+    m->nlevels = s.nlevels;
+    m->planes = s.planes;
+    for (int l = 0; l <= s.nlevels; ++l) {
+      m->level_exponents[l] = s.exps[l];
+      m->level_counts[l] = s.counts[l];
+      for (uint32_t p = 0; segs && p < s.planes; ++p) {
+        mgrc_mdr_segment& o = segs[static_cast<size_t>(l) * s.planes + p];
+        o.bytes = s.seg[l][p].bytes;
+        o.raw_bits = s.seg[l][p].raw_bits;
+        o.crc32 = s.seg[l][p].crc;
+      }
+    }
+    m->value_min = s.vmin;
+    m->value_max = s.vmax;
+    m->value_rms = s.vrms;
+  });
+}
+
+int mgrc_gpu_mdr_store_segment(const void* store, uint32_t level, uint32_t plane, const uint8_t** data, uint64_t* len) {
+  return guarded([&] {
+    require(store != nullptr && data != nullptr && len != nullptr, "null argument");
+    const auto& pl = static_cast<const MdrStore*>(store)->payload;
+    if (level >= pl.size() || plane >= pl[level].size()) raise(Errc::invalid_state, "segment id out of range");
+    *data = pl[level][plane].data();
+    *len = pl[level][plane].size();
+  });
+}
+
+void mgrc_gpu_mdr_store_free(void* store) { delete static_cast<MdrStore*>(store); }
+
+int mgrc_gpu_mdr_request(const mgrc_mdr_manifest* m, const mgrc_mdr_segment* segs, double tol_abs, int norm,
+                         double smoothness, const uint32_t* fetched, uint32_t* levels, uint32_t* planes, uint64_t cap,
+                         uint64_t* n, uint64_t* total_bytes, double* predicted, int* satisfiable) {
+  return guarded([&] {
+    require(n != nullptr, "null argument");
+    const MdrManifest mf = manifest_from(m, segs, nullptr);
+    std::vector<uint32_t> f(mf.nlevels + 1, 0);
+    if (fetched) f.assign(fetched, fetched + mf.nlevels + 1);
+    const MdrRequest r = mdr_request(mf, tol_abs, to_spec(tol_abs, norm, smoothness, 0).norm, smoothness, f);
+    *n = r.segs.size();
+    for (size_t i = 0; i < r.segs.size() && i < cap; ++i) {
+      if (levels) levels[i] = r.segs[i].first;
+      if (planes) planes[i] = r.segs[i].second;
+    }
+    if (total_bytes) *total_bytes = r.bytes;
+    if (predicted) *predicted = r.predicted;
+    if (satisfiable) *satisfiable = r.satisfiable ? 1 : 0;
+  });
+}
+
+int mgrc_gpu_mdr_session_new(const mgrc_mdr_manifest* m, const mgrc_mdr_segment* segs, const double* const* coords,
+                             void** session) {
+  return guarded([&] {
+    require(session != nullptr, "null argument");
+    *session = mdr_session_new(manifest_from(m, segs, coords));
+  });
+}
+
+int mgrc_gpu_mdr_reconstruct(void* session, const uint32_t* levels, const uint32_t* planes, uint64_t n,
+                             const uint8_t* const* payloads, const uint64_t* lens, int norm, double smoothness,
+                             double* out, double* accrued, uint32_t* fetched_out) {
+  return guarded([&] {
+    require(session != nullptr && out != nullptr, "null argument");
+    ensure_device();
+    auto* ss = static_cast<MdrSession*>(session);
+    std::vector<std::pair<uint32_t, uint32_t>> segs;
+    std::vector<const uint8_t*> pl;
+    std::vector<uint64_t> ln;
+    for (uint64_t i = 0; i < n; ++i) {
+      segs.push_back({levels[i], planes[i]});
+      pl.push_back(payloads[i]);
+      ln.push_back(lens[i]);
+    }
+    const double a = mdr_reconstruct(context_for_current_device(), *ss, segs, pl, ln,
+                                     to_spec(1.0, norm, smoothness, 0).norm, smoothness, out);
+    if (accrued) *accrued = a;
+    if (fetched_out) {
+      const auto& f = mdr_session_fetched(ss);
+      for (size_t l = 0; l < f.size(); ++l) fetched_out[l] = f[l];
+    }
+  });
+}
+
+void mgrc_gpu_mdr_session_free(void* session) { mdr_session_free(static_cast<MdrSession*>(session)); }
 
 }  // extern "C"

@@ -155,7 +155,7 @@ __device__ __forceinline__ unsigned long long tfd_map(const uint32_t* sm, const 
 // K1: exit maps, scanned within the tile: gmap[j] = map of subsequences
 // [tile start, j] (entry of the tile -> exit of j).
 template <bool G>
-__global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+static __global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                           const uint16_t* __restrict__ lut_g, int maxlen, int ne,
                                                           uint64_t nseq, unsigned long long* __restrict__ gmap) {
   extern __shared__ uint32_t dyn[];
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t* __rest
 // maps of its chunk, a block scan combines the chunks, and each thread walks
 // its chunk from the true entry (tile 0 starts at offset 0).
 constexpr int kTfdScanThreads = 1024;
-__global__ void __launch_bounds__(kTfdScanThreads) k_tfd_tiles(const unsigned long long* __restrict__ gmap,
+static __global__ void __launch_bounds__(kTfdScanThreads) k_tfd_tiles(const unsigned long long* __restrict__ gmap,
                                                                uint64_t nseq, uint64_t ntile, int ne,
                                                                uint8_t* __restrict__ etile) {
   __shared__ unsigned long long sm[kTfdScanThreads];
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kTfdScanThreads) k_tfd_tiles(const unsigned lo
 // K3: decode every subsequence once along the true path: terminators (for the
 // value offsets) and whether it ends inside a varint.
 template <bool G>
-__global__ void __launch_bounds__(kTfdThreads) k_tfd_count(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+static __global__ void __launch_bounds__(kTfdThreads) k_tfd_count(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                            const uint16_t* __restrict__ lut_g, int maxlen,
                                                            uint64_t nseq, const unsigned long long* __restrict__ gmap,
                                                            const uint8_t* __restrict__ etile, TfdSeq* __restrict__ seqs,
@@ -299,7 +299,9 @@ __device__ __forceinline__ void tfd_emit_values(const uint32_t* sm, const LT& lu
     }
     p += l;
     br.consume(l);
-    uint64_t acc = ent & 0x7Fu;
+    // a terminator carries its whole symbol: < 0x80 for varint bytes, any byte for a raw byte stream
+    // (decode table built with every symbol terminating, mdr.cu)
+    uint64_t acc = ent & (lut_term(ent) ? 0xFFu : 0x7Fu);
     if (!lut_term(ent)) {  // continuation bytes (codec.cpp:75-86)
       for (uint32_t sh = 7;; sh += 7) {
         br.refill();
@@ -340,7 +342,7 @@ __device__ __forceinline__ void tfd_emit_values(const uint32_t* sm, const LT& lu
 // K5: decode every subsequence along the true path and write the zigzag codes
 // of the varints that start in it.
 template <typename Z, bool G>
-__global__ void __launch_bounds__(kTfdThreads) k_tfd_emit(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
+static __global__ void __launch_bounds__(kTfdThreads) k_tfd_emit(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                           const uint16_t* __restrict__ lut_g, int maxlen,
                                                           uint64_t nseq, uint64_t N, const TfdSeq* __restrict__ seqs,
                                                           const unsigned long long* __restrict__ cnt,

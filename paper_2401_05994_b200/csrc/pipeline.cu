@@ -1303,7 +1303,104 @@ static void huff_smem_optin() {
   CK(cudaFuncSetAttribute(k_tfd_emit<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   CK(cudaFuncSetAttribute(k_tfd_emit<unsigned long long, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   CK(cudaFuncSetAttribute(k_tfd_emit<unsigned long long, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_emit<uint8_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
+  CK(cudaFuncSetAttribute(k_tfd_emit<uint8_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   done_mask |= bit;
+}
+
+// Transfer-function Huffman decode (huff_tf.cuh) of a coded body staged on
+// the device (zero padded by >= 64 bytes): N zigzag varint values into ctx.zz
+// (u32, or u64 once one does not fit — the return value), or, with `raw`, N
+// bytes into `raw_out` (every symbol is one byte: huffman_unpack_bytes,
+// codec.cpp:420-429).  Errors follow codec.cpp:75-86 / :370-375.
+static bool tfd_decode(Context& ctx, Prof& prof, const uint8_t* body, uint64_t body_len, const CodeTable& table,
+                       uint64_t N, bool raw, bool wide, const char* msg_truncated, const char* msg_trailing,
+                       uint8_t* raw_out) {
+  cudaStream_t s = ctx.stream;
+  Scratch* sd = ctx.sd();
+  Scratch* sh = ctx.sh();
+  std::vector<uint16_t> lut_h = build_decode_lut(table);
+  if (raw)
+    for (auto& e : lut_h) e = static_cast<uint16_t>(e | (1u << 12));  // every symbol ends a value
+        auto* lut = ctx.lut.get<uint16_t>(lut_h.size() * 2);
+        CK(cudaMemcpyAsync(lut, lut_h.data(), lut_h.size() * 2, cudaMemcpyHostToDevice, s));
+        const int maxlen = table.max_len;
+        const uint64_t T = body_len * 8;
+        const uint64_t nseq = std::max<uint64_t>(1, (T + kSeqBits - 1) / kSeqBits);
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(body);
+        const uint64_t nw = (body_len + 64) / 4;
+        huff_smem_optin();
+          // transfer-function decoder (huff_tf.cuh)
+          int minlen = 99;
+          for (int b = 0; b < 256; ++b)
+            if (table.lengths[b]) minlen = std::min<int>(minlen, table.lengths[b]);
+          const int ne = (minlen == maxlen && kSeqBits % maxlen == 0) ? 1 : maxlen;  // equal lengths: aligned
+          const uint64_t ntile = (nseq + kTfdTile - 1) / kTfdTile;
+          const unsigned ncta = static_cast<unsigned>((ntile + kTfdThreads / 32 - 1) / (kTfdThreads / 32));
+          const bool glut = lut_global(maxlen);
+          const size_t smem = tfd_smem(maxlen);
+          auto* gmap = ctx.tftab.get<unsigned long long>(nseq * 8);
+          auto* etile = ctx.tfst.get<uint8_t>(ntile + 16);
+          auto* seqs = ctx.seq.get<TfdSeq>(nseq * sizeof(TfdSeq));
+          auto* cnt = ctx.tiles.get<unsigned long long>(nseq * 8);
+          auto* toff = ctx.scan.get<unsigned long long>((nseq + 1) * 8);
+          const uint64_t nst = (nseq + kScanTile - 1) / kScanTile;
+          auto* lbst = ctx.lbws.get<unsigned long long>(nst * 8 + 32);
+          auto* lbticket = reinterpret_cast<unsigned int*>(lbst + nst);
+          auto* first_err = reinterpret_cast<unsigned long long*>(lbst + nst + 2);
+          prof.begin("huff_maps", static_cast<double>(body_len));
+          if (glut)
+            k_tfd_maps<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap);
+          else
+            k_tfd_maps<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap);
+          check_launch("k_tfd_maps");
+          k_tfd_tiles<<<1, kTfdScanThreads, 0, s>>>(gmap, nseq, ntile, ne, etile);
+          check_launch("k_tfd_tiles");
+          prof.end();
+          prof.begin("huff_count", static_cast<double>(body_len));
+          if (glut)
+            k_tfd_count<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, gmap, etile, seqs, cnt);
+          else
+            k_tfd_count<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, gmap, etile, seqs, cnt);
+          check_launch("k_tfd_count");
+          CK(cudaMemsetAsync(lbst, 0, nst * 8 + 16, s));
+          k_scan_lb<<<static_cast<unsigned>(nst), kScanThreads, 0, s>>>(cnt, toff, nseq, lbst, lbticket);
+          check_launch("k_scan_lb");
+          prof.end();
+          for (;;) {
+            CK(cudaMemsetAsync(first_err, 0xFF, 8, s));
+            DecodeStatus init{~0ull, 0u, 0u, 0u};
+            CK(cudaMemcpyAsync(&sd->dstat, &init, sizeof init, cudaMemcpyHostToDevice, s));
+            prof.begin("huff_emit", static_cast<double>(body_len) + static_cast<double>(N) * (wide ? 8 : 4));
+            auto launch = [&](auto* zz) {
+              using Z = std::remove_pointer_t<decltype(zz)>;
+              if (glut)
+                k_tfd_emit<Z, true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, cnt, toff, zz,
+                                                                     &sd->dstat, first_err);
+              else
+                k_tfd_emit<Z, false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, cnt, toff, zz,
+                                                                      &sd->dstat, first_err);
+              check_launch("k_tfd_emit");
+            };
+            if (raw) launch(raw_out);
+            else if (wide) launch(ctx.zz.get<unsigned long long>(N * 8));
+            else launch(ctx.zz.get<uint32_t>(N * 4));
+            prof.end();
+            unsigned long long ferr = 0;
+            CK(cudaMemcpyAsync(&sh->dstat, &sd->dstat, sizeof(DecodeStatus), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(&sh->red_bits, first_err, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            ferr = sh->red_bits;
+            if (ferr != ~0ull && (ferr & 3u) == 1u) raise(Errc::corrupt_stream, "varint overflows 64 bits");
+            if (ferr != ~0ull || sh->dstat.end_bit == ~0ull) raise(Errc::corrupt_stream, msg_truncated);
+            if (!sh->dstat.clean) raise(Errc::corrupt_stream, msg_trailing);
+            if (sh->dstat.wide && !wide) {
+              wide = true;
+              continue;
+            }
+            break;
+          }
+  return wide;
 }
 
 template <typename Z>
@@ -1469,87 +1566,11 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
         k_fill<<<grid_blocks(N, 256), 256, 0, s>>>(zz, N, static_cast<uint32_t>(sym));
         check_launch("k_fill");
       } else {
-        const std::vector<uint16_t> lut_h = build_decode_lut(table);
-        auto* lut = ctx.lut.get<uint16_t>(lut_h.size() * 2);
-        CK(cudaMemcpyAsync(lut, lut_h.data(), lut_h.size() * 2, cudaMemcpyHostToDevice, s));
-        const int maxlen = table.max_len;
-        const uint64_t T = body_len * 8;
-        const uint64_t nseq = std::max<uint64_t>(1, (T + kSeqBits - 1) / kSeqBits);
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(body);
-        const uint64_t nw = (body_len + 64) / 4;
-        huff_smem_optin();
-          // transfer-function decoder (huff_tf.cuh)
-          int minlen = 99;
-          for (int b = 0; b < 256; ++b)
-            if (table.lengths[b]) minlen = std::min<int>(minlen, table.lengths[b]);
-          const int ne = (minlen == maxlen && kSeqBits % maxlen == 0) ? 1 : maxlen;  // equal lengths: aligned
-          const uint64_t ntile = (nseq + kTfdTile - 1) / kTfdTile;
-          const unsigned ncta = static_cast<unsigned>((ntile + kTfdThreads / 32 - 1) / (kTfdThreads / 32));
-          const bool glut = lut_global(maxlen);
-          const size_t smem = tfd_smem(maxlen);
-          auto* gmap = ctx.tftab.get<unsigned long long>(nseq * 8);
-          auto* etile = ctx.tfst.get<uint8_t>(ntile + 16);
-          auto* seqs = ctx.seq.get<TfdSeq>(nseq * sizeof(TfdSeq));
-          auto* cnt = ctx.tiles.get<unsigned long long>(nseq * 8);
-          auto* toff = ctx.scan.get<unsigned long long>((nseq + 1) * 8);
-          const uint64_t nst = (nseq + kScanTile - 1) / kScanTile;
-          auto* lbst = ctx.lbws.get<unsigned long long>(nst * 8 + 32);
-          auto* lbticket = reinterpret_cast<unsigned int*>(lbst + nst);
-          auto* first_err = reinterpret_cast<unsigned long long*>(lbst + nst + 2);
-          prof.begin("huff_maps", static_cast<double>(body_len));
-          if (glut)
-            k_tfd_maps<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap);
-          else
-            k_tfd_maps<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap);
-          check_launch("k_tfd_maps");
-          k_tfd_tiles<<<1, kTfdScanThreads, 0, s>>>(gmap, nseq, ntile, ne, etile);
-          check_launch("k_tfd_tiles");
-          prof.end();
-          prof.begin("huff_count", static_cast<double>(body_len));
-          if (glut)
-            k_tfd_count<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, gmap, etile, seqs, cnt);
-          else
-            k_tfd_count<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, gmap, etile, seqs, cnt);
-          check_launch("k_tfd_count");
-          CK(cudaMemsetAsync(lbst, 0, nst * 8 + 16, s));
-          k_scan_lb<<<static_cast<unsigned>(nst), kScanThreads, 0, s>>>(cnt, toff, nseq, lbst, lbticket);
-          check_launch("k_scan_lb");
-          prof.end();
-          for (;;) {
-            CK(cudaMemsetAsync(first_err, 0xFF, 8, s));
-            DecodeStatus init{~0ull, 0u, 0u, 0u};
-            CK(cudaMemcpyAsync(&sd->dstat, &init, sizeof init, cudaMemcpyHostToDevice, s));
-            prof.begin("huff_emit", static_cast<double>(body_len) + static_cast<double>(N) * (wide ? 8 : 4));
-            auto launch = [&](auto* zz) {
-              using Z = std::remove_pointer_t<decltype(zz)>;
-              if (glut)
-                k_tfd_emit<Z, true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, cnt, toff, zz,
-                                                                     &sd->dstat, first_err);
-              else
-                k_tfd_emit<Z, false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, N, seqs, cnt, toff, zz,
-                                                                      &sd->dstat, first_err);
-              check_launch("k_tfd_emit");
-            };
-            if (wide) launch(ctx.zz.get<unsigned long long>(N * 8));
-            else launch(ctx.zz.get<uint32_t>(N * 4));
-            prof.end();
-            unsigned long long ferr = 0;
-            CK(cudaMemcpyAsync(&sh->dstat, &sd->dstat, sizeof(DecodeStatus), cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(&sh->red_bits, first_err, 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            ferr = sh->red_bits;
-            if (ferr != ~0ull && (ferr & 3u) == 1u) raise(Errc::corrupt_stream, "varint overflows 64 bits");
-            if (ferr != ~0ull || sh->dstat.end_bit == ~0ull)
-              raise(Errc::corrupt_stream, info.codec_id == 2 ? "Huffman stream truncated" : "truncated varint stream");
-            if (!sh->dstat.clean)
-              raise(Errc::corrupt_stream, info.codec_id == 2 ? "trailing bits after Huffman stream"
-                                                             : "trailing bytes after varint stream");
-            if (sh->dstat.wide && !wide) {
-              wide = true;
-              continue;
-            }
-            break;
-          }
+        wide = tfd_decode(ctx, prof, body, body_len, table, N, false, wide,
+                          info.codec_id == 2 ? "Huffman stream truncated" : "truncated varint stream",
+                          info.codec_id == 2 ? "trailing bits after Huffman stream"
+                                             : "trailing bytes after varint stream",
+                          nullptr);
       }
     }
     prof.begin("recon", static_cast<double>(N) * ((wide ? 8 : 4) + dtype_size(info.dtype)));
@@ -1585,6 +1606,607 @@ DecodedInfo decompress_into(Context& ctx, const uint8_t* in, uint64_t len, void*
   }
   CK(cudaStreamSynchronize(s));
   return di;
+}
+
+
+// ---------------------------------------------------------------------------
+// MDR refactor / reconstruct (refactor.cpp:144-357)
+
+namespace dev {
+
+constexpr int kBkThreads = 256, kBkPer = 4, kBkNodes = kBkThreads * kBkPer;  // nodes per bucketing block
+
+// Per block of kBkNodes consecutive nodes: the count of nodes of each level
+// (level-major: cnt[l * nblk + blk]) and the level's max |c| (bits).
+template <int D>
+__global__ void __launch_bounds__(kBkThreads) k_bk_count(GridDev g, const double* __restrict__ c, uint64_t nblk,
+                                                         unsigned long long* __restrict__ cnt,
+                                                         unsigned long long* __restrict__ lmax) {
+  __shared__ unsigned int sc[kMaxL];
+  __shared__ unsigned long long sm[kMaxL];
+  for (int l = threadIdx.x; l <= g.L; l += blockDim.x) sc[l] = 0, sm[l] = 0;
+  __syncthreads();
+  const uint64_t n0 = blockIdx.x * static_cast<uint64_t>(kBkNodes) + threadIdx.x * kBkPer;
+  for (int k = 0; k < kBkPer; ++k) {
+    const uint64_t n = n0 + k;
+    if (n >= g.N) break;
+    uint32_t i[4] = {0, 0, 0, 0};
+    decompose<D>(g, n, i);
+    const int tag = node_tag<D>(g, i);
+    atomicAdd(&sc[tag], 1u);
+    if (c) atomicMax(&sm[tag], static_cast<unsigned long long>(__double_as_longlong(fabs(c[n]))));
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l <= g.L; l += blockDim.x) {
+    cnt[static_cast<uint64_t>(l) * nblk + blockIdx.x] = sc[l];
+    if (sm[l]) atomicMax(&lmax[l], sm[l]);
+  }
+}
+
+// Node n <-> its slot in the concatenated level buckets (node scan order
+// within each level, refactor.cpp:89-113): slot = off[tag * nblk + blk] +
+// rank of n among the block's nodes of that level.  dir 0: bucket[slot] =
+// c[n]; dir 1: c[n] = the dequantised fixed-point value of the slot.
+template <int D>
+__global__ void __launch_bounds__(kBkThreads) k_bk_map(GridDev g, uint64_t nblk, const unsigned long long* __restrict__ off,
+                                                       int dir, double* __restrict__ c, double* __restrict__ bucket,
+                                                       const unsigned long long* __restrict__ mags,
+                                                       const uint8_t* __restrict__ signs, const int* __restrict__ exps,
+                                                       int planes) {
+  __shared__ unsigned int wcnt[kBkThreads / 32][kMaxL];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t n0 = blockIdx.x * static_cast<uint64_t>(kBkNodes) + threadIdx.x * kBkPer;
+  int tags[kBkPer];
+#pragma unroll
+  for (int k = 0; k < kBkPer; ++k) {
+    tags[k] = -1;
+    const uint64_t n = n0 + k;
+    if (n < g.N) {
+      uint32_t i[4] = {0, 0, 0, 0};
+      decompose<D>(g, n, i);
+      tags[k] = node_tag<D>(g, i);
+    }
+  }
+  // per level: exclusive rank of this thread's nodes among the block's (thread order = node order)
+  for (int l = 0; l <= g.L; ++l) {
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < kBkPer; ++k) mine += tags[k] == l;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wcnt[warp][l] = incl;
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int l = 0; l <= g.L; ++l) {
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < kBkPer; ++k) mine += tags[k] == l;
+    if (!__any_sync(0xffffffffu, mine)) {
+      continue;
+    }
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t before = incl - mine;
+    for (int w = 0; w < warp; ++w) before += wcnt[w][l];
+    uint64_t slot = off[static_cast<uint64_t>(l) * nblk + blockIdx.x] + before;
+#pragma unroll
+    for (int k = 0; k < kBkPer; ++k)
+      if (tags[k] == l) {
+        const uint64_t n = n0 + k;
+        if (dir == 0) {
+          bucket[slot] = c[n];
+        } else {
+          double v = 0.0;
+          const int e = exps[l];
+          if (e != kMdrEmptyExponent) {
+            const double mag = ldexp(static_cast<double>(mags[slot]), e - planes);
+            v = signs[slot] ? -mag : mag;
+          }
+          c[n] = v;
+        }
+        ++slot;
+      }
+  }
+}
+
+// Bit planes of one level (refactor.cpp:24-65): thread t takes coefficients
+// [8t, 8t+8): plane 0 (sign, then magnitude bit B-1, interleaved) gets 2
+// bytes, plane p >= 1 (magnitude bit B-1-p) one byte; MSB first, zero padded.
+// raw = [plane 0: ceil(2n/8)] [plane 1: ceil(n/8)] ...; per-plane byte histograms.
+__global__ void __launch_bounds__(256) k_mdr_planes(const double* __restrict__ v, uint64_t n, int e, int planes,
+                                                    uint8_t* __restrict__ raw, uint64_t b0, uint64_t b1,
+                                                    unsigned long long* __restrict__ hist) {
+  extern __shared__ uint32_t sh[];  // planes x 256
+  for (int t = threadIdx.x; t < planes * 256; t += blockDim.x) sh[t] = 0;
+  __syncthreads();
+  const double cap = ldexp(1.0, planes);
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t * 8 < n;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long m[8];
+    uint32_t sg = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      m[k] = 0;
+      const uint64_t i = t * 8 + k;
+      if (i < n) {
+        const double c = v[i];
+        const double tr = floor(scalbn(fabs(c), planes - e));
+        m[k] = tr >= cap ? (planes == 64 ? ~0ull : (1ull << planes) - 1ull) : static_cast<unsigned long long>(tr);
+        sg |= (c < 0.0 ? 1u : 0u) << (7 - k);
+      }
+    }
+    // plane 0: s0 m0 s1 m1 ... (two bytes)
+    uint32_t b = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) b = (b << 2) | (((sg >> (7 - k)) & 1u) << 1) | static_cast<uint32_t>((m[k] >> (planes - 1)) & 1ull);
+    const uint8_t hi = static_cast<uint8_t>(b >> 8), lo = static_cast<uint8_t>(b);
+    raw[2 * t] = hi;
+    atomicAdd(&sh[hi], 1u);
+    if (2 * t + 1 < b0) {
+      raw[2 * t + 1] = lo;
+      atomicAdd(&sh[lo], 1u);
+    }
+    for (int p = 1; p < planes; ++p) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x = (x << 1) | static_cast<uint32_t>((m[k] >> (planes - 1 - p)) & 1ull);
+      raw[b0 + static_cast<uint64_t>(p - 1) * b1 + t] = static_cast<uint8_t>(x);
+      atomicAdd(&sh[p * 256 + x], 1u);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < planes * 256; t += blockDim.x)
+    if (sh[t]) atomicAdd(hist + t, static_cast<unsigned long long>(sh[t]));
+}
+
+// Canonical-Huffman packing of a byte stream (codec.cpp:222-247, MSB first):
+// bits of each 2048-byte tile, then (after a scan of the tile totals) every
+// thread ORs its codes into the zeroed output words at its bit offset.
+constexpr int kPbThreads = 256, kPbPer = 8, kPbTile = kPbThreads * kPbPer;
+
+__global__ void __launch_bounds__(kPbThreads) k_pack_bytes_bits(const uint8_t* __restrict__ in, uint64_t n,
+                                                                const uint8_t* __restrict__ lens,
+                                                                unsigned long long* __restrict__ tile_bits) {
+  __shared__ unsigned int ws[kPbThreads / 32];
+  const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(kPbTile) + threadIdx.x * kPbPer;
+  uint32_t bits = 0;
+  for (int k = 0; k < kPbPer; ++k)
+    if (i0 + k < n) bits += __ldg(lens + in[i0 + k]);
+  for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = bits;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kPbThreads / 32; ++w) t += ws[w];
+    tile_bits[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kPbThreads) k_pack_bytes(const uint8_t* __restrict__ in, uint64_t n,
+                                                           const uint32_t* __restrict__ codes,
+                                                           const uint8_t* __restrict__ lens,
+                                                           const unsigned long long* __restrict__ tile_off,
+                                                           uint32_t* __restrict__ words) {
+  __shared__ unsigned int wsum[kPbThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(kPbTile) + threadIdx.x * kPbPer;
+  uint8_t sym[kPbPer];
+  uint32_t mine = 0;
+#pragma unroll
+  for (int k = 0; k < kPbPer; ++k) {
+    sym[k] = i0 + k < n ? in[i0 + k] : 0;
+    if (i0 + k < n) mine += __ldg(lens + sym[k]);
+  }
+  uint32_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  uint64_t pos = tile_off[blockIdx.x] + incl - mine;
+  for (int w = 0; w < warp; ++w) pos += wsum[w];
+  // a 64-bit window of stream bits starting at word pos/32
+  uint64_t acc = 0;
+  uint32_t fill = static_cast<uint32_t>(pos & 31);  // bits already consumed in the first word
+  uint64_t wi = pos >> 5;
+  auto flush_word = [&]() {
+    const uint32_t wv = static_cast<uint32_t>(acc >> 32);
+    if (wv) atomicOr(words + wi, __byte_perm(wv, 0, 0x0123));  // stream byte order in memory
+    acc <<= 32;
+    fill -= 32;
+    ++wi;
+  };
+#pragma unroll
+  for (int k = 0; k < kPbPer; ++k) {
+    if (i0 + k >= n) break;
+    const uint32_t l = __ldg(lens + sym[k]);
+    const uint64_t cd = __ldg(codes + sym[k]);
+    acc |= cd << (64 - fill - l);
+    fill += l;
+    if (fill >= 32) flush_word();
+  }
+  if (fill > 0) {
+    const uint32_t wv = static_cast<uint32_t>(acc >> 32);
+    if (wv) atomicOr(words + wi, __byte_perm(wv, 0, 0x0123));
+  }
+}
+
+// Plane p of a level into the fixed-point state (refactor.cpp:320-327).
+__global__ void k_mdr_apply(const uint8_t* __restrict__ raw, uint64_t n, int plane, int planes,
+                            unsigned long long* __restrict__ mags, uint8_t* __restrict__ signs) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t bit;
+    if (plane == 0) {
+      const uint64_t b = 2 * i;
+      signs[i] = static_cast<uint8_t>((raw[b >> 3] >> (7 - (b & 7))) & 1u);
+      bit = (raw[(b + 1) >> 3] >> (7 - ((b + 1) & 7))) & 1u;
+    } else {
+      bit = (raw[i >> 3] >> (7 - (i & 7))) & 1u;
+    }
+    mags[i] |= static_cast<unsigned long long>(bit) << (planes - 1 - plane);
+  }
+}
+
+}  // namespace dev
+
+template <int D>
+struct BkCount {
+  static void run(cudaStream_t s, const GridDev& g, const double* c, uint64_t nblk, unsigned long long* cnt,
+                  unsigned long long* lmax) {
+    k_bk_count<D><<<static_cast<unsigned>(nblk), kBkThreads, 0, s>>>(g, c, nblk, cnt, lmax);
+    check_launch("k_bk_count");
+  }
+};
+template <template <int> class F, class... Args>
+static void by_dim_raw(int d, Args&&... args) {
+  switch (d) {
+    case 1: F<1>::run(args...); break;
+    case 2: F<2>::run(args...); break;
+    case 3: F<3>::run(args...); break;
+    case 4: F<4>::run(args...); break;
+    default: raise(Errc::too_many_dims, "unsupported dimension count");
+  }
+}
+template <int D>
+struct BkMap {
+  static void run(cudaStream_t s, const GridDev& g, uint64_t nblk, const unsigned long long* off, int dir, double* c,
+                  double* bucket, const unsigned long long* mags, const uint8_t* signs, const int* exps, int planes) {
+    k_bk_map<D><<<static_cast<unsigned>(nblk), kBkThreads, 0, s>>>(g, nblk, off, dir, c, bucket, mags, signs, exps,
+                                                                    planes);
+    check_launch("k_bk_map");
+  }
+};
+
+// Level buckets of a hierarchy: per-(level, block) offsets into the
+// concatenated buckets, and each level's first slot and count.
+struct MdrLayout {
+  uint64_t nblk = 0;
+  unsigned long long* off = nullptr;  // device, (L+1)*nblk + 1
+  std::vector<uint64_t> first, count;
+  std::vector<double> lmax;
+};
+
+static MdrLayout mdr_layout(Context& ctx, DevHier& dh, const double* c, DevBuf& offbuf) {
+  cudaStream_t s = ctx.stream;
+  const GridDev& g = dh.g;
+  const int L = dh.h.L;
+  MdrLayout lay;
+  lay.nblk = (g.N + kBkNodes - 1) / kBkNodes;
+  const uint64_t m = static_cast<uint64_t>(L + 1) * lay.nblk;
+  auto* cnt = ctx.tiles.get<unsigned long long>(m * 8 + 8);
+  auto* lmax = ctx.partial.get<unsigned long long>(kMaxL * 8);
+  lay.off = offbuf.get<unsigned long long>((m + 1) * 8);
+  CK(cudaMemsetAsync(lmax, 0, kMaxL * 8, s));
+  by_dim_raw<BkCount>(g.d, s, g, c ? c : static_cast<const double*>(nullptr), lay.nblk, cnt, lmax);
+  const uint64_t nt = (m + kScanTile - 1) / kScanTile;
+  auto* st = ctx.lbws.get<unsigned long long>(nt * 8 + 16);
+  auto* ticket = reinterpret_cast<unsigned int*>(st + nt);
+  CK(cudaMemsetAsync(st, 0, nt * 8 + 16, s));
+  k_scan_lb<<<static_cast<unsigned>(nt), kScanThreads, 0, s>>>(cnt, lay.off, m, st, ticket);
+  check_launch("k_scan_lb");
+  std::vector<unsigned long long> firsts(L + 2), lm(L + 1);
+  for (int l = 0; l <= L; ++l)
+    CK(cudaMemcpyAsync(&firsts[l], lay.off + static_cast<uint64_t>(l) * lay.nblk, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&firsts[L + 1], lay.off + m, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(lm.data(), lmax, (L + 1) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int l = 0; l <= L; ++l) {
+    lay.first.push_back(firsts[l]);
+    lay.count.push_back(firsts[l + 1] - firsts[l]);
+    double d;
+    std::memcpy(&d, &lm[l], 8);
+    lay.lmax.push_back(d);
+  }
+  return lay;
+}
+
+static int level_exponent(double max_abs) {  // refactor.cpp:26-31
+  if (max_abs == 0.0) return kMdrEmptyExponent;
+  int e = 0;
+  const double m = std::frexp(max_abs, &e);
+  return m == 0.5 ? e - 1 : e;
+}
+
+MdrStore mdr_refactor(Context& ctx, const double* u, const Grid& grid, uint32_t planes) {
+  Prof prof(ctx);
+  cudaStream_t s = ctx.stream;
+  if (planes < 8 || planes > 60)  // min_planes .. max_planes (refactor.hpp:78-79)
+    raise(Errc::plane_count_out_of_range,
+          std::to_string(planes) + " planes, supported range is 8..60");
+  const uint64_t N = grid.count();
+  const bool dev = is_device_pointer(u);
+  const double* du = u;
+  if (!dev) {
+    double* d = ctx.in.get<double>(N * 8);
+    CK(cudaMemcpyAsync(d, u, N * 8, cudaMemcpyHostToDevice, s));
+    du = d;
+  }
+  Scratch* sd = ctx.sd();
+  Scratch* sh = ctx.sh();
+  launch_stats(ctx, du, N, &sd->stats);
+  CK(cudaMemcpyAsync(&sh->stats, &sd->stats, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (sh->stats.nonfinite) raise(Errc::non_finite_input, "input contains NaN or Inf");
+  MdrStore st;
+  MdrManifest& m = st.m;
+  m.grid = grid;
+  m.planes = planes;
+  m.vmin = key_to_double(sh->stats.min_key);
+  m.vmax = key_to_double(sh->stats.max_key);
+  m.vrms = std::sqrt(blocked_sumsq(ctx, du, N) / static_cast<double>(N));  // kernels::sum_squares order
+  DevHier& dh = device_hierarchy(ctx, grid);
+  const int L = dh.h.L;
+  m.nlevels = L;
+  prof.begin("mdr_forward", static_cast<double>(N) * 16);
+  double* c = ctx.r.get<double>(N * 8);
+  forward_transform(ctx, du, c, grid);
+  prof.end();
+  prof.begin("mdr_bucket", static_cast<double>(N) * 16);
+  const MdrLayout lay = mdr_layout(ctx, dh, c, ctx.scan);
+  double* bucket = ctx.e.get<double>(N * 8);
+  by_dim_raw<BkMap>(grid.d, s, dh.g, lay.nblk, lay.off, 0, c, bucket, nullptr, nullptr, nullptr, 0);
+  prof.end();
+  m.counts = lay.count;
+  m.exps.resize(L + 1);
+  m.seg.assign(L + 1, std::vector<MdrSegment>(planes));
+  st.payload.assign(L + 1, std::vector<std::vector<uint8_t>>(planes));
+  prof.begin("mdr_segments", static_cast<double>(N) * 8);
+  for (int l = 0; l <= L; ++l) {
+    m.exps[l] = level_exponent(lay.lmax[l]);
+    if (m.exps[l] == kMdrEmptyExponent) continue;
+    const uint64_t n = lay.count[l];
+    const uint64_t b0 = (2 * n + 7) / 8, b1 = (n + 7) / 8;
+    const uint64_t rawlen = b0 + b1 * (planes - 1);
+    uint8_t* raw = ctx.bits.get<uint8_t>(rawlen + 16);
+    auto* hist = ctx.lbws.get<unsigned long long>(static_cast<size_t>(planes) * 256 * 8);
+    CK(cudaMemsetAsync(hist, 0, static_cast<size_t>(planes) * 256 * 8, s));
+    const size_t smem = static_cast<size_t>(planes) * 256 * 4;
+    CK(cudaFuncSetAttribute(k_mdr_planes, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_mdr_planes<<<grid_blocks((n + 7) / 8, 256), 256, smem, s>>>(bucket + lay.first[l], n, m.exps[l],
+                                                                  static_cast<int>(planes), raw, b0, b1, hist);
+    check_launch("k_mdr_planes");
+    std::vector<unsigned long long> hh(static_cast<size_t>(planes) * 256);
+    CK(cudaMemcpyAsync(hh.data(), hist, hh.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint32_t p = 0; p < planes; ++p) {
+      const uint8_t* seg = raw + (p == 0 ? 0 : b0 + (p - 1) * b1);
+      const uint64_t len = p == 0 ? b0 : b1;
+      // huffman_pack_bytes (codec.cpp:399-418): table header + MSB-first code stream
+      const CodeTable table = build_code_table(reinterpret_cast<const uint64_t*>(hh.data() + p * 256));
+      std::vector<uint8_t> out;
+      write_table_header(out, table);
+      if (table.nsym >= 2) {
+        uint64_t total_bits = 0;
+        for (int b = 0; b < 256; ++b) total_bits += hh[p * 256 + b] * table.lengths[b];
+        struct {
+          uint32_t codes[256];
+          uint8_t lens[256];
+        } tab;
+        for (int b = 0; b < 256; ++b) tab.codes[b] = table.codes[b], tab.lens[b] = table.lengths[b];
+        auto* dtab = ctx.codes.get<uint8_t>(sizeof tab);
+        CK(cudaMemcpyAsync(dtab, &tab, sizeof tab, cudaMemcpyHostToDevice, s));
+        const uint64_t ntile = (len + kPbTile - 1) / kPbTile;
+        auto* tbits = ctx.tfst.get<unsigned long long>(ntile * 8 + 8);
+        auto* toff = ctx.tftab.get<unsigned long long>((ntile + 1) * 8);
+        k_pack_bytes_bits<<<static_cast<unsigned>(ntile), kPbThreads, 0, s>>>(seg, len, dtab + 1024, tbits);
+        check_launch("k_pack_bytes_bits");
+        const uint64_t nt = (ntile + kScanTile - 1) / kScanTile;
+        auto* lst = ctx.lbws.get<unsigned long long>(static_cast<size_t>(planes) * 256 * 8 + nt * 8 + 32);
+        auto* st2 = lst + static_cast<size_t>(planes) * 256;  // after the (consumed) histograms
+        auto* ticket = reinterpret_cast<unsigned int*>(st2 + nt);
+        CK(cudaMemsetAsync(st2, 0, nt * 8 + 16, s));
+        k_scan_lb<<<static_cast<unsigned>(nt), kScanThreads, 0, s>>>(tbits, toff, ntile, st2, ticket);
+        check_launch("k_scan_lb");
+        const uint64_t nbytes = (total_bits + 7) / 8;
+        auto* words = ctx.zz.get<uint32_t>(((total_bits + 31) / 32 + 2) * 4);
+        CK(cudaMemsetAsync(words, 0, ((total_bits + 31) / 32 + 2) * 4, s));
+        k_pack_bytes<<<static_cast<unsigned>(ntile), kPbThreads, 0, s>>>(
+            seg, len, reinterpret_cast<const uint32_t*>(dtab), dtab + 1024, toff, words);
+        check_launch("k_pack_bytes");
+        const size_t h = out.size();
+        out.resize(h + nbytes);
+        CK(cudaMemcpyAsync(out.data() + h, words, nbytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+      }
+      MdrSegment& sg = m.seg[l][p];
+      sg.raw_bits = n * (p == 0 ? 2 : 1);
+      sg.bytes = out.size();
+      sg.crc = crc32_host(out.data(), out.size());
+      st.payload[l][p] = std::move(out);
+    }
+  }
+  prof.end();
+  return st;
+}
+
+// segment_estimator (error_control.cpp:110-153)
+double mdr_estimator(const MdrManifest& m, const std::vector<uint32_t>& fetched, Norm norm, double s) {
+  const int L = m.nlevels;
+  std::vector<double> rho(L + 1, 0.0);
+  for (int l = 0; l <= L; ++l) {
+    if (fetched[l] > m.planes) raise(Errc::invalid_state, "level " + std::to_string(l) + " claims too many planes");
+    if (m.exps[l] == kMdrEmptyExponent) continue;
+    rho[l] = std::ldexp(1.0, m.exps[l] - static_cast<int>(fetched[l]) + 1);
+  }
+  if (norm == Norm::inf) {
+    const double cells = std::ldexp(1.0, m.grid.d);
+    double acc = rho[0];
+    for (int l = 1; l <= L; ++l) acc += cells * rho[l];
+    return acc;
+  }
+  double acc = 0.0;
+  const double Ld = static_cast<double>(L);
+  const double n = static_cast<double>(m.grid.count());
+  for (int l = 0; l <= L; ++l)
+    acc += std::exp2(2.0 * s * (static_cast<double>(l) - Ld)) * rho[l] * rho[l] * static_cast<double>(m.counts[l]) / n;
+  return std::sqrt(acc);
+}
+
+// request (refactor.cpp:226-272): the greedy plan
+MdrRequest mdr_request(const MdrManifest& m, double tol_abs, Norm norm, double s, std::vector<uint32_t> fetched) {
+  if (!(tol_abs > 0.0)) raise(Errc::invalid_state, "tolerance must be > 0");
+  if (fetched.size() != static_cast<size_t>(m.nlevels) + 1) raise(Errc::invalid_state, "state does not match the manifest");
+  for (uint32_t b : fetched)
+    if (b > m.planes) raise(Errc::invalid_state, "state claims more planes than the store");
+  MdrRequest req;
+  double current = mdr_estimator(m, fetched, norm, s);
+  while (current > tol_abs) {
+    int best = -1;
+    double best_ratio = -1.0, best_after = 0.0;
+    for (int l = 0; l <= m.nlevels; ++l) {
+      if (fetched[l] >= m.planes) continue;
+      if (m.exps[l] == kMdrEmptyExponent) continue;
+      ++fetched[l];
+      const double after = mdr_estimator(m, fetched, norm, s);
+      --fetched[l];
+      const double decrease = current - after;
+      if (decrease <= 0.0) continue;
+      const uint64_t size = m.seg[l][fetched[l]].bytes;
+      const double ratio = decrease / static_cast<double>(size > 0 ? size : 1);
+      if (ratio > best_ratio) {
+        best_ratio = ratio;
+        best = l;
+        best_after = after;
+      }
+    }
+    if (best < 0) break;
+    req.segs.push_back({static_cast<uint32_t>(best), fetched[best]});
+    req.bytes += m.seg[best][fetched[best]].bytes;
+    ++fetched[best];
+    current = best_after;
+  }
+  req.predicted = mdr_estimator(m, fetched, norm, s);
+  req.satisfiable = req.predicted <= tol_abs;
+  return req;
+}
+
+class MdrSession {
+ public:
+  MdrManifest m;
+  std::vector<uint32_t> fetched;
+  DevBuf mags, signs, off, exps;
+  bool ready = false;
+  MdrLayout lay;
+};
+
+MdrSession* mdr_session_new(const MdrManifest& m) {
+  auto* ss = new MdrSession;
+  ss->m = m;
+  ss->fetched.assign(m.nlevels + 1, 0);
+  return ss;
+}
+void mdr_session_free(MdrSession* s) { delete s; }
+const std::vector<uint32_t>& mdr_session_fetched(const MdrSession* s) { return s->fetched; }
+
+double mdr_reconstruct(Context& ctx, MdrSession& ss, const std::vector<std::pair<uint32_t, uint32_t>>& segs,
+                       const std::vector<const uint8_t*>& payloads, const std::vector<uint64_t>& lens, Norm norm,
+                       double sm, double* out) {
+  Prof prof(ctx);
+  cudaStream_t s = ctx.stream;
+  const MdrManifest& m = ss.m;
+  const uint64_t N = m.grid.count();
+  DevHier& dh = device_hierarchy(ctx, m.grid);
+  if (dh.h.L != m.nlevels) raise(Errc::corrupt_stream, "manifest level count does not match the shape");
+  if (!ss.ready) {  // make_initial_state: zero accumulators, the bucket layout of the hierarchy
+    ss.lay = mdr_layout(ctx, dh, nullptr, ss.off);
+    for (int l = 0; l <= m.nlevels; ++l)
+      if (ss.lay.count[l] != m.counts[l]) raise(Errc::corrupt_stream, "manifest level counts do not match the shape");
+    auto* mg = ss.mags.get<unsigned long long>(N * 8);
+    auto* sg = ss.signs.get<uint8_t>(N + 16);
+    CK(cudaMemsetAsync(mg, 0, N * 8, s));
+    CK(cudaMemsetAsync(sg, 0, N, s));
+    int* ex = ss.exps.get<int>(kMaxL * 4);
+    CK(cudaMemcpyAsync(ex, m.exps.data(), m.exps.size() * 4, cudaMemcpyHostToDevice, s));
+    ss.ready = true;
+  }
+  auto* mags = ss.mags.get<unsigned long long>(N * 8);
+  auto* signs = ss.signs.get<uint8_t>(N + 16);
+  prof.begin("mdr_apply", 0);
+  for (size_t i = 0; i < segs.size(); ++i) {  // refactor.cpp:279-329
+    const uint32_t l = segs[i].first, p = segs[i].second;
+    if (l > static_cast<uint32_t>(m.nlevels) || p >= m.planes) raise(Errc::invalid_state, "segment id out of range");
+    if (p != ss.fetched[l])
+      raise(Errc::prefix_violation, "level " + std::to_string(l) + " expects plane " + std::to_string(ss.fetched[l]) +
+                                        ", got " + std::to_string(p));
+    const MdrSegment& meta = m.seg[l][p];
+    if (m.exps[l] == kMdrEmptyExponent) {
+      ++ss.fetched[l];
+      continue;
+    }
+    if (lens[i] != meta.bytes || crc32_host(payloads[i], lens[i]) != meta.crc)
+      raise(Errc::checksum_mismatch, "segment l" + std::to_string(l) + "_b" + std::to_string(p) +
+                                         ".bin does not match the manifest");
+    const uint64_t expect_bits = m.counts[l] * (p == 0 ? 2 : 1);
+    if (meta.raw_bits != expect_bits) raise(Errc::corrupt_stream, "segment bit count mismatch");
+    const uint64_t nraw = (expect_bits + 7) / 8;
+    // huffman_unpack_bytes (codec.cpp:420-429)
+    uint64_t used = 0;
+    const CodeTable table = read_table_header(payloads[i], lens[i], &used);
+    uint8_t* raw = ctx.bits.get<uint8_t>(nraw + 64);
+    if (table.nsym == 0) raise(Errc::corrupt_stream, "read past empty Huffman stream");
+    if (table.nsym == 1) {
+      int sym = 0;
+      for (int b = 0; b < 256; ++b)
+        if (table.lengths[b]) sym = b;
+      if (lens[i] != used) raise(Errc::corrupt_stream, "trailing data after Huffman stream");
+      CK(cudaMemsetAsync(raw, sym, nraw, s));
+    } else {
+      const uint64_t body_len = lens[i] - used;
+      uint8_t* body = ctx.in.get<uint8_t>(body_len + 64);
+      CK(cudaMemsetAsync(body + (body_len & ~uint64_t{15}), 0, 64, s));
+      CK(cudaMemcpyAsync(body, payloads[i] + used, body_len, cudaMemcpyHostToDevice, s));
+      huff_smem_optin();
+      tfd_decode(ctx, prof, body, body_len, table, nraw, true, false, "Huffman stream truncated",
+                 "trailing data after Huffman stream", raw);
+    }
+    k_mdr_apply<<<grid_blocks(m.counts[l], 256), 256, 0, s>>>(raw, m.counts[l], static_cast<int>(p),
+                                                               static_cast<int>(m.planes), mags + ss.lay.first[l],
+                                                               signs + ss.lay.first[l]);
+    check_launch("k_mdr_apply");
+    ++ss.fetched[l];
+  }
+  prof.end();
+  const double accrued = mdr_estimator(m, ss.fetched, norm, sm);
+  // scatter the fixed-point values back into coefficient layout and invert (refactor.cpp:331-357)
+  prof.begin("mdr_inverse", static_cast<double>(N) * 24);
+  double* c = ctx.r.get<double>(N * 8);
+  by_dim_raw<BkMap>(m.grid.d, s, dh.g, ss.lay.nblk, ss.lay.off, 1, c, static_cast<double*>(nullptr), mags, signs,
+                    ss.exps.get<int>(kMaxL * 4), static_cast<int>(m.planes));
+  inverse_transform(ctx, c, out, m.grid);
+  prof.end();
+  return accrued;
 }
 
 }  // namespace mgrc_gpu

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -94,5 +95,47 @@ double exact_serial_sum(Context& ctx, const void* v, DType dtype, uint64_t n, bo
 // s0 + Σ v_i² serially in index order over a host or device array (the
 // continuation of the CLI's scan_stats sum, tools/mgrc.cpp:227).
 double serial_sumsq(Context& ctx, const void* data, DType dtype, uint64_t n, double s0);
+
+
+// ---- MDR refactor / request / reconstruct (refactor.hpp:81-117) ----------
+// Per-(level, bitplane) precision segments of the multilevel coefficients,
+// each canonical-Huffman coded with its CRC; the greedy planner on the host;
+// progressive reconstruction on the device.
+constexpr int kMdrEmptyExponent = INT32_MIN;  // empty_level_exponent (error_control.hpp:40)
+struct MdrSegment {
+  uint64_t bytes = 0, raw_bits = 0;
+  uint32_t crc = 0;
+};
+struct MdrManifest {  // StoreManifest (refactor.hpp:33-45); dtype is always f64
+  Grid grid;
+  int nlevels = 0;
+  uint32_t planes = 32;
+  std::vector<int> exps;
+  std::vector<uint64_t> counts;
+  double vmin = 0, vmax = 0, vrms = 0;
+  std::vector<std::vector<MdrSegment>> seg;  // [level][plane]
+};
+struct MdrStore {
+  MdrManifest m;
+  std::vector<std::vector<std::vector<uint8_t>>> payload;  // [level][plane]
+};
+struct MdrRequest {
+  std::vector<std::pair<uint32_t, uint32_t>> segs;  // (level, plane) in fetch order
+  uint64_t bytes = 0;
+  double predicted = 0;
+  bool satisfiable = true;
+};
+MdrStore mdr_refactor(Context& ctx, const double* u, const Grid& grid, uint32_t planes);
+double mdr_estimator(const MdrManifest& m, const std::vector<uint32_t>& fetched, Norm norm, double s);
+MdrRequest mdr_request(const MdrManifest& m, double tol_abs, Norm norm, double s, std::vector<uint32_t> fetched);
+class MdrSession;  // device-resident RetrievalState (refactor.hpp:56-62)
+MdrSession* mdr_session_new(const MdrManifest& m);
+void mdr_session_free(MdrSession* s);
+const std::vector<uint32_t>& mdr_session_fetched(const MdrSession* s);
+// Applies the segments (payloads given in request order), then writes the
+// refined field (host or device pointer); returns the accrued estimator.
+double mdr_reconstruct(Context& ctx, MdrSession& ss, const std::vector<std::pair<uint32_t, uint32_t>>& segs,
+                       const std::vector<const uint8_t*>& payloads, const std::vector<uint64_t>& lens, Norm norm,
+                       double s, double* out);
 
 }  // namespace mgrc_gpu
