@@ -91,6 +91,149 @@ __global__ void __launch_bounds__(kTfmThreads) k_inverse_level(GridDev g, BoxDev
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Row forms over the full grid (the finest-level box, where almost all the
+// bytes are): a warp per row, the lanes across the last axis (coalesced).
+// The row's outer indices, their levels and the outer corner rows with their
+// weight products are decoded once per row; per column the node's tag is
+// max(outer tag, level of the column) and the stencil follows from it:
+//   column level > outer tag: only the last axis is new (in-row neighbours);
+//   column level = outer tag: the outer new axes and the last one (corner
+//                             rows x left/right columns, last-axis bit highest);
+//   column level < outer tag: the outer new axes only (corner rows, same column).
+// Corner order, weight products and accumulation are transform.cpp:111-128's.
+template <int D>
+struct RowCorners {
+  static constexpr int NS = 1 << (D - 1);
+  uint64_t own, off[NS];
+  double w[NS];
+  int nsub, t_o;
+};
+
+template <int D>
+__device__ __forceinline__ void row_corners(const GridDev& g, uint64_t row, int lvl, RowCorners<D>& m) {
+  uint32_t o[4] = {0, 0, 0, 0};
+  uint64_t q = row;
+#pragma unroll
+  for (int a = D - 2; a >= 0; --a) {
+    const uint64_t qq = q / g.shape[a];
+    o[a] = static_cast<uint32_t>(q - qq * g.shape[a]);
+    q = qq;
+  }
+  int t_o = 0;
+  uint32_t F = 0;
+  uint64_t own = 0;
+  int lv[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < D - 1; ++a) {
+    lv[a] = __ldg(g.ax[a].lvl + o[a]);
+    t_o = max(t_o, lv[a]);
+    own += static_cast<uint64_t>(o[a]) * g.stride[a];
+  }
+  // lvl < 0: the forward pass (each node at its own tag); else the inverse pass of level lvl
+  const int tl = lvl < 0 ? t_o : lvl;
+#pragma unroll
+  for (int a = 0; a < D - 1; ++a)
+    if (lv[a] == tl && tl > 0) F |= 1u << a;
+  m.own = own;
+  m.t_o = t_o;
+  m.nsub = 1 << __popc(F);
+#pragma unroll
+  for (int j = 0; j < RowCorners<D>::NS; ++j) {
+    m.off[j] = 0;
+    m.w[j] = 0.0;
+    if (j >= m.nsub) continue;
+    double w = 1.0;
+    uint64_t uo = 0;
+    int b = 0;
+#pragma unroll
+    for (int a = 0; a < D - 1; ++a) {
+      if ((F >> a) & 1u) {
+        const bool right = (j >> b) & 1;
+        ++b;
+        w = __dmul_rn(w, right ? __ldg(g.ax[a].wr + o[a]) : __ldg(g.ax[a].wl + o[a]));
+        uo += static_cast<uint64_t>(right ? __ldg(g.ax[a].right + o[a]) : __ldg(g.ax[a].left + o[a])) * g.stride[a];
+      } else {
+        uo += static_cast<uint64_t>(o[a]) * g.stride[a];
+      }
+    }
+    m.off[j] = uo;
+    m.w[j] = w;
+  }
+}
+
+// I(v) of node (row m, column k) at level `tag`; `lastfresh`: the column is new at `tag`.
+template <int D, class Load>
+__device__ __forceinline__ double row_interp(const GridDev& g, const RowCorners<D>& m, uint32_t k, bool lastfresh,
+                                             bool outer, Load ld) {
+  const AxisTab& t = g.ax[D - 1];
+  double acc = 0.0;
+  if (lastfresh) {
+    const uint32_t kl = __ldg(t.left + k), kr = __ldg(t.right + k);
+    const double wl = __ldg(t.wl + k), wr = __ldg(t.wr + k);
+    if (!outer) return __dadd_rn(__dmul_rn(wl, ld(m.own + kl)), __dmul_rn(wr, ld(m.own + kr)));
+#pragma unroll
+    for (int j = 0; j < RowCorners<D>::NS; ++j)
+      if (j < m.nsub) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wl), ld(m.off[j] + kl)));
+#pragma unroll
+    for (int j = 0; j < RowCorners<D>::NS; ++j)
+      if (j < m.nsub) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(m.w[j], wr), ld(m.off[j] + kr)));
+  } else {
+#pragma unroll
+    for (int j = 0; j < RowCorners<D>::NS; ++j)
+      if (j < m.nsub) acc = __dadd_rn(acc, __dmul_rn(m.w[j], ld(m.off[j] + k)));
+  }
+  return acc;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTfmThreads) k_forward_rows(GridDev g, const double* __restrict__ u,
+                                                               double* __restrict__ c) {
+  const uint32_t n_last = g.shape[D - 1];
+  const uint64_t nrows = g.N / n_last;
+  const int lane = threadIdx.x & 31;
+  auto ld = [u](uint64_t off) { return __ldg(u + off); };
+  for (uint64_t row = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; row < nrows;
+       row += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    RowCorners<D> m;
+    row_corners<D>(g, row, -1, m);
+    for (uint32_t k = lane; k < n_last; k += 32) {
+      const int lk = __ldg(g.ax[D - 1].lvl + k);
+      const uint64_t n = m.own + k;
+      const double v = __ldg(u + n);
+      double out = v;
+      if (lk > m.t_o) {  // only the last axis is new (tag = lk)
+        out = __dsub_rn(v, row_interp<D>(g, m, k, true, false, ld));
+      } else if (m.t_o > 0) {  // tag = t_o: the outer new axes, and the last if new at t_o
+        out = __dsub_rn(v, row_interp<D>(g, m, k, lk == m.t_o, true, ld));
+      }
+      c[n] = out;
+    }
+  }
+}
+
+// The inverse pass of the finest level L over the full grid: nodes tagged L get c + I(v).
+template <int D>
+__global__ void __launch_bounds__(kTfmThreads) k_inverse_rows(GridDev g, const double* __restrict__ c, double* v) {
+  const uint32_t n_last = g.shape[D - 1];
+  const uint64_t nrows = g.N / n_last;
+  const int lane = threadIdx.x & 31;
+  const int L = g.L;
+  auto ld = [v](uint64_t off) { return v[off]; };
+  for (uint64_t row = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; row < nrows;
+       row += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    RowCorners<D> m;
+    row_corners<D>(g, row, L, m);
+    for (uint32_t k = lane; k < n_last; k += 32) {
+      const int lk = __ldg(g.ax[D - 1].lvl + k);
+      if (m.t_o < L && lk < L) continue;  // tag < L: written by a coarser pass
+      const uint64_t n = m.own + k;
+      v[n] = __dadd_rn(__ldg(c + n), row_interp<D>(g, m, k, lk == L, m.t_o == L, ld));
+    }
+  }
+}
+
 struct QuantOut {
   unsigned long long overflow, outliers;
 };
@@ -233,8 +376,18 @@ struct Fwd {
   template <int D>
   struct L {
     static void run(cudaStream_t s, const GridDev& g, const BoxDev& b, const double* u, double* c) {
-      k_forward<D><<<blocks_for(b.count), kTfmThreads, 0, s>>>(g, b, u, c);
-      check_launch("k_forward");
+      (void)b;
+      k_forward_rows<D><<<blocks_for(g.N / g.shape[D - 1] * 32), kTfmThreads, 0, s>>>(g, u, c);
+      check_launch("k_forward_rows");
+    }
+  };
+};
+struct InvRows {
+  template <int D>
+  struct L {
+    static void run(cudaStream_t s, const GridDev& g, const double* c, double* v) {
+      k_inverse_rows<D><<<blocks_for(g.N / g.shape[D - 1] * 32), kTfmThreads, 0, s>>>(g, c, v);
+      check_launch("k_inverse_rows");
     }
   };
 };
@@ -475,7 +628,9 @@ void inverse_transform(Context& ctx, const double* c, double* u, const Grid& gri
   double* du = staged<double>(ctx, ctx.v, u, N, false);
   if (du == dc) raise(Errc::invalid_argument, "inverse_transform: output aliases the coefficients");
   prof.begin("inverse", static_cast<double>(N) * 16);
-  for (int l = 0; l <= dh.h.L; ++l) by_dim<Inv::L>(grid.d, s, dh.g, dh.boxes[l], l, dc, du);
+  for (int l = 0; l < dh.h.L; ++l) by_dim<Inv::L>(grid.d, s, dh.g, dh.boxes[l], l, dc, du);
+  if (dh.h.L >= 1) by_dim<InvRows::L>(grid.d, s, dh.g, dc, du);  // the finest level: rows of the full grid
+  else by_dim<Inv::L>(grid.d, s, dh.g, dh.boxes[0], 0, dc, du);
   prof.end();
   download(ctx, u, du, N * 8);
   CK(cudaStreamSynchronize(s));
