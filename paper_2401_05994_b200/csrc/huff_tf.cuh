@@ -98,22 +98,26 @@ __device__ __forceinline__ unsigned long long tfd_map_impl(const uint32_t* sm, c
   unsigned long long r = 0;
   for (int e = 0; e < ne; ++e) r |= static_cast<unsigned long long>(e + 1) << (4 * e);
   unsigned long long parent = kNibId;  // union-find parent of each cursor id
+  uint32_t occ = (1u << ne) - 1u;  // bit i: a cursor at base + i (mirror of r's nonzero nibbles)
   BitReader br;
   br.init(sm, base);
-  while ((r & ~15ull) && base < end) {
+  while ((occ & (occ - 1u)) && base < end) {
     const uint32_t id = static_cast<uint32_t>(r) & 15u;
     br.refill();
     const uint32_t l = lut_len(lut[br.peek(maxlen)]);
     r &= ~15ull;
+    occ &= ~1u;
     if (NEAR_END && base + l > tl) {
       // the stream ends inside this codeword: the cursor dies
+    } else if ((occ >> l) & 1u) {  // two parses met: merge
+      parent = nib_set(parent, id - 1u, (static_cast<uint32_t>(r >> (4u * l)) & 15u) - 1u);
     } else {
-      const uint32_t there = static_cast<uint32_t>(r >> (4u * l)) & 15u;
-      if (there) parent = nib_set(parent, id - 1u, there - 1u);  // two parses met: merge
-      else r |= static_cast<unsigned long long>(id) << (4u * l);
+      r |= static_cast<unsigned long long>(id) << (4u * l);
+      occ |= 1u << l;
     }
-    if (!r) break;
-    const uint32_t sh = static_cast<uint32_t>(__ffsll(static_cast<long long>(r)) - 1) >> 2;
+    if (!occ) break;
+    const uint32_t sh = static_cast<uint32_t>(__ffs(static_cast<int>(occ)) - 1);
+    occ >>= sh;
     r >>= 4u * sh;
     base += sh;
     br.consume(sh);
