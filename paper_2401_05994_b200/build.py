@@ -35,8 +35,14 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+FLAGS_STAMP = PKG / "build" / "extra_flags.txt"  # the MGRC_NVCC_EXTRA the library was built with
+
+
 def needs_build() -> bool:
     if not LIB.exists():
+        return True
+    extra = os.environ.get("MGRC_NVCC_EXTRA", "")
+    if (FLAGS_STAMP.read_text() if FLAGS_STAMP.exists() else "") != extra:
         return True
     t = LIB.stat().st_mtime
     deps = ([CSRC / s for s in SOURCES] + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.hpp")) +
@@ -74,6 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
     tmp.replace(LIB)
+    FLAGS_STAMP.write_text(" ".join(extra))
     return LIB
 
 

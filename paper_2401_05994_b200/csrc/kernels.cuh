@@ -317,6 +317,16 @@ __device__ __forceinline__ void hist_varint(uint32_t* sh, uint64_t z, uint32_t& 
   }
 }
 
+// continuation bytes of one code (z = code >> 7): rare, straight into the block histogram
+__device__ __forceinline__ void hist_tail(uint32_t* sh, uint64_t z) {
+  for (;;) {
+    const uint32_t b = z >= 0x80 ? static_cast<uint32_t>((z & 0x7F) | 0x80) : static_cast<uint32_t>(z);
+    atomicAdd(&sh[b], 1u);
+    if (z < 0x80) return;
+    z >>= 7;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Inverse transform, coarse → fine (transform.cpp:155-159).  Level l ≥ 1
 // touches only nodes tagged l and reads only nodes of lower tag, which are

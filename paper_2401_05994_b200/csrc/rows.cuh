@@ -407,6 +407,30 @@ __device__ __forceinline__ bool quantize_fast(double c, double delta, double inv
   return true;
 }
 
+// Per-lane first-byte counters of the code histogram: one byte per (symbol,
+// lane), w[b][l/4] byte l%4, so a lane increments its own byte with a plain
+// load/add/store (no atomics, at most 4-way bank conflicts: lanes of one
+// word never conflict).  A lane adds at most 2 per unit (one per column), so
+// the warp folds the counters into the block histogram every kUnits units.
+struct LaneHist {
+  static constexpr uint32_t kUnits = 127;
+  uint32_t w[256][8];
+  __device__ __forceinline__ void flush(uint32_t* sh, int lane) {
+    __syncwarp();
+#pragma unroll 1
+    for (int b = lane; b < 256; b += 32) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c = __dp4a(w[b][j], 0x01010101u, c);
+        w[b][j] = 0u;
+      }
+      if (c) atomicAdd(&sh[b], c);
+    }
+    __syncwarp();
+  }
+};
+
 // Fused finest-level pass, column-pair form.  Each lane owns columns (k, k+1)
 // with k even: at the finest level an even column is never fresh and an odd
 // one is fresh unless it is the last index, whose bracketing neighbours are
@@ -430,9 +454,9 @@ struct PairCtx {
   double dL, inv_L;
   Chk chk;
   uint32_t* sh;
-  uint32_t hsym, hcnt;
+  uint8_t* hl;         // this lane's column of the warp's first-byte counters: hl[32 * b] (LaneHist)
   unsigned long long ovf;
-  unsigned wide;
+  unsigned wide;       // high halves of the codes OR-ed (u32 streams: any nonzero -> the wide fallback)
   double red;
 
   __device__ __forceinline__ uint64_t quant(double c, double& r) {
@@ -445,9 +469,14 @@ struct PairCtx {
     return zigzag(q);
   }
   __device__ __forceinline__ void emit(uint64_t n, uint64_t z, double e, double src) {
-    if (sizeof(Z) == 4 && z > 0xFFFFFFFFull) wide = 1;
+    if constexpr (sizeof(Z) == 4) wide |= static_cast<unsigned>(z >> 32);
     zz[n] = static_cast<Z>(z);
-    hist_varint(sh, z, hsym, hcnt);
+    if (z < 0x80) {
+      ++hl[32u * static_cast<uint32_t>(z)];
+    } else {  // first byte into the lane counters, continuation bytes straight into the block histogram
+      ++hl[32u * static_cast<uint32_t>((z & 0x7F) | 0x80)];
+      hist_tail(sh, z >> 7);
+    }
     chk(n, e, src, red);
   }
   __device__ __forceinline__ double ld(uint64_t i) const { return static_cast<double>(__ldg(u + i)); }
@@ -658,9 +687,13 @@ __global__ void __launch_bounds__(kFineThreads, MGRC_FINE_MINB) k_fine_warp(Grid
                                                              Chk chk, unsigned long long* __restrict__ red_out,
                                                              unsigned long long* queue) {
   __shared__ uint32_t sh[256];
+  __shared__ LaneHist lh[kFineThreads / 32];
   for (int t = threadIdx.x; t < 256; t += blockDim.x) sh[t] = 0;
+  for (int t = threadIdx.x; t < kFineThreads / 32 * 256 * 8; t += blockDim.x) (&lh[0].w[0][0])[t] = 0u;
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  LaneHist& myh = lh[threadIdx.x >> 5];
+  uint32_t units = 0;
   PairCtx<T, Z, Chk> P;
   P.g = &g;
   P.u = u;
@@ -673,7 +706,7 @@ __global__ void __launch_bounds__(kFineThreads, MGRC_FINE_MINB) k_fine_warp(Grid
   P.inv_L = inv_L;
   P.chk = chk;
   P.sh = sh;
-  P.hsym = P.hcnt = 0;
+  P.hl = reinterpret_cast<uint8_t*>(&myh.w[0][0]) + lane;
   P.ovf = 0;
   P.wide = 0;
   P.red = 0.0;
@@ -711,11 +744,15 @@ __global__ void __launch_bounds__(kFineThreads, MGRC_FINE_MINB) k_fine_warp(Grid
       else if (D >= 4 && mm.nsub == 8) P.template unit<(D >= 4 ? 8 : 2)>(mm, k0, kk, Kt, lane);
       else if (D >= 3 && mm.nsub == 4) P.template unit<(D >= 3 ? 4 : 2)>(mm, k0, kk, Kt, lane);
       else P.template unit<2>(mm, k0, kk, Kt, lane);
+      if (++units == LaneHist::kUnits) {  // ≤ 2 counts per lane per unit: flush before a byte counter wraps
+        myh.flush(sh, lane);
+        units = 0;
+      }
     }
     if (lane == 0) item = atomicAdd(queue, 1ull);
     item = __shfl_sync(0xffffffffu, item, 0);
   }
-  hist_flush(sh, P.hsym, P.hcnt);
+  myh.flush(sh, lane);
   if (P.ovf) atomicAdd(&flags->overflow, P.ovf);
   if (P.wide) atomicOr(&flags->wide, 1u);
   if (red_out) {

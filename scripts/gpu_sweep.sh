@@ -1,14 +1,23 @@
 #!/bin/bash
-# Build variants (MGRC_NVCC_EXTRA flag sets separated by ';' in $VARIANTS), for each: decode parity subset + cfg2 phases
+# build-flag sweep of the fused pass (MGRC_NVCC_EXTRA variants), staged on/off, then one ncu capture of the default build
 mkdir -p gpurun_out
-IFS=';' read -ra VS <<< "${VARIANTS}"
-i=0
-for V in "${VS[@]}"; do
-  i=$((i+1))
-  MGRC_NVCC_EXTRA="$V" python paper_2401_05994_b200/build.py --force > /dev/null 2>&1 || { echo "build [$V] failed"; continue; }
-  timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "${PYK:-container_parity or slab}" > gpurun_out/sw_${i}_pytest.log 2>&1; tail -1 gpurun_out/sw_${i}_pytest.log
-  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e ${BENCH_ARGS} > gpurun_out/sw_$i.json 2>/dev/null
-  python -c "
-import json; d=json.load(open('gpurun_out/sw_$i.json')); p=d['phases_ms_per_step']
-print('[$V]', round(d['value'],1), round(d['compress_gbs'],1), round(d['decompress_gbs'],1), {k: v['ms'] for k, v in p.items()})"
+TAG=${1:-sw}
+VARIANTS=${VARIANTS:-"-DMGRC_FINE_MINB=5 -DMGRC_FINE_MINB=6 -DMGRC_FINE_MINB=8"}
+for v in $VARIANTS; do
+  MGRC_NVCC_EXTRA="$v" timeout 900 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/${TAG}_build.log 2>&1 || { echo "build $v failed"; tail -5 gpurun_out/${TAG}_build.log; continue; }
+  for st in 1 0; do
+    MGRC_FINE_STAGED=$st timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_b.json 2>> gpurun_out/${TAG}_bench.err
+    V="$v" ST=$st TAG=$TAG python - <<"PY"
+import json,os
+d=json.loads(open(f"gpurun_out/{os.environ['TAG']}_b.json").read().strip().splitlines()[-1])
+p=d["phases_ms_per_step"]
+print(os.environ['V'], "staged", os.environ['ST'], "c", round(d["compress_gbs"],1), "fine", p["fine"]["ms"], "pack", p["pack"]["ms"])
+PY
+  done
 done
+if [ -n "$NCU_K" ]; then
+  timeout 900 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/${TAG}_build.log 2>&1
+  MGRC_FINE_STAGED=${NCU_STAGED:-0} timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${NCU_K} -s 3 -c 1 -o gpurun_out/${TAG}_ncu \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu.log 2>&1
+  tail -2 gpurun_out/${TAG}_ncu.log
+fi
