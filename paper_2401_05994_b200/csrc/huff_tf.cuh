@@ -91,6 +91,45 @@ __device__ __forceinline__ void tfd_stage(const uint32_t* __restrict__ w, uint64
 // length l <= 15 lands on nibble l — occupied means two parses met (merge:
 // union-find parent of the cursor id) — and the map is rebased to the next
 // smallest cursor by one shift.  Everything stays in registers.
+//
+// Parses that have not met after kTfdMergeBits are usually out of phase over
+// a periodic stretch and will not meet soon: the survivors then walk on one by
+// one with the plain two-codewords-per-refill loop (parses that would still
+// meet simply reach the same exit).
+#ifndef MGRC_TFD_MERGE_BITS
+#define MGRC_TFD_MERGE_BITS 256
+#endif
+constexpr uint32_t kTfdMergeBits = MGRC_TFD_MERGE_BITS;
+
+// walk one parse from p to its exit (>= end); ~0u: it ran into the stream end
+template <bool NEAR_END, class LT>
+__device__ __forceinline__ uint32_t tfd_walk(const uint32_t* sm, const LT& lut, int maxlen, uint32_t p, uint32_t end,
+                                             uint32_t tl) {
+  BitReader br;
+  br.init(sm, p);
+  if (!NEAR_END) {  // no codeword can run past the stream end: two per refill
+    while (p < end) {
+      br.refill();
+      uint32_t l = lut_len(lut[br.peek(maxlen)]);
+      p += l;
+      br.consume(l);
+      if (p >= end) break;
+      l = lut_len(lut[br.peek(maxlen)]);
+      p += l;
+      br.consume(l);
+    }
+    return p;
+  }
+  while (p < end) {
+    br.refill();
+    const uint32_t l = lut_len(lut[br.peek(maxlen)]);
+    if (p + l > tl) return ~0u;
+    p += l;
+    br.consume(l);
+  }
+  return p;
+}
+
 template <bool NEAR_END, class LT>
 __device__ __forceinline__ unsigned long long tfd_map_impl(const uint32_t* sm, const LT& lut, int maxlen, int ne,
                                                            uint32_t S, uint32_t end, uint32_t tl) {
@@ -101,7 +140,8 @@ __device__ __forceinline__ unsigned long long tfd_map_impl(const uint32_t* sm, c
   uint32_t occ = (1u << ne) - 1u;  // bit i: a cursor at base + i (mirror of r's nonzero nibbles)
   BitReader br;
   br.init(sm, base);
-  while ((occ & (occ - 1u)) && base < end) {
+  const uint32_t mend = min(end, S + kTfdMergeBits);
+  while ((occ & (occ - 1u)) && base < mend) {
     const uint32_t id = static_cast<uint32_t>(r) & 15u;
     br.refill();
     const uint32_t l = lut_len(lut[br.peek(maxlen)]);
@@ -122,23 +162,14 @@ __device__ __forceinline__ unsigned long long tfd_map_impl(const uint32_t* sm, c
     base += sh;
     br.consume(sh);
   }
-  if (r && !(r & ~15ull) && base < end) {  // one parse left: walk it to the exit
-    uint32_t p = base;
-    while (p < end) {
-      br.refill();
-      const uint32_t l = lut_len(lut[br.peek(maxlen)]);
-      if (NEAR_END && p + l > tl) break;
-      p += l;
-      br.consume(l);
-    }
-    if (p < end) r = 0;  // died at the stream end
-    else base = p;
-  }
-  // exits of the live cursors, then every entry through its union-find root
+  // every live cursor walks on alone to its exit, then every entry maps through its union-find root
   unsigned long long exit_of = ~0ull;  // id -> exit offset (15: dead)
   for (uint32_t i = 0; r; ++i, r >>= 4) {
     const uint32_t id = static_cast<uint32_t>(r) & 15u;
-    if (id) exit_of = nib_set(exit_of, id - 1u, min(base + i - end, 14u));
+    if (!id) continue;
+    uint32_t p = base + i;
+    if (p < end) p = tfd_walk<NEAR_END>(sm, lut, maxlen, p, end, tl);
+    if (p != ~0u) exit_of = nib_set(exit_of, id - 1u, min(p - end, 14u));
   }
   unsigned long long f = ~0ull;
   for (int e = 0; e < ne; ++e) {
