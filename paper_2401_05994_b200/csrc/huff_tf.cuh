@@ -130,9 +130,15 @@ __device__ __forceinline__ uint32_t tfd_walk(const uint32_t* sm, const LT& lut, 
   return p;
 }
 
+// The merging part: returns the live cursors (nibble map r over [base, base +
+// 16)) and the union-find parents; the survivors are walked by the warp.
+struct TfdCursors {
+  unsigned long long r, parent;
+  uint32_t base;
+};
 template <bool NEAR_END, class LT>
-__device__ __forceinline__ unsigned long long tfd_map_impl(const uint32_t* sm, const LT& lut, int maxlen, int ne,
-                                                           uint32_t S, uint32_t end, uint32_t tl) {
+__device__ __forceinline__ TfdCursors tfd_merge(const uint32_t* sm, const LT& lut, int maxlen, int ne, uint32_t S,
+                                                uint32_t end, uint32_t tl) {
   uint32_t base = S;
   unsigned long long r = 0;
   for (int e = 0; e < ne; ++e) r |= static_cast<unsigned long long>(e + 1) << (4 * e);
@@ -162,29 +168,96 @@ __device__ __forceinline__ unsigned long long tfd_map_impl(const uint32_t* sm, c
     base += sh;
     br.consume(sh);
   }
-  // every live cursor walks on alone to its exit, then every entry maps through its union-find root
+  return TfdCursors{r, parent, base};
+}
+
+// Survivor walks of a warp, balanced across its lanes: every lane queues its
+// live cursors that are still before their end (position, end, lane, id) in
+// shared memory, the 32 lanes walk the queue together, and each lane reads its
+// cursors' exits back (one byte per (lane, id)).  A queue overflow is walked
+// by its owner.
+constexpr uint32_t kTfdJobs = 128;  // queued walks per warp
+struct TfdWarpQueue {
+  unsigned long long job[kTfdJobs];
+  uint8_t exit[32][16];
+};
+__device__ __forceinline__ unsigned long long tfd_job(uint32_t p, uint32_t end, uint32_t lane, uint32_t id, bool near) {
+  return p | (static_cast<unsigned long long>(end) << 16) | (static_cast<unsigned long long>(lane) << 32) |
+         (static_cast<unsigned long long>(id) << 37) | (static_cast<unsigned long long>(near) << 41);
+}
+template <class LT>
+__device__ __forceinline__ uint32_t tfd_walk_exit(const uint32_t* sm, const LT& lut, int maxlen, uint32_t p,
+                                                  uint32_t end, uint32_t tl, bool near) {
+  const uint32_t x = near ? tfd_walk<true>(sm, lut, maxlen, p, end, tl) : tfd_walk<false>(sm, lut, maxlen, p, end, tl);
+  return x == ~0u ? kDeadEx : min(x - end, 14u);
+}
+
+// Exit map of one subsequence [S, end) of every lane (live: it has a map to
+// compute); warp-synchronous.
+template <class LT>
+__device__ __forceinline__ unsigned long long tfd_map_warp(const uint32_t* sm, const LT& lut, int maxlen, int ne,
+                                                           uint32_t S, uint32_t end, uint32_t tl, bool live,
+                                                           TfdWarpQueue& wq, int lane) {
+  TfdCursors cs{0ull, kNibId, S};
+  if (live) cs = end + 32 >= tl ? tfd_merge<true>(sm, lut, maxlen, ne, S, end, tl)
+                                : tfd_merge<false>(sm, lut, maxlen, ne, S, end, tl);
+  const bool near = end + 32 >= tl;
   unsigned long long exit_of = ~0ull;  // id -> exit offset (15: dead)
-  for (uint32_t i = 0; r; ++i, r >>= 4) {
-    const uint32_t id = static_cast<uint32_t>(r) & 15u;
-    if (!id) continue;
-    uint32_t p = base + i;
-    if (p < end) p = tfd_walk<NEAR_END>(sm, lut, maxlen, p, end, tl);
-    if (p != ~0u) exit_of = nib_set(exit_of, id - 1u, min(p - end, 14u));
+  uint32_t nj = 0;  // cursors still before the end
+  {
+    uint32_t i = 0;
+    for (unsigned long long r = cs.r; r; r >>= 4, ++i) nj += (static_cast<uint32_t>(r) & 15u) != 0 && cs.base + i < end;
   }
+  uint32_t off = nj;  // inclusive warp scan -> exclusive offset
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t h = __shfl_up_sync(0xffffffffu, off, d);
+    if (lane >= d) off += h;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
+  off -= nj;
+  {
+    uint32_t q = off, i = 0;
+    for (unsigned long long r = cs.r; r; r >>= 4, ++i) {
+      const uint32_t id = static_cast<uint32_t>(r) & 15u;
+      if (!id) continue;
+      const uint32_t p = cs.base + i;
+      if (p >= end) {
+        exit_of = nib_set(exit_of, id - 1u, min(p - end, 14u));
+        continue;
+      }
+      if (q < kTfdJobs) wq.job[q] = tfd_job(p, end, static_cast<uint32_t>(lane), id - 1u, near);
+      else exit_of = nib_set(exit_of, id - 1u, tfd_walk_exit(sm, lut, maxlen, p, end, tl, near));
+      ++q;
+    }
+  }
+  __syncwarp();
+  const uint32_t nq = min(total, kTfdJobs);
+  for (uint32_t q = lane; q < nq; q += 32) {
+    const unsigned long long jb = wq.job[q];
+    const uint32_t p = static_cast<uint32_t>(jb) & 0xFFFFu, e = static_cast<uint32_t>(jb >> 16) & 0xFFFFu;
+    wq.exit[(jb >> 32) & 31u][(jb >> 37) & 15u] =
+        static_cast<uint8_t>(tfd_walk_exit(sm, lut, maxlen, p, e, tl, (jb >> 41) & 1u));
+  }
+  __syncwarp();
+  {
+    uint32_t q = off, i = 0;
+    for (unsigned long long r = cs.r; r; r >>= 4, ++i) {
+      const uint32_t id = static_cast<uint32_t>(r) & 15u;
+      if (!id) continue;
+      if (cs.base + i >= end) continue;
+      if (q < kTfdJobs) exit_of = nib_set(exit_of, id - 1u, wq.exit[lane][id - 1u]);
+      ++q;
+    }
+  }
+  __syncwarp();  // the queue is reused by the next call
   unsigned long long f = ~0ull;
   for (int e = 0; e < ne; ++e) {
     uint32_t q = e;
-    for (uint32_t pq = nib(parent, q); pq != q; pq = nib(parent, q)) q = pq;
+    for (uint32_t pq = nib(cs.parent, q); pq != q; pq = nib(cs.parent, q)) q = pq;
     f = nib_set(f, e, nib(exit_of, q));
   }
   return f;
-}
-
-template <class LT>
-__device__ __forceinline__ unsigned long long tfd_map(const uint32_t* sm, const LT& lut, int maxlen, int ne,
-                                                      uint32_t S, uint32_t end, uint32_t tl) {
-  return end + 32 >= tl ? tfd_map_impl<true>(sm, lut, maxlen, ne, S, end, tl)
-                        : tfd_map_impl<false>(sm, lut, maxlen, ne, S, end, tl);
 }
 
 // K1: exit maps, scanned within the tile: gmap[j] = map of subsequences
@@ -194,6 +267,7 @@ static __global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t*
                                                           const uint16_t* __restrict__ lut_g, int maxlen, int ne,
                                                           uint64_t nseq, unsigned long long* __restrict__ gmap) {
   extern __shared__ uint32_t dyn[];
+  __shared__ TfdWarpQueue wqs[kTfdThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + (kTfdThreads / 32) * kTfdWarpSmem);
   uint32_t* sm = dyn + wid * kTfdWarpSmem;
@@ -210,7 +284,8 @@ static __global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t*
   const uint32_t S = static_cast<uint32_t>(lane) * kSeqBits;
   const uint32_t end = min(S + static_cast<uint32_t>(kSeqBits), tl);
   // the last subsequence ends the stream (all dead); identity past it
-  unsigned long long g = j < nseq ? (j + 1 < nseq ? tfd_map(sm, lut, maxlen, ne, S, end, tl) : ~0ull) : kNibId;
+  const unsigned long long m = tfd_map_warp(sm, lut, maxlen, ne, S, end, tl, j + 1 < nseq, wqs[wid], lane);
+  unsigned long long g = j < nseq ? (j + 1 < nseq ? m : ~0ull) : kNibId;
 #pragma unroll
   for (int d = 1; d < kTfdTile; d <<= 1) {
     const unsigned long long h = __shfl_up_sync(0xffffffffu, g, d);
