@@ -97,7 +97,7 @@ __device__ __forceinline__ void tfd_stage(const uint32_t* __restrict__ w, uint64
 // one with the plain two-codewords-per-refill loop (parses that would still
 // meet simply reach the same exit).
 #ifndef MGRC_TFD_MERGE_BITS
-#define MGRC_TFD_MERGE_BITS 256
+#define MGRC_TFD_MERGE_BITS 64
 #endif
 constexpr uint32_t kTfdMergeBits = MGRC_TFD_MERGE_BITS;
 
@@ -176,7 +176,10 @@ __device__ __forceinline__ TfdCursors tfd_merge(const uint32_t* sm, const LT& lu
 // shared memory, the 32 lanes walk the queue together, and each lane reads its
 // cursors' exits back (one byte per (lane, id)).  A queue overflow is walked
 // by its owner.
-constexpr uint32_t kTfdJobs = 128;  // queued walks per warp
+#ifndef MGRC_TFD_JOBS
+#define MGRC_TFD_JOBS 128
+#endif
+constexpr uint32_t kTfdJobs = MGRC_TFD_JOBS;  // queued walks per warp
 struct TfdWarpQueue {
   unsigned long long job[kTfdJobs];
   uint8_t exit[32][16];
