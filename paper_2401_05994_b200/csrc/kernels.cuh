@@ -554,7 +554,6 @@ static __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __rest
     len[c] = len_g[c];
   }
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-  for (uint32_t w = threadIdx.x; w <= cap_words; w += blockDim.x) words[w] = 0;
   __syncthreads();
   const uint64_t t = s_tile;
   const uint64_t base = t * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
@@ -586,13 +585,21 @@ static __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __rest
     for (int w = 1; w < kPackThreads / 32; ++w) wsum[w] += wsum[w - 1];
   __syncthreads();
   const uint32_t tile_total = wsum[kPackThreads / 32 - 1];
+  const uint32_t p0 = (warp ? wsum[warp - 1] : 0) + incl - mine;
+  // only the words two threads share need zeroing (the edge words of every range, ORed into), and the
+  // word past the last one (read by the shifted store)
+  if (mine) {
+    words[p0 >> 5] = 0u;
+    words[(p0 + mine - 1) >> 5] = 0u;
+  }
+  if (threadIdx.x == 0 && tile_total) words[((tile_total - 1) >> 5) + 1] = 0u;
+  __syncthreads();
   // warp 0 looks back for the tile's global start bit while the other warps
   // already pack at tile-relative positions
   if (warp == 0) {
     const unsigned long long pfx = lookback(status, t, tile_total);
     if (lane == 0) s_prefix = pfx;
   }
-  const uint32_t p0 = (warp ? wsum[warp - 1] : 0) + incl - mine;
   if (mine) {
     const uint32_t p1 = p0 + mine;
     const uint32_t w_first = p0 >> 5, w_last = (p1 - 1) >> 5;
