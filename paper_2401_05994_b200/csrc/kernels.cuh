@@ -520,7 +520,8 @@ constexpr int kPackPerThread = MGRC_PACK_PER;  // a multiple of 4
 constexpr int kPackTile = kPackThreads * kPackPerThread;  // values per tile
 constexpr int kPackMaxWords = kPackTile * 150 / 32 + 2;   // ≤ 10 bytes × 15 bits per value
 
-__device__ __forceinline__ uint32_t varint_bits(uint64_t z, const uint8_t* len) {
+template <typename V>
+__device__ __forceinline__ uint32_t varint_bits(V z, const uint8_t* len) {
   uint32_t b = 0;
   for (;;) {
     if (z < 0x80) return b + len[z];
@@ -544,29 +545,34 @@ static __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __rest
                                                           uint32_t* __restrict__ edge_last,
                                                           uint32_t* __restrict__ out, uint32_t cap_words) {
   extern __shared__ uint32_t words[];  // cap_words + 1: the tile's stream, packed from tile-relative bit 0
-  __shared__ uint32_t code[256];
+  __shared__ uint32_t cl[256];  // code << 4 | length: one lookup per byte
   __shared__ uint8_t len[256];
   __shared__ uint32_t wsum[kPackThreads / 32];
   __shared__ unsigned long long s_prefix;
   __shared__ uint32_t s_tile;
   for (int c = threadIdx.x; c < 256; c += blockDim.x) {
-    code[c] = code_g[c];
+    cl[c] = code_g[c] << 4 | len_g[c];
     len[c] = len_g[c];
   }
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint64_t t = s_tile;
   const uint64_t base = t * static_cast<uint64_t>(kPackTile) + threadIdx.x * kPackPerThread;
-  uint64_t z[kPackPerThread];
-  if (sizeof(Z) == 4 && base + kPackPerThread <= n) {  // 16-byte loads
+  Z z[kPackPerThread];
+  if constexpr (sizeof(Z) == 4) {
+    if (base + kPackPerThread <= n) {  // 16-byte loads
 #pragma unroll
-    for (int q = 0; q < kPackPerThread / 4; ++q) {
-      const uint4 a = __ldg(reinterpret_cast<const uint4*>(zz + base) + q);
-      z[4 * q] = a.x, z[4 * q + 1] = a.y, z[4 * q + 2] = a.z, z[4 * q + 3] = a.w;
+      for (int q = 0; q < kPackPerThread / 4; ++q) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(zz + base) + q);
+        z[4 * q] = a.x, z[4 * q + 1] = a.y, z[4 * q + 2] = a.z, z[4 * q + 3] = a.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kPackPerThread; ++k) z[k] = base + k < n ? zz[base + k] : Z(0);
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < kPackPerThread; ++k) z[k] = base + k < n ? static_cast<uint64_t>(zz[base + k]) : 0;
+    for (int k = 0; k < kPackPerThread; ++k) z[k] = base + k < n ? zz[base + k] : Z(0);
   }
   uint32_t mine = 0;  // ≤ kPackPerThread values × 150 bits
 #pragma unroll
@@ -614,10 +620,10 @@ static __global__ void __launch_bounds__(kPackThreads) k_pack_lb(const Z* __rest
 #pragma unroll
     for (int k = 0; k < kPackPerThread; ++k) {
       if (base + k >= n) break;
-      uint64_t v = z[k];
+      Z v = z[k];
       for (;;) {
         const uint32_t sym = v >= 0x80 ? static_cast<uint32_t>((v & 0x7F) | 0x80) : static_cast<uint32_t>(v);
-        const uint32_t l = len[sym], c = code[sym];
+        const uint32_t e = cl[sym], l = e & 15u, c = e >> 4;
         acc |= static_cast<uint64_t>(c) << (64 - nacc - l);
         nacc += l;
         if (nacc >= 32) {
