@@ -308,7 +308,7 @@ struct CoarseQuantRows {
                     double inv, const T* u, double* ec, Z* zc, QuantFlags* fl, unsigned long long* queue) {
       const RowTiling rt = row_tiling(gc);
       CK(cudaMemsetAsync(queue, 0, 8, s));
-      k_cq_warp<D, T, Z><<<num_sms() * MGRC_BOX_MINB, kBoxThreads, 0, s>>>(g, gc, rt, W, inv, u, ec, zc, fl, queue);
+      k_cq_warp<D, T, Z><<<num_sms() * box_minb<D>(), kBoxThreads, 0, s>>>(g, gc, rt, W, inv, u, ec, zc, fl, queue);
       check_launch("k_cq_warp");
       k_cq_box<D, T, Z><<<grid_blocks(box2.count, 256), 256, 0, s>>>(g, box2, W, u, ec, zc, fl);
       check_launch("k_cq_box");
@@ -337,7 +337,7 @@ struct FinePairs {
     static void run(cudaStream_t s, const GridDev& g, const RowTiling& rt, const Widths& W, double inv_L, const T* u,
                     Z* zz, unsigned long long* hist, QuantFlags* fl, const double* ec, const Z* zc, const Chk& chk,
                     unsigned long long* red, int blocks) {
-      k_fine_warp<D, T, Z, Chk><<<num_sms() * MGRC_FINE_MINB, kFineThreads, 0, s>>>(g, rt, W, inv_L, u, zz, hist, fl, ec, zc, chk,
+      k_fine_warp<D, T, Z, Chk><<<num_sms() * fine_minb<D, Chk>(), kFineThreads, 0, s>>>(g, rt, W, inv_L, u, zz, hist, fl, ec, zc, chk,
                                                                        red, &fl->queue);
       check_launch("k_fine_warp");
       (void)blocks;
@@ -351,7 +351,7 @@ struct InvWarp {
     static void run(cudaStream_t s, const GridDev& g, double* v, unsigned long long* queue) {
       const RowTiling rt = row_tiling(g);
       CK(cudaMemsetAsync(queue, 0, 8, s));
-      k_inv_warp<D><<<num_sms() * MGRC_BOX_MINB, kBoxThreads, 0, s>>>(g, rt, v, queue);
+      k_inv_warp<D><<<num_sms() * box_minb<D>(), kBoxThreads, 0, s>>>(g, rt, v, queue);
       check_launch("k_inv_warp");
     }
   };
@@ -376,7 +376,7 @@ struct ReconRows {
                     const double* vc, const Out& out, unsigned long long* queue) {
       if (g.L >= 1) {
         CK(cudaMemsetAsync(queue, 0, 8, s));
-        k_recon_warp<D, Z, Out><<<num_sms() * MGRC_RECON_MINB, kReconThreads, 0, s>>>(g, rt, W, zz, vc, out, queue);
+        k_recon_warp<D, Z, Out><<<num_sms() * recon_minb<D>(), kReconThreads, 0, s>>>(g, rt, W, zz, vc, out, queue);
         check_launch("k_recon_warp");
       } else {
         k_recon_rows<D, Z, Out><<<static_cast<unsigned>(row_tiles(rt)), kRowThreads, 0, s>>>(g, rt, W, zz, vc, out);

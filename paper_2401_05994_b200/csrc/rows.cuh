@@ -53,6 +53,16 @@ constexpr int kFineThreads = MGRC_FINE_THREADS;  // k_fine_warp CTA size
 constexpr int kReconThreads = MGRC_RECON_THREADS;  // k_recon_warp CTA size
 constexpr int kBoxThreads = MGRC_BOX_THREADS;
 static_assert(kFineThreads % 32 == 0 && kReconThreads % 32 == 0 && kBoxThreads % 32 == 0, "whole warps");
+// Resident CTAs per SM each variant is compiled (and launched) for: the measured
+// best for the 3-D passes; fewer for the variants carrying more live state
+// (the exact a-posteriori epilogues, 4-D rows with 8 corner rows) so that no
+// variant spills.
+template <int D, class Chk>
+constexpr int fine_minb() { return D >= 4 ? 2 : (Chk::kNeedsE ? 4 : MGRC_FINE_MINB); }
+template <int D>
+constexpr int recon_minb() { return D >= 4 ? 4 : MGRC_RECON_MINB; }
+template <int D>
+constexpr int box_minb() { return D >= 4 ? 4 : MGRC_BOX_MINB; }
 constexpr int kRowTileElems = 4096;  // nodes per CTA (rows × columns)
 constexpr int kRowMaxR = 16;         // rows per CTA
 
@@ -680,7 +690,7 @@ struct UnitLoads {
 };
 
 template <int D, typename T, typename Z, class Chk>
-__global__ void __launch_bounds__(kFineThreads, MGRC_FINE_MINB) k_fine_warp(GridDev g, RowTiling rt, Widths W, double inv_L,
+__global__ void __launch_bounds__(kFineThreads, fine_minb<D, Chk>()) k_fine_warp(GridDev g, RowTiling rt, Widths W, double inv_L,
                                                              const T* __restrict__ u, Z* __restrict__ zz,
                                                              unsigned long long* __restrict__ hist, QuantFlags* flags,
                                                              const double* __restrict__ ec, const Z* __restrict__ zc,
@@ -952,7 +962,7 @@ struct ReconCtx {
 };
 
 template <int D, typename Z, class Out>
-__global__ void __launch_bounds__(kReconThreads, MGRC_RECON_MINB) k_recon_warp(GridDev g, RowTiling rt, Widths W,
+__global__ void __launch_bounds__(kReconThreads, recon_minb<D>()) k_recon_warp(GridDev g, RowTiling rt, Widths W,
                                                               const Z* __restrict__ zz, const double* __restrict__ vc,
                                                               Out out, unsigned long long* queue) {
   const int lane = threadIdx.x & 31;
@@ -1094,7 +1104,7 @@ __device__ __forceinline__ void inv_unit(const GridDev& g, const RowU<NS>& m, do
 }
 
 template <int D>
-__global__ void __launch_bounds__(kBoxThreads, MGRC_BOX_MINB) k_inv_warp(GridDev g, RowTiling rt, double* v,
+__global__ void __launch_bounds__(kBoxThreads, box_minb<D>()) k_inv_warp(GridDev g, RowTiling rt, double* v,
                                                             unsigned long long* queue) {
   const int lane = threadIdx.x & 31;
   const uint64_t nitems = rt.nrows * rt.ncol_tiles;
@@ -1242,7 +1252,7 @@ __device__ __forceinline__ void cq_unit(const GridDev& g, const GridDev& gc, con
 }
 
 template <int D, typename T, typename Z>
-__global__ void __launch_bounds__(kBoxThreads, MGRC_BOX_MINB) k_cq_warp(GridDev g, GridDev gc, RowTiling rt, Widths W, double inv,
+__global__ void __launch_bounds__(kBoxThreads, box_minb<D>()) k_cq_warp(GridDev g, GridDev gc, RowTiling rt, Widths W, double inv,
                                                            const T* __restrict__ u, double* __restrict__ ec,
                                                            Z* __restrict__ zc, QuantFlags* flags,
                                                            unsigned long long* queue) {
