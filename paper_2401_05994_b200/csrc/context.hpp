@@ -120,6 +120,7 @@ class Context {
   bool own_stream = false;
   bool profiling = false;
   std::vector<PhaseTime> profile;
+  std::vector<cudaEvent_t> event_pool;  // timing events reused by Prof (creating them per call costs ~µs each)
   // workspace
   DevBuf ssmaps;
   PinnedBuf ssmaps_h;
@@ -137,6 +138,7 @@ class Context {
   Scratch* sh() { return scratch_h.get<Scratch>(sizeof(Scratch)); }
 
   ~Context() {
+    for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
     if (aux) cudaStreamDestroy(aux);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_crc) cudaEventDestroy(ev_crc);
@@ -154,8 +156,8 @@ class Prof {
     Rec r;
     r.name = name;
     r.bytes = bytes;
-    cudaEventCreate(&r.a);
-    cudaEventCreate(&r.b);
+    r.a = take();
+    r.b = take();
     cudaEventRecord(r.a, c_.stream);
     recs_.push_back(r);
   }
@@ -170,12 +172,22 @@ class Prof {
       float ms = 0;
       cudaEventElapsedTime(&ms, r.a, r.b);
       c_.profile.push_back({r.name, ms, r.bytes});
-      cudaEventDestroy(r.a);
-      cudaEventDestroy(r.b);
+      c_.event_pool.push_back(r.a);
+      c_.event_pool.push_back(r.b);
     }
   }
 
  private:
+  cudaEvent_t take() {
+    if (c_.event_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = c_.event_pool.back();
+    c_.event_pool.pop_back();
+    return e;
+  }
   struct Rec {
     std::string name;
     double bytes;
