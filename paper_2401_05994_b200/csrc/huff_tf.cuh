@@ -21,8 +21,9 @@
 //                   scan composes the maps across the tile;
 //   K2 k_tfd_tiles  one CTA scans the tile maps: the true entry of every tile
 //                   (tile 0 starts at bit 0);
-//   K3 k_tfd_count  every lane decodes its subsequence once along the true
-//                   path: varint terminators, and whether it ends inside one;
+//   K3 k_tfd_count  the true path's terminator count and open-varint flag,
+//                   gathered from K1's per-entry records (K1 counts
+//                   terminators per cursor as it decodes);
 //   K4 k_scan_lb    exclusive scan of the terminator counts: value offsets;
 //   K5 k_tfd_emit   every lane decodes its subsequence again and writes the
 //                   zigzag codes of the varints that start in it (an open value
@@ -101,30 +102,40 @@ __device__ __forceinline__ void tfd_stage(const uint32_t* __restrict__ w, uint64
 #endif
 constexpr uint32_t kTfdMergeBits = MGRC_TFD_MERGE_BITS;
 
-// walk one parse from p to its exit (>= end); ~0u: it ran into the stream end
+// Walk one parse from p to its exit (>= end); ~0u: it ran into the stream end.
+// nt: terminators of the codewords walked; last: the last codeword's entry (0: none).
 template <bool NEAR_END, class LT>
 __device__ __forceinline__ uint32_t tfd_walk(const uint32_t* sm, const LT& lut, int maxlen, uint32_t p, uint32_t end,
-                                             uint32_t tl) {
+                                             uint32_t tl, uint32_t& nt, uint32_t& last) {
   BitReader br;
   br.init(sm, p);
   if (!NEAR_END) {  // no codeword can run past the stream end: two per refill
     while (p < end) {
       br.refill();
-      uint32_t l = lut_len(lut[br.peek(maxlen)]);
+      uint32_t ent = lut[br.peek(maxlen)];
+      uint32_t l = lut_len(ent);
       p += l;
+      nt += lut_term(ent);
+      last = ent;
       br.consume(l);
       if (p >= end) break;
-      l = lut_len(lut[br.peek(maxlen)]);
+      ent = lut[br.peek(maxlen)];
+      l = lut_len(ent);
       p += l;
+      nt += lut_term(ent);
+      last = ent;
       br.consume(l);
     }
     return p;
   }
   while (p < end) {
     br.refill();
-    const uint32_t l = lut_len(lut[br.peek(maxlen)]);
+    const uint32_t ent = lut[br.peek(maxlen)];
+    const uint32_t l = lut_len(ent);
     if (p + l > tl) return ~0u;
     p += l;
+    nt += lut_term(ent);
+    last = ent;
     br.consume(l);
   }
   return p;
@@ -132,13 +143,21 @@ __device__ __forceinline__ uint32_t tfd_walk(const uint32_t* sm, const LT& lut, 
 
 // The merging part: returns the live cursors (nibble map r over [base, base +
 // 16)) and the union-find parents; the survivors are walked by the warp.
+//
+// Terminator counts ride along (the value offsets, replacing a second decode
+// of the stream): cnt[id] (shared memory, one int16 per (id, lane)) counts the
+// terminators cursor id decoded; when id merges into the cursor it met, its
+// counter becomes the difference to that cursor's count at the meeting point,
+// so an entry's count is the root's final count plus the differences along
+// its union-find path.  `last` holds, per id, whether its last codeword was a
+// terminator (bit id) and whether it decoded any (bit 16 + id).
 struct TfdCursors {
   unsigned long long r, parent;
-  uint32_t base;
+  uint32_t base, last;
 };
 template <bool NEAR_END, class LT>
 __device__ __forceinline__ TfdCursors tfd_merge(const uint32_t* sm, const LT& lut, int maxlen, int ne, uint32_t S,
-                                                uint32_t end, uint32_t tl) {
+                                                uint32_t end, uint32_t tl, int16_t* cnt) {
   uint32_t base = S;
   unsigned long long r = 0;
   for (int e = 0; e < ne; ++e) r |= static_cast<unsigned long long>(e + 1) << (4 * e);
@@ -146,20 +165,30 @@ __device__ __forceinline__ TfdCursors tfd_merge(const uint32_t* sm, const LT& lu
   uint32_t occ = (1u << ne) - 1u;  // bit i: a cursor at base + i (mirror of r's nonzero nibbles)
   BitReader br;
   br.init(sm, base);
+  uint32_t last = 0;
+  for (int e = 0; e < ne; ++e) cnt[32 * e] = 0;
   const uint32_t mend = min(end, S + kTfdMergeBits);
   while ((occ & (occ - 1u)) && base < mend) {
     const uint32_t id = static_cast<uint32_t>(r) & 15u;
     br.refill();
-    const uint32_t l = lut_len(lut[br.peek(maxlen)]);
+    const uint32_t ent = lut[br.peek(maxlen)];
+    const uint32_t l = lut_len(ent);
     r &= ~15ull;
     occ &= ~1u;
     if (NEAR_END && base + l > tl) {
-      // the stream ends inside this codeword: the cursor dies
-    } else if ((occ >> l) & 1u) {  // two parses met: merge
-      parent = nib_set(parent, id - 1u, (static_cast<uint32_t>(r >> (4u * l)) & 15u) - 1u);
+      // the stream ends inside this codeword: the cursor dies (its count and last codeword stand)
     } else {
-      r |= static_cast<unsigned long long>(id) << (4u * l);
-      occ |= 1u << l;
+      const uint32_t t = lut_term(ent);
+      if (t) ++cnt[32 * (id - 1u)];
+      last = (last & ~(1u << (id - 1u))) | (t << (id - 1u)) | (1u << (15u + id));
+      if ((occ >> l) & 1u) {  // two parses met: merge (counter -> difference to the met cursor's)
+        const uint32_t other = (static_cast<uint32_t>(r >> (4u * l)) & 15u) - 1u;
+        parent = nib_set(parent, id - 1u, other);
+        cnt[32 * (id - 1u)] -= cnt[32 * other];
+      } else {
+        r |= static_cast<unsigned long long>(id) << (4u * l);
+        occ |= 1u << l;
+      }
     }
     if (!occ) break;
     const uint32_t sh = static_cast<uint32_t>(__ffs(static_cast<int>(occ)) - 1);
@@ -168,7 +197,7 @@ __device__ __forceinline__ TfdCursors tfd_merge(const uint32_t* sm, const LT& lu
     base += sh;
     br.consume(sh);
   }
-  return TfdCursors{r, parent, base};
+  return TfdCursors{r, parent, base, last};
 }
 
 // Survivor walks of a warp, balanced across its lanes: every lane queues its
@@ -183,6 +212,8 @@ constexpr uint32_t kTfdJobs = MGRC_TFD_JOBS;  // queued walks per warp
 struct TfdWarpQueue {
   unsigned long long job[kTfdJobs];
   uint8_t exit[32][16];
+  uint16_t tail[32][16];  // the walk's terminators | its last codeword was a terminator << 13 | decoded any << 14
+  int16_t cnt[16][32];    // per-cursor terminator counters (tfd_merge)
 };
 __device__ __forceinline__ unsigned long long tfd_job(uint32_t p, uint32_t end, uint32_t lane, uint32_t id, bool near) {
   return p | (static_cast<unsigned long long>(end) << 16) | (static_cast<unsigned long long>(lane) << 32) |
@@ -190,22 +221,28 @@ __device__ __forceinline__ unsigned long long tfd_job(uint32_t p, uint32_t end, 
 }
 template <class LT>
 __device__ __forceinline__ uint32_t tfd_walk_exit(const uint32_t* sm, const LT& lut, int maxlen, uint32_t p,
-                                                  uint32_t end, uint32_t tl, bool near) {
-  const uint32_t x = near ? tfd_walk<true>(sm, lut, maxlen, p, end, tl) : tfd_walk<false>(sm, lut, maxlen, p, end, tl);
+                                                  uint32_t end, uint32_t tl, bool near, uint32_t& tail) {
+  uint32_t nt = 0, last = 0;
+  const uint32_t x = near ? tfd_walk<true>(sm, lut, maxlen, p, end, tl, nt, last)
+                          : tfd_walk<false>(sm, lut, maxlen, p, end, tl, nt, last);
+  tail = nt | (last ? (lut_term(last) << 13) | (1u << 14) : 0u);
   return x == ~0u ? kDeadEx : min(x - end, 14u);
 }
 
 // Exit map of one subsequence [S, end) of every lane (live: it has a map to
-// compute); warp-synchronous.
+// compute); warp-synchronous.  rec (4 words): per entry e, 16 bits at 16e =
+// its parse's terminator count | (its last codeword continues a varint) << 15.
 template <class LT>
 __device__ __forceinline__ unsigned long long tfd_map_warp(const uint32_t* sm, const LT& lut, int maxlen, int ne,
                                                            uint32_t S, uint32_t end, uint32_t tl, bool live,
-                                                           TfdWarpQueue& wq, int lane) {
-  TfdCursors cs{0ull, kNibId, S};
-  if (live) cs = end + 32 >= tl ? tfd_merge<true>(sm, lut, maxlen, ne, S, end, tl)
-                                : tfd_merge<false>(sm, lut, maxlen, ne, S, end, tl);
+                                                           TfdWarpQueue& wq, int lane, unsigned long long* rec) {
+  int16_t* cnt = &wq.cnt[0][lane];
+  TfdCursors cs{0ull, kNibId, S, 0u};
+  if (live) cs = end + 32 >= tl ? tfd_merge<true>(sm, lut, maxlen, ne, S, end, tl, cnt)
+                                : tfd_merge<false>(sm, lut, maxlen, ne, S, end, tl, cnt);
   const bool near = end + 32 >= tl;
   unsigned long long exit_of = ~0ull;  // id -> exit offset (15: dead)
+  uint32_t last = cs.last;
   uint32_t nj = 0;  // cursors still before the end
   {
     uint32_t i = 0;
@@ -219,6 +256,11 @@ __device__ __forceinline__ unsigned long long tfd_map_warp(const uint32_t* sm, c
   }
   const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
   off -= nj;
+  // a survivor's walk adds its terminators to the cursor's counter and may replace its last codeword
+  auto add_tail = [&](uint32_t id0, uint32_t tail) {
+    cnt[32 * id0] += static_cast<int16_t>(tail & 0x1FFFu);
+    if (tail & (1u << 14)) last = (last & ~(1u << id0)) | (((tail >> 13) & 1u) << id0) | (1u << (16u + id0));
+  };
   {
     uint32_t q = off, i = 0;
     for (unsigned long long r = cs.r; r; r >>= 4, ++i) {
@@ -229,8 +271,13 @@ __device__ __forceinline__ unsigned long long tfd_map_warp(const uint32_t* sm, c
         exit_of = nib_set(exit_of, id - 1u, min(p - end, 14u));
         continue;
       }
-      if (q < kTfdJobs) wq.job[q] = tfd_job(p, end, static_cast<uint32_t>(lane), id - 1u, near);
-      else exit_of = nib_set(exit_of, id - 1u, tfd_walk_exit(sm, lut, maxlen, p, end, tl, near));
+      if (q < kTfdJobs) {
+        wq.job[q] = tfd_job(p, end, static_cast<uint32_t>(lane), id - 1u, near);
+      } else {
+        uint32_t tail;
+        exit_of = nib_set(exit_of, id - 1u, tfd_walk_exit(sm, lut, maxlen, p, end, tl, near, tail));
+        add_tail(id - 1u, tail);
+      }
       ++q;
     }
   }
@@ -239,8 +286,10 @@ __device__ __forceinline__ unsigned long long tfd_map_warp(const uint32_t* sm, c
   for (uint32_t q = lane; q < nq; q += 32) {
     const unsigned long long jb = wq.job[q];
     const uint32_t p = static_cast<uint32_t>(jb) & 0xFFFFu, e = static_cast<uint32_t>(jb >> 16) & 0xFFFFu;
-    wq.exit[(jb >> 32) & 31u][(jb >> 37) & 15u] =
-        static_cast<uint8_t>(tfd_walk_exit(sm, lut, maxlen, p, e, tl, (jb >> 41) & 1u));
+    const uint32_t jl = (jb >> 32) & 31u, jid = (jb >> 37) & 15u;
+    uint32_t tail;
+    wq.exit[jl][jid] = static_cast<uint8_t>(tfd_walk_exit(sm, lut, maxlen, p, e, tl, (jb >> 41) & 1u, tail));
+    wq.tail[jl][jid] = static_cast<uint16_t>(tail);
   }
   __syncwarp();
   {
@@ -249,16 +298,34 @@ __device__ __forceinline__ unsigned long long tfd_map_warp(const uint32_t* sm, c
       const uint32_t id = static_cast<uint32_t>(r) & 15u;
       if (!id) continue;
       if (cs.base + i >= end) continue;
-      if (q < kTfdJobs) exit_of = nib_set(exit_of, id - 1u, wq.exit[lane][id - 1u]);
+      if (q < kTfdJobs) {
+        exit_of = nib_set(exit_of, id - 1u, wq.exit[lane][id - 1u]);
+        add_tail(id - 1u, wq.tail[lane][id - 1u]);
+      }
       ++q;
     }
   }
-  __syncwarp();  // the queue is reused by the next call
   unsigned long long f = ~0ull;
-  for (int e = 0; e < ne; ++e) {
+  unsigned long long rw[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    if (e >= ne) break;
     uint32_t q = e;
-    for (uint32_t pq = nib(cs.parent, q); pq != q; pq = nib(cs.parent, q)) q = pq;
+    int32_t c = cnt[32 * e];
+    for (uint32_t pq = nib(cs.parent, q); pq != q; pq = nib(cs.parent, q)) {
+      q = pq;
+      c += cnt[32 * q];
+    }
     f = nib_set(f, e, nib(exit_of, q));
+    const uint32_t lc = ((last >> (16u + q)) & 1u) & (((last >> q) & 1u) ^ 1u);
+    rw[e >> 2] |= static_cast<unsigned long long>(static_cast<uint32_t>(c) | (lc << 15)) << (16u * (e & 3));
+  }
+  __syncwarp();  // the queue and the counters are reused by the next call
+  if (live && rec) {
+    rec[0] = rw[0];
+    rec[1] = rw[1];
+    rec[2] = rw[2];
+    rec[3] = rw[3];
   }
   return f;
 }
@@ -268,7 +335,8 @@ __device__ __forceinline__ unsigned long long tfd_map_warp(const uint32_t* sm, c
 template <bool G>
 static __global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
                                                           const uint16_t* __restrict__ lut_g, int maxlen, int ne,
-                                                          uint64_t nseq, unsigned long long* __restrict__ gmap) {
+                                                          uint64_t nseq, unsigned long long* __restrict__ gmap,
+                                                          unsigned long long* __restrict__ rec) {
   extern __shared__ uint32_t dyn[];
   __shared__ TfdWarpQueue wqs[kTfdThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -287,7 +355,7 @@ static __global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t*
   const uint32_t S = static_cast<uint32_t>(lane) * kSeqBits;
   const uint32_t end = min(S + static_cast<uint32_t>(kSeqBits), tl);
   // the last subsequence ends the stream (all dead); identity past it
-  const unsigned long long m = tfd_map_warp(sm, lut, maxlen, ne, S, end, tl, j + 1 < nseq, wqs[wid], lane);
+  const unsigned long long m = tfd_map_warp(sm, lut, maxlen, ne, S, end, tl, j < nseq, wqs[wid], lane, rec + 4 * j);
   unsigned long long g = j < nseq ? (j + 1 < nseq ? m : ~0ull) : kNibId;
 #pragma unroll
   for (int d = 1; d < kTfdTile; d <<= 1) {
@@ -326,42 +394,24 @@ static __global__ void __launch_bounds__(kTfdScanThreads) k_tfd_tiles(const unsi
   }
 }
 
-// K3: decode every subsequence once along the true path: terminators (for the
-// value offsets) and whether it ends inside a varint.
-template <bool G>
-static __global__ void __launch_bounds__(kTfdThreads) k_tfd_count(const uint32_t* __restrict__ w, uint64_t nw, uint64_t T,
-                                                           const uint16_t* __restrict__ lut_g, int maxlen,
-                                                           uint64_t nseq, const unsigned long long* __restrict__ gmap,
-                                                           const uint8_t* __restrict__ etile, TfdSeq* __restrict__ seqs,
-                                                           unsigned long long* __restrict__ cnt) {
-  extern __shared__ uint32_t dyn[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint16_t* lut_s = reinterpret_cast<uint16_t*>(dyn + (kTfdThreads / 32) * kTfdWarpSmem);
-  uint32_t* sm = dyn + wid * kTfdWarpSmem;
-  if (!G)
-    for (int k = threadIdx.x; k < (1 << maxlen); k += kTfdThreads) lut_s[k] = lut_g[k];
-  __syncthreads();
-  const Lut<G> lut{G ? lut_g : lut_s};
-  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * (kTfdThreads / 32) + wid;
-  if (c * kTfdTile >= nseq) return;
-  const uint64_t base = c * kTfdTile * kSeqBits;
-  tfd_stage(w, nw, base, sm, lane);
-  const uint64_t j = c * kTfdTile + lane;
+// K3: the true path through every subsequence: entry and exit from the maps,
+// terminator count and open-varint flag from the maps pass's per-entry records.
+static __global__ void __launch_bounds__(256) k_tfd_count(uint64_t nseq, const unsigned long long* __restrict__ gmap,
+                                                          const uint8_t* __restrict__ etile,
+                                                          const unsigned long long* __restrict__ rec,
+                                                          TfdSeq* __restrict__ seqs, unsigned long long* __restrict__ cnt) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= nseq) return;
-  const uint32_t tl = static_cast<uint32_t>(umin64(T - base, 0x7FFFFFFFu));
-  const uint32_t S = static_cast<uint32_t>(lane) * kSeqBits;
+  const uint64_t c = j / kTfdTile;
   const uint32_t e = etile[c];
-  const uint32_t entry = e == kDeadEx ? kDeadEx : (lane > 0 ? nib(gmap[j - 1], e) : e);
+  const uint32_t entry = e == kDeadEx ? kDeadEx : (j % kTfdTile ? nib(gmap[j - 1], e) : e);
   const uint32_t exo = e == kDeadEx ? kDeadEx : nib(gmap[j], e);
   TfdSeq q{static_cast<uint8_t>(entry), static_cast<uint8_t>(exo), 0, 0};
   uint32_t nterm = 0;
   if (entry != kDeadEx) {
-    const uint32_t ex = (j + 1 == nseq || exo == kDeadEx) ? tl : S + kSeqBits + exo;
-    BitReader br;
-    br.init(sm, S + entry);
-    uint32_t last = 0;
-    count_to(br, lut, maxlen, S + entry, ex, tl, nterm, last);
-    q.lc = last ? static_cast<uint8_t>(lut_term(last) ^ 1u) : 0;
+    const uint32_t r = static_cast<uint32_t>(rec[4 * j + (entry >> 2)] >> (16u * (entry & 3u))) & 0xFFFFu;
+    nterm = r & 0x7FFFu;
+    q.lc = static_cast<uint8_t>(r >> 15);
   }
   seqs[j] = q;
   cnt[j] = nterm;

@@ -1297,8 +1297,6 @@ static void huff_smem_optin() {
   const int mt = static_cast<int>(tfd_smem(kSmemLutMaxLen));
   CK(cudaFuncSetAttribute(k_tfd_maps<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   CK(cudaFuncSetAttribute(k_tfd_maps<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
-  CK(cudaFuncSetAttribute(k_tfd_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
-  CK(cudaFuncSetAttribute(k_tfd_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   CK(cudaFuncSetAttribute(k_tfd_emit<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   CK(cudaFuncSetAttribute(k_tfd_emit<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
   CK(cudaFuncSetAttribute(k_tfd_emit<unsigned long long, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mt));
@@ -1349,19 +1347,17 @@ static bool tfd_decode(Context& ctx, Prof& prof, const uint8_t* body, uint64_t b
           auto* lbticket = reinterpret_cast<unsigned int*>(lbst + nst);
           auto* first_err = reinterpret_cast<unsigned long long*>(lbst + nst + 2);
           prof.begin("huff_maps", static_cast<double>(body_len));
+          auto* rec = ctx.tfrec.get<unsigned long long>(nseq * 32);
           if (glut)
-            k_tfd_maps<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap);
+            k_tfd_maps<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap, rec);
           else
-            k_tfd_maps<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap);
+            k_tfd_maps<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap, rec);
           check_launch("k_tfd_maps");
           k_tfd_tiles<<<1, kTfdScanThreads, 0, s>>>(gmap, nseq, ntile, ne, etile);
           check_launch("k_tfd_tiles");
           prof.end();
           prof.begin("huff_count", static_cast<double>(body_len));
-          if (glut)
-            k_tfd_count<true><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, gmap, etile, seqs, cnt);
-          else
-            k_tfd_count<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, nseq, gmap, etile, seqs, cnt);
+          k_tfd_count<<<static_cast<unsigned>((nseq + 255) / 256), 256, 0, s>>>(nseq, gmap, etile, rec, seqs, cnt);
           check_launch("k_tfd_count");
           CK(cudaMemsetAsync(lbst, 0, nst * 8 + 16, s));
           k_scan_lb<<<static_cast<unsigned>(nst), kScanThreads, 0, s>>>(cnt, toff, nseq, lbst, lbticket);
