@@ -234,6 +234,56 @@ __global__ void __launch_bounds__(kTfmThreads) k_inverse_rows(GridDev g, const d
   }
 }
 
+// The finest level of the L²-projection transform as rows: nodes tagged L
+// get v ∓ I(v) in place (forward: sub; inverse: add) — k_interp_level's
+// arithmetic for l = L with the row stencil of k_inverse_rows.
+template <int D>
+__global__ void __launch_bounds__(kTfmThreads) k_interp_rows(GridDev g, double* v, int sub) {
+  const uint32_t n_last = g.shape[D - 1];
+  const uint64_t nrows = g.N / n_last;
+  const int lane = threadIdx.x & 31;
+  const int L = g.L;
+  auto ld = [v](uint64_t off) { return v[off]; };
+  for (uint64_t row = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; row < nrows;
+       row += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    RowCorners<D> m;
+    row_corners<D>(g, row, L, m);
+    for (uint32_t k = lane; k < n_last; k += 32) {
+      const int lk = __ldg(g.ax[D - 1].lvl + k);
+      if (m.t_o < L && lk < L) continue;  // tag < L
+      const uint64_t n = m.own + k;
+      const double acc = row_interp<D>(g, m, k, lk == L, m.t_o == L, ld);
+      v[n] = sub ? __dsub_rn(v[n], acc) : __dadd_rn(v[n], acc);
+    }
+  }
+}
+
+// The dense level-L array of the correction (the full grid): v at the nodes tagged L, zero elsewhere.
+template <int D>
+__global__ void __launch_bounds__(kTfmThreads) k_l2_gather_rows(GridDev g, const double* __restrict__ v,
+                                                                 double* __restrict__ out) {
+  const uint32_t n_last = g.shape[D - 1];
+  const uint64_t nrows = g.N / n_last;
+  const int lane = threadIdx.x & 31;
+  const int L = g.L;
+  for (uint64_t row = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; row < nrows;
+       row += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+    int t_o = 0;
+    uint64_t q = row;
+#pragma unroll
+    for (int a = D - 2; a >= 0; --a) {
+      const uint64_t qq = q / g.shape[a];
+      t_o = max(t_o, static_cast<int>(__ldg(g.ax[a].lvl + (q - qq * g.shape[a]))));
+      q = qq;
+    }
+    const uint64_t own = row * n_last;
+    for (uint32_t k = lane; k < n_last; k += 32) {
+      const bool fine = t_o == L || __ldg(g.ax[D - 1].lvl + k) == L;
+      out[own + k] = fine ? v[own + k] : 0.0;
+    }
+  }
+}
+
 struct QuantOut {
   unsigned long long overflow, outliers;
 };
@@ -426,6 +476,11 @@ struct InterpLevel {
   template <int D>
   struct L {
     static void run(cudaStream_t s, const GridDev& g, const BoxDev& b, int l, int sub, double* v) {
+      if (l == g.L) {  // the finest level (7/8 of the nodes in 3-D): rows
+        k_interp_rows<D><<<blocks_for(g.N / g.shape[D - 1] * 32), kTfmThreads, 0, s>>>(g, v, sub);
+        check_launch("k_interp_rows");
+        return;
+      }
       k_interp_level<D><<<blocks_for(b.count), kTfmThreads, 0, s>>>(g, b, l, sub, v);
       check_launch("k_interp_level");
     }
@@ -435,6 +490,11 @@ struct L2Gather {
   template <int D>
   struct L {
     static void run(cudaStream_t s, const GridDev& g, const BoxDev& b, int l, const double* v, double* out) {
+      if (l == g.L) {
+        k_l2_gather_rows<D><<<blocks_for(g.N / g.shape[D - 1] * 32), kTfmThreads, 0, s>>>(g, v, out);
+        check_launch("k_l2_gather_rows");
+        return;
+      }
       k_l2_gather<D><<<blocks_for(b.count), kTfmThreads, 0, s>>>(g, b, l, v, out);
       check_launch("k_l2_gather");
     }
