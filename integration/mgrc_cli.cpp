@@ -15,6 +15,7 @@
 // are rejected with an error.  Raw input is read straight into a page-locked
 // buffer (mgrc_gpu_host_alloc) so the host->device staging runs at PCIe rate.
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -27,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -136,6 +138,26 @@ struct HostBuf {
     else std::free(p);
   }
   uint8_t* data() { return static_cast<uint8_t*>(p); }
+};
+
+// A raw input file mapped read-only: the multiblock compress reads it block by
+// block in file order (the reference's read_block, mgrc.cpp:91-145), so host
+// memory stays bounded by the page cache instead of holding the whole file.
+struct MappedFile {
+  void* p = MAP_FAILED;
+  uint64_t n = 0;
+  MappedFile(const std::string& path, uint64_t bytes) : n(bytes) {
+    const int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) raise(MGRC_E_IO_ERROR, "cannot read " + path);
+    p = ::mmap(nullptr, bytes, PROT_READ, MAP_PRIVATE, fd, 0);
+    ::close(fd);
+    if (p == MAP_FAILED) raise(MGRC_E_IO_ERROR, "cannot map " + path);
+    ::madvise(p, bytes, MADV_SEQUENTIAL);
+  }
+  ~MappedFile() {
+    if (p != MAP_FAILED) ::munmap(p, n);
+  }
+  const uint8_t* data() const { return static_cast<const uint8_t*>(p); }
 };
 
 void read_exact(const std::string& path, uint8_t* dst, uint64_t n) {
@@ -269,11 +291,22 @@ int run_compress(const Args& a) {
     for (auto& c : coords) cptr.push_back(c.data());
   }
   select_device(a);
-  HostBuf in(expect);
-  read_exact(input, in.data(), expect);
+  // one container: the whole array is uploaded, read it into pinned memory (PCIe rate); several blocks:
+  // stream them from the mapped file
+  std::unique_ptr<HostBuf> whole;
+  std::unique_ptr<MappedFile> mapped;
+  const uint8_t* src = nullptr;
+  if (chunk_mem > 0 && expect > chunk_mem) {
+    mapped = std::make_unique<MappedFile>(input, expect);
+    src = mapped->data();
+  } else {
+    whole = std::make_unique<HostBuf>(expect);
+    read_exact(input, whole->data(), expect);
+    src = whole->data();
+  }
   uint8_t* out = nullptr;
   uint64_t out_len = 0;
-  check(mgrc_gpu_compress_chunked_multi(in.data(), dtype, static_cast<int>(shape.size()), shape.data(),
+  check(mgrc_gpu_compress_chunked_multi(src, dtype, static_cast<int>(shape.size()), shape.data(),
                                         cptr.empty() ? nullptr : cptr.data(), tol, norm, s, mode, codec, chunk_mem,
                                         gpus(a), &out, &out_len));
   const uint32_t nblocks = out_len >= 4 ? (uint32_t(out[0]) | uint32_t(out[1]) << 8 | uint32_t(out[2]) << 16 |
