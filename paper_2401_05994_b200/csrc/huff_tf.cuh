@@ -54,15 +54,32 @@ __device__ __forceinline__ uint32_t nib(unsigned long long m, uint32_t i) {
 __device__ __forceinline__ unsigned long long nib_set(unsigned long long m, uint32_t i, uint32_t v) {
   return (m & ~(15ull << (4u * i))) | (static_cast<unsigned long long>(v) << (4u * i));
 }
-// first f, then g (dead stays dead)
+// 4 nibbles (16 bits) -> 4 bytes
+__device__ __forceinline__ uint32_t nib4_to_bytes(uint32_t x) {
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  return (x | (x << 4)) & 0x0F0F0F0Fu;
+}
+// first f, then g: r[e] = g[f[e]], 16 table lookups as byte permutes (the low
+// 3 bits of f[e] pick among 8 bytes of g, its bit 3 the half).  Nibble 15 of
+// every map is 15 (dead), so dead stays dead; entries >= ne are not used.
 __device__ __forceinline__ unsigned long long nib_then(unsigned long long f, unsigned long long g, int ne) {
-  unsigned long long r = ~0ull;
+  (void)ne;
+  const uint32_t glo = static_cast<uint32_t>(g), ghi = static_cast<uint32_t>(g >> 32);
+  const uint32_t G0 = nib4_to_bytes(glo), G1 = nib4_to_bytes(glo >> 16);
+  const uint32_t G2 = nib4_to_bytes(ghi), G3 = nib4_to_bytes(ghi >> 16);
+  unsigned long long r = 0;
 #pragma unroll
-  for (int e = 0; e < 16; ++e)
-    if (e < ne) {
-      const uint32_t x = nib(f, e);
-      r = nib_set(r, e, x == kDeadEx ? kDeadEx : nib(g, x));
-    }
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t sx = static_cast<uint32_t>(f >> (16 * i)) & 0xFFFFu;
+    const uint32_t sel = sx & 0x7777u;
+    const uint32_t lo = __byte_perm(G0, G1, sel), hi = __byte_perm(G2, G3, sel);
+    const uint32_t mask = nib4_to_bytes((sx & 0x8888u) >> 3) * 0xFFu;
+    uint32_t b = (lo & ~mask) | (hi & mask);  // 4 result bytes, each < 16
+    b = (b | (b >> 4)) & 0x00FF00FFu;
+    b = (b | (b >> 8)) & 0xFFFFu;
+    r |= static_cast<unsigned long long>(b) << (16 * i);
+  }
   return r;
 }
 
