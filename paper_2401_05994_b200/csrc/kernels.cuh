@@ -220,14 +220,27 @@ static __global__ void __launch_bounds__(256) k_stats(const T* __restrict__ u, u
   unsigned bad = 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t n4 = vec_ok ? n / 4 : 0;
-  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n4; k += stride) {
-    double v[4];
-    load4<T>(u + 4 * k, v);
+  if constexpr (sizeof(T) == 4) {  // f32: min / max in single precision (the widening is monotone and exact)
+    float fmn = __int_as_float(0x7f800000), fmx = -fmn;
+    const float4* u4 = reinterpret_cast<const float4*>(u);
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n4; k += stride) {
+      const float4 a = __ldg(u4 + k);
+      bad |= !isfinite(a.x) | !isfinite(a.y) | !isfinite(a.z) | !isfinite(a.w);
+      fmn = fminf(fminf(fmn, a.x), fminf(a.y, fminf(a.z, a.w)));
+      fmx = fmaxf(fmaxf(fmx, a.x), fmaxf(a.y, fmaxf(a.z, a.w)));
+    }
+    mn = static_cast<double>(fmn);
+    mx = static_cast<double>(fmx);
+  } else {
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n4; k += stride) {
+      double v[4];
+      load4<T>(u + 4 * k, v);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      bad |= !isfinite(v[j]);
-      mn = fmin(mn, v[j]);
-      mx = fmax(mx, v[j]);
+      for (int j = 0; j < 4; ++j) {
+        bad |= !isfinite(v[j]);
+        mn = fmin(mn, v[j]);
+        mx = fmax(mx, v[j]);
+      }
     }
   }
   for (uint64_t k = 4 * n4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += stride) {
