@@ -125,6 +125,7 @@ class Context {
   DevBuf ssmaps;
   PinnedBuf ssmaps_h;
   DevBuf in, zz, zc, r, e, v, bits, tiles, scan, seq, lut, codes, crc_tab, crc_a, crc_b, partial, lbws, tfst, tftab;
+  DevBuf tftab2;  // decoder: per-tile prefix maps within their group, then the group maps
   DevBuf tfrec;  // decoder: per-subsequence, per-entry terminator counts (k_tfd_maps -> k_tfd_count)
   DevBuf l2a, l2b;  // dense level arrays of the L²-projection correction
   DevBuf scratch_d;

@@ -10,7 +10,7 @@
 // found by a scan — no serial chains, however long a stream stays out of
 // phase (periodic stretches keep parses desynchronised for megabits).
 //
-// Five launches; the three stream passes give each warp a tile of kTfdTile
+// Six launches; the three stream passes give each warp a tile of kTfdTile
 // consecutive subsequences staged in shared memory (coalesced, byte-swapped):
 //   K1 k_tfd_maps   every lane evaluates its subsequence's map: one cursor per
 //                   entry, always advancing the smallest position, so all live
@@ -19,8 +19,9 @@
 //                   some step and merge (union-find on 4-bit cursor ids, all in
 //                   registers); a lone cursor finishes by a plain walk; a warp
 //                   scan composes the maps across the tile;
-//   K2 k_tfd_tiles  one CTA scans the tile maps: the true entry of every tile
-//                   (tile 0 starts at bit 0);
+//   K2 k_tfd_tiles  scans the tile maps in groups of 256 tiles, and
+//      k_tfd_groups one CTA scans the group maps: the true entry of every
+//                   group (tile 0 starts at bit 0), hence of every tile;
 //   K3 k_tfd_count  the true path's terminator count and open-varint flag,
 //                   gathered from K1's per-entry records (K1 counts
 //                   terminators per cursor as it decodes);
@@ -382,20 +383,56 @@ static __global__ void __launch_bounds__(kTfdThreads) k_tfd_maps(const uint32_t*
   if (j < nseq) gmap[j] = g;
 }
 
-// K2 (one CTA): the true entry of every tile.  Each thread composes the tile
+// K2: the true entry of every tile, in two launches.  K2a: each CTA scans the
+// maps of kTfdGroup consecutive tiles (warp shuffles, then the warp
+// aggregates): tpre[i] = map of the tiles [group start, i]; gagg = the
+// group's map.  K2b (one CTA) scans the group maps: each thread composes the
 // maps of its chunk, a block scan combines the chunks, and each thread walks
-// its chunk from the true entry (tile 0 starts at offset 0).
-constexpr int kTfdScanThreads = 1024;
-static __global__ void __launch_bounds__(kTfdScanThreads) k_tfd_tiles(const unsigned long long* __restrict__ gmap,
+// its chunk from the true entry (group 0 starts at offset 0) — gentry[g].
+// K3 then reads a tile's entry as tpre[i-1] applied to its group's entry.
+constexpr int kTfdGroup = 256;
+static __global__ void __launch_bounds__(kTfdGroup) k_tfd_tiles(const unsigned long long* __restrict__ gmap,
                                                                uint64_t nseq, uint64_t ntile, int ne,
-                                                               uint8_t* __restrict__ etile) {
+                                                               unsigned long long* __restrict__ tpre,
+                                                               unsigned long long* __restrict__ gagg) {
+  __shared__ unsigned long long wagg[kTfdGroup / 32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kTfdGroup + t;
+  unsigned long long m = i < ntile ? gmap[umin64(i * kTfdTile + kTfdTile - 1, nseq - 1)] : kNibId;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long h = __shfl_up_sync(0xffffffffu, m, d);
+    if (lane >= d) m = nib_then(h, m, ne);
+  }
+  if (lane == 31) wagg[wid] = m;
+  __syncthreads();
+  if (wid == 0) {  // exclusive prefixes of the warp aggregates
+    unsigned long long x = lane < kTfdGroup / 32 ? wagg[lane] : kNibId;
+#pragma unroll
+    for (int d = 1; d < kTfdGroup / 32; d <<= 1) {
+      const unsigned long long h = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x = nib_then(h, x, ne);
+    }
+    const unsigned long long ex = __shfl_up_sync(0xffffffffu, x, 1);
+    __syncwarp();
+    if (lane < kTfdGroup / 32) wagg[lane] = lane ? ex : kNibId;
+  }
+  __syncthreads();
+  if (wid) m = nib_then(wagg[wid], m, ne);
+  if (i < ntile) tpre[i] = m;
+  if (t == kTfdGroup - 1) gagg[blockIdx.x] = m;  // identity past the last tile
+}
+
+constexpr int kTfdScanThreads = 1024;
+static __global__ void __launch_bounds__(kTfdScanThreads) k_tfd_groups(const unsigned long long* __restrict__ gagg,
+                                                                uint64_t ngroup, int ne,
+                                                                uint8_t* __restrict__ gentry) {
   __shared__ unsigned long long sm[kTfdScanThreads];
   const int t = threadIdx.x;
-  const uint64_t per = (ntile + kTfdScanThreads - 1) / kTfdScanThreads;
-  const uint64_t a = umin64(ntile, t * per), b = umin64(ntile, a + per);
-  auto tile_agg = [&](uint64_t i) { return gmap[umin64(i * kTfdTile + kTfdTile - 1, nseq - 1)]; };
+  const uint64_t per = (ngroup + kTfdScanThreads - 1) / kTfdScanThreads;
+  const uint64_t a = umin64(ngroup, t * per), b = umin64(ngroup, a + per);
   unsigned long long f = kNibId;
-  for (uint64_t i = a; i < b; ++i) f = nib_then(f, tile_agg(i), ne);
+  for (uint64_t i = a; i < b; ++i) f = nib_then(f, gagg[i], ne);
   sm[t] = f;
   __syncthreads();
   for (int d = 1; d < kTfdScanThreads; d <<= 1) {  // inclusive Hillis-Steele
@@ -406,21 +443,23 @@ static __global__ void __launch_bounds__(kTfdScanThreads) k_tfd_tiles(const unsi
   }
   uint32_t e = t > 0 ? nib(sm[t - 1], 0) : 0u;
   for (uint64_t i = a; i < b; ++i) {
-    etile[i] = static_cast<uint8_t>(e);
-    if (e != kDeadEx) e = nib(tile_agg(i), e);
+    gentry[i] = static_cast<uint8_t>(e);
+    if (e != kDeadEx) e = nib(gagg[i], e);
   }
 }
 
 // K3: the true path through every subsequence: entry and exit from the maps,
 // terminator count and open-varint flag from the maps pass's per-entry records.
 static __global__ void __launch_bounds__(256) k_tfd_count(uint64_t nseq, const unsigned long long* __restrict__ gmap,
-                                                          const uint8_t* __restrict__ etile,
+                                                          const unsigned long long* __restrict__ tpre,
+                                                          const uint8_t* __restrict__ gentry,
                                                           const unsigned long long* __restrict__ rec,
                                                           TfdSeq* __restrict__ seqs, unsigned long long* __restrict__ cnt) {
   const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= nseq) return;
   const uint64_t c = j / kTfdTile;
-  const uint32_t e = etile[c];
+  const uint32_t ge = gentry[c / kTfdGroup];
+  const uint32_t e = (ge == kDeadEx || c % kTfdGroup == 0) ? ge : nib(tpre[c - 1], ge);  // the tile's entry
   const uint32_t entry = e == kDeadEx ? kDeadEx : (j % kTfdTile ? nib(gmap[j - 1], e) : e);
   const uint32_t exo = e == kDeadEx ? kDeadEx : nib(gmap[j], e);
   TfdSeq q{static_cast<uint8_t>(entry), static_cast<uint8_t>(exo), 0, 0};

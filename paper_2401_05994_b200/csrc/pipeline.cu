@@ -1353,11 +1353,16 @@ static bool tfd_decode(Context& ctx, Prof& prof, const uint8_t* body, uint64_t b
           else
             k_tfd_maps<false><<<ncta, kTfdThreads, smem, s>>>(w, nw, T, lut, maxlen, ne, nseq, gmap, rec);
           check_launch("k_tfd_maps");
-          k_tfd_tiles<<<1, kTfdScanThreads, 0, s>>>(gmap, nseq, ntile, ne, etile);
+          const uint64_t ngroup = (ntile + kTfdGroup - 1) / kTfdGroup;
+          auto* tpre = ctx.tftab2.get<unsigned long long>((ntile + ngroup + 1) * 8);
+          auto* gagg = tpre + ntile;
+          k_tfd_tiles<<<static_cast<unsigned>(ngroup), kTfdGroup, 0, s>>>(gmap, nseq, ntile, ne, tpre, gagg);
           check_launch("k_tfd_tiles");
+          k_tfd_groups<<<1, kTfdScanThreads, 0, s>>>(gagg, ngroup, ne, etile);
+          check_launch("k_tfd_groups");
           prof.end();
           prof.begin("huff_count", static_cast<double>(body_len));
-          k_tfd_count<<<static_cast<unsigned>((nseq + 255) / 256), 256, 0, s>>>(nseq, gmap, etile, rec, seqs, cnt);
+          k_tfd_count<<<static_cast<unsigned>((nseq + 255) / 256), 256, 0, s>>>(nseq, gmap, tpre, etile, rec, seqs, cnt);
           check_launch("k_tfd_count");
           CK(cudaMemsetAsync(lbst, 0, nst * 8 + 16, s));
           k_scan_lb<<<static_cast<unsigned>(nst), kScanThreads, 0, s>>>(cnt, toff, nseq, lbst, lbticket);
