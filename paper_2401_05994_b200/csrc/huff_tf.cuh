@@ -233,6 +233,7 @@ struct TfdWarpQueue {
   uint16_t tail[32][16];  // the walk's terminators | its last codeword was a terminator << 13 | decoded any << 14
   int16_t cnt[16][32];    // per-cursor terminator counters (tfd_merge)
 };
+static_assert(kTfdTile * kSeqBits + 32 * kTailWords < (1 << 16), "walk jobs hold tile-local bit positions in 16 bits");
 __device__ __forceinline__ unsigned long long tfd_job(uint32_t p, uint32_t end, uint32_t lane, uint32_t id, bool near) {
   return p | (static_cast<unsigned long long>(end) << 16) | (static_cast<unsigned long long>(lane) << 32) |
          (static_cast<unsigned long long>(id) << 37) | (static_cast<unsigned long long>(near) << 41);
