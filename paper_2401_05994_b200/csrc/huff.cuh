@@ -74,44 +74,5 @@ struct BitReader {
   }
 };
 
-// Count codewords / varint terminators starting in [p, end); returns the exit.
-template <class LT>
-__device__ __forceinline__ uint32_t count_to(BitReader& br, const LT& lut, int maxlen, uint32_t p, uint32_t end,
-                                             uint32_t tl, uint32_t& nterm, uint32_t& last_ent) {
-  uint32_t nt = 0, last = 0;
-  if (end + 16 <= tl) {  // no codeword can run past the stream end: two symbols per refill
-    while (p < end) {
-      br.refill();
-      uint32_t ent = lut[br.peek(maxlen)];
-      uint32_t l = lut_len(ent);
-      p += l;
-      nt += lut_term(ent);
-      last = ent;
-      br.consume(l);
-      if (p >= end) break;
-      ent = lut[br.peek(maxlen)];
-      l = lut_len(ent);
-      p += l;
-      nt += lut_term(ent);
-      last = ent;
-      br.consume(l);
-    }
-  } else {
-    while (p < end) {
-      br.refill();
-      const uint32_t ent = lut[br.peek(maxlen)];
-      const uint32_t l = lut_len(ent);
-      if (p + l > tl) break;
-      p += l;
-      nt += lut_term(ent);
-      last = ent;
-      br.consume(l);
-    }
-  }
-  nterm = nt;
-  last_ent = last;
-  return p;
-}
-
 }  // namespace dev
 }  // namespace mgrc_gpu
