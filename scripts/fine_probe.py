@@ -19,5 +19,7 @@ for _ in range(7):
     except mg.MgrcError:
         pass
     ts.append({k: ms for k, ms, _ in mg.last_profile()})
-fine = sorted(t.get("fine", 0.0) for t in ts)[3]
-print(json.dumps({"tag": sys.argv[1] if len(sys.argv) > 1 else "", "fine_ms": round(fine, 4)}))
+import os
+ph = os.environ.get("PHASE", "fine")
+val = sorted(t.get(ph, 0.0) for t in ts)[3]
+print(json.dumps({"tag": sys.argv[1] if len(sys.argv) > 1 else "", ph + "_ms": round(val, 4)}))
