@@ -399,12 +399,26 @@ __global__ void __launch_bounds__(256) k_l2_line(L2Axis t, const double* __restr
   double* b = B + o * t.nc * inner + ii;
   // restriction + Thomas forward sweep: dp_q = (r_q - lo_q dp_{q-1}) / den_q
   double dp = 0.0;
+  uint32_t mk = ~0u;  // the last mass row computed (a fresh node between two coarse ones is needed twice)
+  double mv = 0.0;
+  auto mass = [&](uint32_t k) {
+    if (k != mk) {
+      mk = k;
+      mv = l2_mass(t, a, inner, k);
+    }
+    return mv;
+  };
   for (uint32_t q = 0; q < t.nc; ++q) {
     const uint32_t k = __ldg(t.kq + q);
-    double r = l2_mass(t, a, inner, k);
-    if (k > 0 && __ldg(t.fresh + k - 1)) r = __dadd_rn(r, __dmul_rn(__ldg(t.wr + k - 1), l2_mass(t, a, inner, k - 1)));
+    double r;
+    if (k > 0 && __ldg(t.fresh + k - 1)) {
+      const double ml = mass(k - 1);
+      r = __dadd_rn(l2_mass(t, a, inner, k), __dmul_rn(__ldg(t.wr + k - 1), ml));
+    } else {
+      r = l2_mass(t, a, inner, k);
+    }
     if (k + 1 < t.nl && __ldg(t.fresh + k + 1))
-      r = __dadd_rn(r, __dmul_rn(__ldg(t.wl + k + 1), l2_mass(t, a, inner, k + 1)));
+      r = __dadd_rn(r, __dmul_rn(__ldg(t.wl + k + 1), mass(k + 1)));
     dp = q == 0 ? __ddiv_rn(r, __ldg(t.den)) : __ddiv_rn(__dsub_rn(r, __dmul_rn(__ldg(t.clo + q), dp)), __ldg(t.den + q));
     b[q * inner] = dp;
   }
