@@ -335,3 +335,42 @@ def test_chunked_multi_rank(mg, oracle, case, ngpus):
     got = mg.compress_chunked(u, spec, mg.Codec.huffman, chunk_mem=cm, ngpus=ngpus)
     assert got == want
     assert np.array_equal(mg.decompress_chunked(got, ngpus=ngpus), mg.decompress_chunked(got))
+
+
+# ---------------------------------------------------------------------------
+# device-resident containers at every body alignment (the library copies the
+# body into its padded, aligned buffer): the host path's output and errors
+
+
+@pytest.mark.parametrize("case", [((65, 33, 17), "noisy", "f32", 1e-4), ((129, 130), "random", "f64", 1e-3),
+                                  ((33, 9, 8, 5), "noisy", "f64", 1e-2)], ids=lambda c: "x".join(map(str, c[0])))
+def test_device_containers_in_place_and_copied(mg, oracle, case):
+    import torch
+
+    shape, kind, dt, tol = case
+    u = make_field(oracle, kind, shape, dt)
+    blob = mg.compress(u, mg.make_grid(shape), mg.ErrorSpec(tol, mg.Norm.inf, 0.0, mg.Mode.rel))
+    want = mg.decompress(blob)
+    raw = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+    for shift in range(4):  # the body's alignment cycles through 0..3 bytes
+        buf = torch.zeros(len(blob) + shift + 256, dtype=torch.uint8, device="cuda")
+        dev = buf[shift:shift + len(blob)]
+        dev.copy_(raw.cuda())
+        out = torch.empty(shape, dtype=torch.float32 if dt == "f32" else torch.float64, device="cuda")
+        mg.decompress_into(dev, out)
+        assert np.array_equal(out.cpu().numpy(), want)
+        # a flipped bit in the body: the same error as the host path
+        bad = bytearray(blob)
+        bad[len(bad) - 20] ^= 0x10
+        try:
+            mg.decompress(bytes(bad))
+            host_err = None
+        except mg.MgrcError as e:
+            host_err = e.name
+        dev.copy_(torch.frombuffer(bad, dtype=torch.uint8).cuda())
+        try:
+            mg.decompress_into(dev, out)
+            dev_err = None
+        except mg.MgrcError as e:
+            dev_err = e.name
+        assert dev_err == host_err
