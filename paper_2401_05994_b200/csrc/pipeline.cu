@@ -2001,50 +2001,81 @@ MdrStore mdr_refactor(Context& ctx, const double* u, const Grid& grid, uint32_t 
     std::vector<unsigned long long> hh(static_cast<size_t>(planes) * 256);
     CK(cudaMemcpyAsync(hh.data(), hist, hh.size() * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    // the level's planes in one batch: code tables on the host, every plane packed into its own
+    // 16-byte aligned slot of one device buffer with its CRC computed on the device, one download
+    struct PlaneTab {
+      uint32_t codes[256];
+      uint8_t lens[256];
+    };
+    std::vector<CodeTable> tables(planes);
+    std::vector<PlaneTab> tabs(planes);
+    std::vector<uint64_t> nbytes(planes, 0), slot(planes + 1, 0);
     for (uint32_t p = 0; p < planes; ++p) {
+      tables[p] = build_code_table(reinterpret_cast<const uint64_t*>(hh.data() + p * 256));
+      if (tables[p].nsym >= 2) {
+        uint64_t total_bits = 0;
+        for (int b = 0; b < 256; ++b) {
+          total_bits += hh[p * 256 + b] * tables[p].lengths[b];
+          tabs[p].codes[b] = tables[p].codes[b];
+          tabs[p].lens[b] = tables[p].lengths[b];
+        }
+        nbytes[p] = (total_bits + 7) / 8;
+      }
+      slot[p + 1] = slot[p] + ((nbytes[p] + 8 + 15) & ~uint64_t{15});  // + the packer's word overrun
+    }
+    auto* dtabs = ctx.codes.get<PlaneTab>(sizeof(PlaneTab) * planes);
+    CK(cudaMemcpyAsync(dtabs, tabs.data(), sizeof(PlaneTab) * planes, cudaMemcpyHostToDevice, s));
+    auto* lvl = ctx.zz.get<uint8_t>(slot[planes] + 16);
+    CK(cudaMemsetAsync(lvl, 0, slot[planes] + 16, s));
+    auto* dcrc = ctx.tiles.get<uint32_t>(planes * 4 + 16);
+    {  // grow the CRC scratch to the largest plane first: no reallocation while launches are queued
+      uint64_t big = 0;
+      for (uint32_t p = 0; p < planes; ++p) big = std::max(big, nbytes[p]);
+      if (big) {
+        const CrcSlot c = device_crc_launch(ctx, lvl, big);
+        (void)c;
+      }
+    }
+    for (uint32_t p = 0; p < planes; ++p) {
+      if (!nbytes[p]) continue;
       const uint8_t* seg = raw + (p == 0 ? 0 : b0 + (p - 1) * b1);
       const uint64_t len = p == 0 ? b0 : b1;
+      const uint8_t* dtab = reinterpret_cast<const uint8_t*>(dtabs + p);
+      const uint64_t ntile = (len + kPbTile - 1) / kPbTile;
+      auto* tbits = ctx.tfst.get<unsigned long long>(ntile * 8 + 8);
+      auto* toff = ctx.tftab.get<unsigned long long>((ntile + 1) * 8);
+      k_pack_bytes_bits<<<static_cast<unsigned>(ntile), kPbThreads, 0, s>>>(seg, len, dtab + 1024, tbits);
+      check_launch("k_pack_bytes_bits");
+      const uint64_t nt = (ntile + kScanTile - 1) / kScanTile;
+      auto* lst = ctx.lbws.get<unsigned long long>(static_cast<size_t>(planes) * 256 * 8 + nt * 8 + 32);
+      auto* st2 = lst + static_cast<size_t>(planes) * 256;  // after the (consumed) histograms
+      auto* ticket = reinterpret_cast<unsigned int*>(st2 + nt);
+      CK(cudaMemsetAsync(st2, 0, nt * 8 + 16, s));
+      k_scan_lb<<<static_cast<unsigned>(nt), kScanThreads, 0, s>>>(tbits, toff, ntile, st2, ticket);
+      check_launch("k_scan_lb");
+      uint32_t* words = reinterpret_cast<uint32_t*>(lvl + slot[p]);
+      k_pack_bytes<<<static_cast<unsigned>(ntile), kPbThreads, 0, s>>>(
+          seg, len, reinterpret_cast<const uint32_t*>(dtab), dtab + 1024, toff, words);
+      check_launch("k_pack_bytes");
+      const CrcSlot c = device_crc_launch(ctx, lvl + slot[p], nbytes[p]);
+      CK(cudaMemcpyAsync(dcrc + p, c.crc, 4, cudaMemcpyDeviceToDevice, s));
+    }
+    std::vector<uint8_t> host_lvl(slot[planes]);
+    std::vector<uint32_t> crcs(planes, 0);
+    if (slot[planes]) CK(cudaMemcpyAsync(host_lvl.data(), lvl, slot[planes], cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(crcs.data(), dcrc, planes * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint32_t p = 0; p < planes; ++p) {
       // huffman_pack_bytes (codec.cpp:399-418): table header + MSB-first code stream
-      const CodeTable table = build_code_table(reinterpret_cast<const uint64_t*>(hh.data() + p * 256));
       std::vector<uint8_t> out;
-      write_table_header(out, table);
-      if (table.nsym >= 2) {
-        uint64_t total_bits = 0;
-        for (int b = 0; b < 256; ++b) total_bits += hh[p * 256 + b] * table.lengths[b];
-        struct {
-          uint32_t codes[256];
-          uint8_t lens[256];
-        } tab;
-        for (int b = 0; b < 256; ++b) tab.codes[b] = table.codes[b], tab.lens[b] = table.lengths[b];
-        auto* dtab = ctx.codes.get<uint8_t>(sizeof tab);
-        CK(cudaMemcpyAsync(dtab, &tab, sizeof tab, cudaMemcpyHostToDevice, s));
-        const uint64_t ntile = (len + kPbTile - 1) / kPbTile;
-        auto* tbits = ctx.tfst.get<unsigned long long>(ntile * 8 + 8);
-        auto* toff = ctx.tftab.get<unsigned long long>((ntile + 1) * 8);
-        k_pack_bytes_bits<<<static_cast<unsigned>(ntile), kPbThreads, 0, s>>>(seg, len, dtab + 1024, tbits);
-        check_launch("k_pack_bytes_bits");
-        const uint64_t nt = (ntile + kScanTile - 1) / kScanTile;
-        auto* lst = ctx.lbws.get<unsigned long long>(static_cast<size_t>(planes) * 256 * 8 + nt * 8 + 32);
-        auto* st2 = lst + static_cast<size_t>(planes) * 256;  // after the (consumed) histograms
-        auto* ticket = reinterpret_cast<unsigned int*>(st2 + nt);
-        CK(cudaMemsetAsync(st2, 0, nt * 8 + 16, s));
-        k_scan_lb<<<static_cast<unsigned>(nt), kScanThreads, 0, s>>>(tbits, toff, ntile, st2, ticket);
-        check_launch("k_scan_lb");
-        const uint64_t nbytes = (total_bits + 7) / 8;
-        auto* words = ctx.zz.get<uint32_t>(((total_bits + 31) / 32 + 2) * 4);
-        CK(cudaMemsetAsync(words, 0, ((total_bits + 31) / 32 + 2) * 4, s));
-        k_pack_bytes<<<static_cast<unsigned>(ntile), kPbThreads, 0, s>>>(
-            seg, len, reinterpret_cast<const uint32_t*>(dtab), dtab + 1024, toff, words);
-        check_launch("k_pack_bytes");
-        const size_t h = out.size();
-        out.resize(h + nbytes);
-        CK(cudaMemcpyAsync(out.data() + h, words, nbytes, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-      }
+      write_table_header(out, tables[p]);
+      const uint32_t hcrc = crc32_host(out.data(), out.size());
+      if (nbytes[p]) out.insert(out.end(), host_lvl.begin() + static_cast<std::ptrdiff_t>(slot[p]),
+                                host_lvl.begin() + static_cast<std::ptrdiff_t>(slot[p] + nbytes[p]));
       MdrSegment& sg = m.seg[l][p];
       sg.raw_bits = n * (p == 0 ? 2 : 1);
       sg.bytes = out.size();
-      sg.crc = crc32_host(out.data(), out.size());
+      sg.crc = nbytes[p] ? crc32_combine(hcrc, crcs[p], nbytes[p]) : hcrc;
       st.payload[l][p] = std::move(out);
     }
   }
