@@ -130,6 +130,7 @@ class Context {
   DevBuf l2a, l2b;  // dense level arrays of the L²-projection correction
   DevBuf scratch_d;
   PinnedBuf scratch_h, partial_h;
+  PinnedBuf mdr_h;  // MDR refactor: a level's packed planes on their way to the host
   std::vector<std::unique_ptr<DevHier>> hiers;  // most recently used first (chunked slabs alternate shapes)
   cudaStream_t aux = nullptr;            // concurrent side work (decompress CRC)
   cudaEvent_t ev_in = nullptr, ev_crc = nullptr;

@@ -2060,18 +2060,17 @@ MdrStore mdr_refactor(Context& ctx, const double* u, const Grid& grid, uint32_t 
       const CrcSlot c = device_crc_launch(ctx, lvl + slot[p], nbytes[p]);
       CK(cudaMemcpyAsync(dcrc + p, c.crc, 4, cudaMemcpyDeviceToDevice, s));
     }
-    std::vector<uint8_t> host_lvl(slot[planes]);
-    std::vector<uint32_t> crcs(planes, 0);
-    if (slot[planes]) CK(cudaMemcpyAsync(host_lvl.data(), lvl, slot[planes], cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(crcs.data(), dcrc, planes * 4, cudaMemcpyDeviceToHost, s));
+    uint8_t* host_lvl = ctx.mdr_h.get<uint8_t>(((slot[planes] + 15) & ~uint64_t{15}) + planes * 4 + 16);  // pinned: full PCIe rate
+    uint32_t* crcs = reinterpret_cast<uint32_t*>(host_lvl + ((slot[planes] + 15) & ~uint64_t{15}));
+    if (slot[planes]) CK(cudaMemcpyAsync(host_lvl, lvl, slot[planes], cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(crcs, dcrc, planes * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     for (uint32_t p = 0; p < planes; ++p) {
       // huffman_pack_bytes (codec.cpp:399-418): table header + MSB-first code stream
       std::vector<uint8_t> out;
       write_table_header(out, tables[p]);
       const uint32_t hcrc = crc32_host(out.data(), out.size());
-      if (nbytes[p]) out.insert(out.end(), host_lvl.begin() + static_cast<std::ptrdiff_t>(slot[p]),
-                                host_lvl.begin() + static_cast<std::ptrdiff_t>(slot[p] + nbytes[p]));
+      if (nbytes[p]) out.insert(out.end(), host_lvl + slot[p], host_lvl + slot[p] + nbytes[p]);
       MdrSegment& sg = m.seg[l][p];
       sg.raw_bits = n * (p == 0 ? 2 : 1);
       sg.bytes = out.size();
